@@ -1,0 +1,147 @@
+/*
+ * flmisr.h -- C ABI of the B200-native FL-MISR SCG reconstruction (arXiv 2108.04315).
+ *
+ * One call reconstructs one high-resolution (HR) projection x from K low-resolution (LR)
+ * projections y_i taken at sub-pixel detector shifts, by minimising the MAP objective
+ *
+ *     J(x) = sum_i || A_i x - y_i ||_p^p  +  lambda * sum_d gamma(d) || x - S_d x ||_1
+ *
+ * (Eq. objective; forward model y = A x + eps with A = D B M, Eq. sisr
+ * P:65-71; BTV prior Eq. prior) with Moller's scaled conjugate gradient (SCG, the
+ * [SCG] citation of P:186/P:206), run as in Algorithm 1: the HR image is
+ * row-partitioned over `world` GPUs (Eq. subfunction), SCG scalars are consensus sums
+ * of per-partition inner products (tab:parameters P:140-160), and partition borders
+ * are exchanged every iteration (inner-outer border exchange, fig:communication).
+ * The readings of everything the paper leaves open are in DESIGN.md section 3 ("reading k").
+ *
+ * Types are C99 only; pointers are plain host or device pointers as stated per argument.
+ * All entry points are thread-compatible (a plan must not be used from two threads at once;
+ * different plans may run concurrently on different streams).
+ */
+#ifndef FLMISR_H
+#define FLMISR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct flmisr_plan_s* flmisr_plan_t;
+
+typedef enum {
+    FLMISR_OK = 0,
+    FLMISR_ERR_CONFIG = -1,  /* invalid configuration (raised by flmisr_plan, before any GPU work)  */
+    FLMISR_ERR_SHAPE = -2,   /* argument shape / pointer error (raised before any launch)           */
+    FLMISR_ERR_CUDA = -3,    /* CUDA runtime error (message in flmisr_last_error)                   */
+    FLMISR_ERR_NCCL = -4,    /* NCCL error (multi-GPU)                                              */
+    FLMISR_ERR_NUMERIC = -5  /* non-finite consensus scalar: loop frozen on device   */
+} flmisr_status;
+
+typedef struct {
+    /* LR stack: k frames of lr_h x lr_w, fp32 row-major, intensities normalised to [0,1]
+     * (reading 20).  Requirements: k >= 1, lr_h, lr_w >= 1.                          */
+    int32_t k, lr_h, lr_w;
+    /* host, k x 2 doubles: detector shift (dy, dx) of frame i in LR pixels; frame i samples the
+     * HR image at HR position mag*(a,b) + mag*shift_i (reading 3: +dx = lattice moved right). */
+    const double* shifts;
+    /* host, psf_h x psf_w doubles, odd sizes <= 5, entries >= 0, sum 1 (+-1e-6); centred,
+     * applied as correlation on the HR grid (B of Eq. sisr; reading 2).                      */
+    const double* psf;
+    int32_t psf_h, psf_w;
+    int32_t mag;         /* SR factor r in [1, 4]; HR = (mag*lr_h) x (mag*lr_w) (D of Eq. sisr) */
+    int32_t p_norm;      /* 1: Charbonnier-smoothed L1 (the paper's choice); 2: squared L2 */
+    double l1_eps;       /* Charbonnier epsilon > 0 for the data term and BTV (reading 8); 1e-3  */
+    double lambda;       /* regularisation weight >= 0 (Eq. objective; 0.05 at P:271)           */
+    double btv_alpha;    /* 0 < alpha < 1, gamma(d) = alpha^(dx+dy) (Eq. prior; 0.4 at P:271)   */
+    int32_t btv_window;  /* w in [1, 3]: offsets dx, dy in [0, w-1] (Eq. prior, reading 6/7)   */
+    int32_t n_iter;      /* SCG loop passes incl. rejected ones (20 at P:271)      */
+    double scg_sigma0;   /* Moller sigma0; unused: curvature is exact (reading 16)      */
+    double scg_lambda0;  /* Moller initial scale lambda_1 > 0; 1e-6                      */
+    int32_t rank, world; /* row band `rank` of `world` partitions; world = 1: no NCCL    */
+    const void* nccl_unique_id; /* host, 128-byte ncclUniqueId (same on all ranks) or NULL if world == 1 */
+    int32_t device;      /* CUDA device ordinal for this rank                                    */
+} flmisr_config;
+
+typedef struct {
+    int32_t iters_run;    /* SCG loop passes executed (<= n_iter)                                 */
+    int32_t accepted;     /* passes whose step was accepted (runtime grows with these)     */
+    int32_t converged_at; /* pass at which <r,r> == 0 stopped the loop, or -1                     */
+    int32_t failed_stage; /* 0 none; 1 curvature/step, 2 value/accept (non-finite consensus)      */
+    int32_t failed_iter;  /* pass index of the numeric failure, or -1                             */
+    double* f_trace;      /* optional caller-owned host array of (n_iter+1)*6 doubles, or NULL:
+                             rows (k, f, <r,r>, alpha, lambda_scg, accepted); row 0 = init */
+} flmisr_report;
+
+/*
+ * flmisr_plan: validate `cfg`, derive the per-frame taps kappa_i = PSF (*) bilinear(frac(mag*shift_i))
+ * and integer phases, choose the polyphase fast path (K = mag^2 distinct phases in [0,mag)^2 with one
+ * common kappa), compute the row band and halo, allocate all device scratch on
+ * cfg->device and (world > 1) initialise the NCCL communicator from cfg->nccl_unique_id.
+ * Ownership: the plan copies everything it needs from cfg (shifts/psf may be freed afterwards).
+ * Errors: FLMISR_ERR_CONFIG for invalid parameters or an unsupported geometry (message names the
+ * violated rule, e.g. the minimum band height); FLMISR_ERR_CUDA / _NCCL for runtime failures.
+ * On error *out is set to NULL.  A plan is reusable for any number of projections.
+ */
+flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out);
+
+/*
+ * flmisr_reconstruct: run SCG for cfg.n_iter passes on one projection (Alg. 1).
+ *   lr_stack  device pointer, k x lr_h x lr_w fp32, full frames on every rank (read only).
+ *   x0        device pointer, H x W fp32 initial estimate, or NULL for the bilinear upsample of
+ *             frame 0 (reading 14).  Read only.
+ *   hr_out    device pointer, H x W fp32 (world == 1 or rank 0: the fused image, Alg. 1 line 24,
+ *             P:227); on other ranks rows of the owned band only are written (may be NULL).
+ *   cuda_stream  cudaStream_t to enqueue on, or NULL for the plan's own stream.
+ *   report    nullable; filled after the end-of-call stream synchronisation.
+ * Blocking: returns after the stream has drained (matches SPEC's function semantics).
+ * Returns FLMISR_ERR_NUMERIC when a consensus scalar became non-finite (the device froze the loop;
+ * hr_out then holds the last finite iterate), FLMISR_ERR_SHAPE on NULL required pointers.
+ */
+flmisr_status flmisr_reconstruct(flmisr_plan_t plan, const float* lr_stack, const float* x0, float* hr_out,
+                                 void* cuda_stream, flmisr_report* report);
+
+/*
+ * flmisr_reconstruct_host: flmisr_reconstruct for HOST buffers (end-to-end path): lr_stack_host
+ * (k x lr_h x lr_w fp32) is staged through the plan's pinned buffer and copied H2D, hr_out_host
+ * (H x W fp32; rank 0 / world 1) receives the D2H copy.  Same errors as flmisr_reconstruct.
+ */
+flmisr_status flmisr_reconstruct_host(flmisr_plan_t plan, const float* lr_stack_host, float* hr_out_host,
+                                      flmisr_report* report);
+
+/* flmisr_destroy: free all device memory, the CUDA graph, streams and the NCCL communicator.
+ * NULL is accepted.  Always returns FLMISR_OK unless a CUDA call fails. */
+flmisr_status flmisr_destroy(flmisr_plan_t plan);
+
+/* Thread-local message describing the last error returned on this thread ("" if none). */
+const char* flmisr_last_error(void);
+
+/* Fill out128 (128 bytes, host) with a fresh ncclUniqueId (rank 0 calls this and broadcasts the
+ * bytes to the other ranks, e.g. over the torch process group; S:288 coordinator role). */
+flmisr_status flmisr_nccl_unique_id(void* out128);
+
+/* HR geometry of a plan: H, W, owned rows [row_lo, row_hi), and whether the fast path is used. */
+flmisr_status flmisr_plan_info(flmisr_plan_t plan, int32_t* H, int32_t* W, int32_t* row_lo, int32_t* row_hi,
+                               int32_t* fast_path);
+
+/* ------------------------------------------------------------------------------------------
+ * Debug entry points (parity tests).  Each runs the SAME kernels as the SCG loop (for VALUE,
+ * GRAD and CURV) or shares their device stencil code (FORWARD, ADJOINT) on the plan's stream,
+ * synchronises, and returns.  All array arguments are device pointers (fp32), scalars host.
+ * ------------------------------------------------------------------------------------------ */
+typedef enum {
+    FLMISR_OP_FORWARD = 0, /* in0 = x (H x W)            -> out = A x as k x lr_h x lr_w frames          */
+    FLMISR_OP_ADJOINT = 1, /* in0 = w (k x lr_h x lr_w)  -> out = sum_i A_i^T w_i (H x W)                */
+    FLMISR_OP_GRAD = 2,    /* in0 = x, lr = y            -> out = -grad J(x) (H x W); s[0..1] = D, R      */
+    FLMISR_OP_CURV = 3,    /* in0 = x, in1 = p, lr = y   -> s[0] = p^T Hess J(x) p, s[1] = <p,p>          */
+    FLMISR_OP_VALUE = 4,   /* in0 = x, lr = y            -> s[0] = D(x), s[1] = R(x)  (J = D + lambda R)  */
+    FLMISR_OP_X0 = 5       /* lr = y                     -> out = bilinear initial estimate (H x W)       */
+} flmisr_op;
+
+flmisr_status flmisr_debug_apply(flmisr_plan_t plan, int32_t op, const float* lr_stack, const float* in0,
+                                 const float* in1, float* out, double* scalars_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLMISR_H */

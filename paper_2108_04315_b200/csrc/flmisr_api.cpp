@@ -1,0 +1,598 @@
+// flmisr_api.cpp -- C ABI (include/flmisr.h): plan validation and construction, device memory,
+// the SCG driver that enqueues one reconstruction, NCCL plumbing for row bands, debug entries.
+//
+// Host-side design: the plan derives the per-frame taps kappa_i =
+// PSF (*) bilinear(frac(mag*shift_i)) in fp64 (A_i = D B M_i, Eq. sisr), detects the
+// polyphase fast path, fixes the row band + halo of this rank (Eq. subfunction; halo eta =
+// max(2 KR, w-1), reading 17), and allocates every buffer once ("calculated once ... and
+// shared by all rotation angles").  flmisr_reconstruct enqueues the whole SCG loop; every SCG
+// decision is taken on the device (no host round-trip until the final synchronisation).
+#include "flmisr.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "flmisr_internal.h"
+
+using namespace flmisr;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+flmisr_status fail(flmisr_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (expr);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return fail(FLMISR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+// ---- NCCL through dlopen (the torch-bundled libnccl.so.2 is already mapped in torch processes) ----
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+    api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+    api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.ok = api.CommInitRank && api.CommDestroy && api.AllGather && api.Send && api.Recv && api.GroupStart &&
+             api.GroupEnd && api.GetErrorString;
+    return api;
+}
+
+#define NCCL_TRY(expr)                                                                              \
+    do {                                                                                            \
+        ncclResult_t r_ = (expr);                                                                   \
+        if (r_ != ncclSuccess)                                                                      \
+            return fail(FLMISR_ERR_NCCL, std::string(#expr) + ": " + nccl().GetErrorString(r_));   \
+    } while (0)
+
+}  // namespace
+
+struct flmisr_plan_s {
+    flmisr_config cfg{};
+    std::vector<double> shifts, psf;
+    int H = 0, W = 0, pitch = 0, kr = 0, bw = 0, pn = 1, eta = 0;
+    int row_lo = 0, row_hi = 0, store_lo = 0, store_hi = 0;
+    int fast = 0;
+    StencilParams sp{};
+    IngestParams ip{};
+    Buffers b{};
+    size_t hr_bytes = 0;     // bytes of one stored HR buffer
+    float* mem = nullptr;    // one allocation for all HR buffers
+    double* dmem = nullptr;  // partials + rank sums + trace + gathered
+    ScgState* st = nullptr;
+    ScgState* st_host = nullptr;  // pinned
+    double* trace_host = nullptr; // pinned
+    float* pin_in = nullptr;      // pinned staging for the host entry point
+    float* pin_out = nullptr;
+    float* d_lr = nullptr;        // device LR stack for the host entry point
+    float* d_out = nullptr;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    float* recv_top = nullptr;
+    float* recv_bot = nullptr;
+    double* gathered = nullptr;
+};
+
+namespace {
+
+bool is_odd(int v) { return v > 0 && (v & 1); }
+
+// kappa_i = h (*) b_phi on offsets P in [-R, R+1] x [-R, R+1] (A_i = D B M_i, reading 19).
+void composed_taps(const flmisr_config& c, int i, std::vector<double>& kap, int& sy, int& sx, double& fy,
+                   double& fx) {
+    double ty = c.mag * c.shifts[2 * i], tx = c.mag * c.shifts[2 * i + 1];
+    double fsy = std::floor(ty), fsx = std::floor(tx);
+    sy = (int)fsy; sx = (int)fsx;
+    fy = ty - fsy; fx = tx - fsx;
+    int ry = c.psf_h / 2, rx = c.psf_w / 2, R = std::max(ry, rx);
+    int KD = 2 * R + 2;
+    kap.assign((size_t)KD * KD, 0.0);
+    double bw[2][2] = {{(1 - fy) * (1 - fx), (1 - fy) * fx}, {fy * (1 - fx), fy * fx}};
+    for (int P = -ry; P <= ry; ++P)
+        for (int Q = -rx; Q <= rx; ++Q) {
+            double h = c.psf[(P + ry) * c.psf_w + (Q + rx)];
+            for (int a = 0; a < 2; ++a)
+                for (int bb = 0; bb < 2; ++bb) kap[(size_t)(P + a + R) * KD + (Q + bb + R)] += h * bw[a][bb];
+        }
+}
+
+flmisr_status validate(const flmisr_config* c) {
+    if (!c) return fail(FLMISR_ERR_CONFIG, "config is NULL");
+    if (c->k < 1) return fail(FLMISR_ERR_CONFIG, "k must be >= 1 (S:96)");
+    if (c->lr_h < 1 || c->lr_w < 1) return fail(FLMISR_ERR_CONFIG, "lr_h and lr_w must be >= 1");
+    if (c->mag < 1 || c->mag > 4) return fail(FLMISR_ERR_CONFIG, "mag must be in [1, 4]");
+    if (!c->shifts || !c->psf) return fail(FLMISR_ERR_CONFIG, "shifts and psf must be non-NULL host arrays");
+    if (!is_odd(c->psf_h) || !is_odd(c->psf_w) || c->psf_h > 5 || c->psf_w > 5)
+        return fail(FLMISR_ERR_CONFIG, "psf sizes must be odd and <= 5 (S:123)");
+    double s = 0.0;
+    for (int i = 0; i < c->psf_h * c->psf_w; ++i) {
+        if (!(c->psf[i] >= 0.0) || !std::isfinite(c->psf[i]))
+            return fail(FLMISR_ERR_CONFIG, "psf entries must be finite and >= 0 (S:95)");
+        s += c->psf[i];
+    }
+    if (std::fabs(s - 1.0) > 1e-6) return fail(FLMISR_ERR_CONFIG, "psf must sum to 1 within 1e-6 (S:95)");
+    for (int i = 0; i < 2 * c->k; ++i)
+        if (!std::isfinite(c->shifts[i])) return fail(FLMISR_ERR_CONFIG, "shifts must be finite");
+    if (c->p_norm != 1 && c->p_norm != 2) return fail(FLMISR_ERR_CONFIG, "p_norm must be 1 or 2 (Eq. misr, P:121)");
+    if (!(c->l1_eps > 0.0) || !std::isfinite(c->l1_eps)) return fail(FLMISR_ERR_CONFIG, "l1_eps must be > 0 (S:183)");
+    if (!(c->lambda >= 0.0) || !std::isfinite(c->lambda)) return fail(FLMISR_ERR_CONFIG, "lambda must be >= 0 (S:183)");
+    if (!(c->btv_alpha > 0.0 && c->btv_alpha < 1.0))
+        return fail(FLMISR_ERR_CONFIG, "btv_alpha must be in (0, 1) (P:138, S:183)");
+    if (c->btv_window < 1 || c->btv_window > MAXBW) return fail(FLMISR_ERR_CONFIG, "btv_window must be in [1, 3]");
+    if (c->n_iter < 0) return fail(FLMISR_ERR_CONFIG, "n_iter must be >= 0");
+    if (!(c->scg_lambda0 > 0.0) || !std::isfinite(c->scg_lambda0))
+        return fail(FLMISR_ERR_CONFIG, "scg_lambda0 must be > 0 (S:362)");
+    if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(FLMISR_ERR_CONFIG, "need 0 <= rank < world");
+    if (c->world > 1 && !c->nccl_unique_id) return fail(FLMISR_ERR_CONFIG, "world > 1 needs nccl_unique_id");
+    return FLMISR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* flmisr_last_error(void) { return g_last_error.c_str(); }
+
+flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
+    if (!out) return fail(FLMISR_ERR_CONFIG, "out is NULL");
+    *out = nullptr;
+    flmisr_status vs = validate(cfg);
+    if (vs != FLMISR_OK) return vs;
+    const flmisr_config& c = *cfg;
+
+    // ---- taps, phases, fast-path detection ----
+    const int mag = c.mag, K = c.k;
+    const int R = std::max(c.psf_h / 2, c.psf_w / 2);
+    std::vector<double> kap0;
+    int sy0, sx0;
+    double fy0, fx0;
+    composed_taps(c, 0, kap0, sy0, sx0, fy0, fx0);
+    bool fast = (K == mag * mag);
+    std::vector<int> frame_of_phase(mag * mag, -1);
+    std::vector<int> sy(K), sx(K);
+    for (int i = 0; i < K; ++i) {
+        std::vector<double> kap;
+        double fy, fx;
+        composed_taps(c, i, kap, sy[i], sx[i], fy, fx);
+        for (size_t j = 0; j < kap.size(); ++j)   // common kappa up to fp64 rounding of mag*shift
+            if (std::fabs(kap[j] - kap0[j]) > 1e-12) fast = false;
+        if (sy[i] < 0 || sy[i] >= mag || sx[i] < 0 || sx[i] >= mag) { fast = false; continue; }
+        int ph = sy[i] * mag + sx[i];
+        if (frame_of_phase[ph] >= 0) fast = false;
+        else frame_of_phase[ph] = i;
+    }
+    if (!fast)
+        return fail(FLMISR_ERR_CONFIG,
+                    "unsupported geometry: this build implements the polyphase-complete fast path (K = mag^2 "
+                    "frames with distinct integer HR phases in [0,mag)^2 and one common sub-pixel remainder); "
+                    "general shifts are SURVEY 8(f) NEXT-2");
+    const bool frac = (fy0 != 0.0 || fx0 != 0.0);
+    const int kr = frac ? R + 1 : R;
+    if (kr > MAXKR) return fail(FLMISR_ERR_CONFIG, "kappa radius exceeds 3");
+    if (c.world > 1 && !nccl().ok) return fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded");
+
+    auto* p = new flmisr_plan_s();
+    p->cfg = c;
+    p->shifts.assign(c.shifts, c.shifts + 2 * K);
+    p->psf.assign(c.psf, c.psf + c.psf_h * c.psf_w);
+    p->cfg.shifts = p->shifts.data();
+    p->cfg.psf = p->psf.data();
+    p->cfg.nccl_unique_id = nullptr;
+    p->fast = 1;
+    p->H = mag * c.lr_h;
+    p->W = mag * c.lr_w;
+    p->pitch = (p->W + 31) / 32 * 32;
+    p->kr = kr;
+    p->bw = c.btv_window;
+    p->pn = c.p_norm;
+    p->eta = std::max(2 * kr, c.btv_window - 1);
+
+    // ---- row band (Eq. subfunction): multiples of mag, remainder to the last band ----
+    const int world = c.world, rank = c.rank;
+    auto band = [&](int h, int& lo, int& hi) {
+        lo = (int)(((long long)h * p->H / world) / mag * mag);
+        hi = (h == world - 1) ? p->H : (int)(((long long)(h + 1) * p->H / world) / mag * mag);
+    };
+    for (int h = 0; h < world; ++h) {
+        int lo, hi;
+        band(h, lo, hi);
+        if (hi - lo < std::max(p->eta, 1)) {
+            const int need = std::max(p->eta, 1);
+            const int minH = world * need * mag;
+            delete p;
+            return fail(FLMISR_ERR_CONFIG, "image too small for " + std::to_string(world) +
+                                               " partitions: every band needs >= eta = " + std::to_string(need) +
+                                               " rows; minimum HR height " + std::to_string(minH) + " (S:254)");
+        }
+    }
+    band(rank, p->row_lo, p->row_hi);
+    p->store_lo = std::max(0, p->row_lo - p->eta);
+    p->store_hi = std::min(p->H, p->row_hi + p->eta);
+    const int srows = p->store_hi - p->store_lo;
+
+    // ---- stencil parameters ----
+    StencilParams& sp = p->sp;
+    sp.H = p->H; sp.W = p->W; sp.pitch = p->pitch;
+    sp.row_lo = p->row_lo; sp.row_hi = p->row_hi;
+    sp.store_lo = p->store_lo; sp.store_hi = p->store_hi;
+    sp.tile_row0 = p->row_lo;
+    sp.tiles_x = (p->W + TX - 1) / TX;
+    sp.tiles_y = (p->row_hi - p->row_lo + TY - 1) / TY;
+    sp.world = world;
+    sp.eps = (float)c.l1_eps;
+    sp.eps2 = (float)(c.l1_eps * c.l1_eps);
+    sp.lam = (float)c.lambda;
+    {
+        const int KD = 2 * R + 2, kd = 2 * kr + 1;
+        for (int i = 0; i < MAXTAPS; ++i) sp.taps[i] = 0.0f;
+        // kap0 offsets [-R, R+1] -> centred (2kr+1)^2 with offset index P + kr
+        for (int P = -R; P <= R + 1; ++P)
+            for (int Q = -R; Q <= R + 1; ++Q) {
+                double v = kap0[(size_t)(P + R) * KD + (Q + R)];
+                if (v == 0.0) continue;
+                sp.taps[(P + kr) * kd + (Q + kr)] = (float)v;
+            }
+        for (int i = 0; i < MAXBW * MAXBW; ++i) sp.gam[i] = 0.0f;
+        for (int dy = 0; dy < c.btv_window; ++dy)
+            for (int dx = 0; dx < c.btv_window; ++dx)
+                if (dy || dx) sp.gam[dy * MAXBW + dx] = (float)std::pow(c.btv_alpha, dx + dy);
+    }
+    IngestParams& ip = p->ip;
+    ip.H = p->H; ip.W = p->W; ip.pitch = p->pitch; ip.k = K; ip.lr_h = c.lr_h; ip.lr_w = c.lr_w; ip.mag = mag;
+    ip.store_lo = p->store_lo; ip.store_hi = p->store_hi;
+    for (int i = 0; i < 16; ++i) { ip.frame_of_phase[i] = 0; ip.sy[i] = 0; ip.sx[i] = 0; }
+    for (int ph = 0; ph < mag * mag; ++ph) ip.frame_of_phase[ph] = frame_of_phase[ph];
+    for (int i = 0; i < K; ++i) { ip.sy[i] = sy[i]; ip.sx[i] = sx[i]; }
+    ip.t0y = (float)(mag * c.shifts[0]);
+    ip.t0x = (float)(mag * c.shifts[1]);
+
+    // ---- device memory ----
+    auto cleanup_fail = [&](flmisr_status st) { flmisr_destroy(p); return st; };
+    cudaError_t e = cudaSetDevice(c.device);
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)));
+    e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e)));
+    p->hr_bytes = (size_t)srows * p->pitch * sizeof(float);
+    const int nhr = 7;  // Y, X0, X1, P0, P1, R0, R1
+    e = cudaMalloc(&p->mem, p->hr_bytes * nhr);
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc HR buffers: ") + cudaGetErrorString(e)));
+    cudaMemset(p->mem, 0, p->hr_bytes * nhr);
+    const size_t fl = p->hr_bytes / sizeof(float);
+    Buffers& b = p->b;
+    b.Y = p->mem;
+    b.X[0] = p->mem + 1 * fl; b.X[1] = p->mem + 2 * fl;
+    b.P[0] = p->mem + 3 * fl; b.P[1] = p->mem + 4 * fl;
+    b.R[0] = p->mem + 5 * fl; b.R[1] = p->mem + 6 * fl;
+    const size_t ntiles = (size_t)sp.tiles_x * sp.tiles_y;
+    const size_t npart = std::max<size_t>(NSLOT * ntiles, (size_t)NSLOT * world);
+    const size_t ntrace = (size_t)(c.n_iter + 1) * 6;
+    const size_t nd = npart + NSLOT + ntrace + (size_t)NSLOT * world;
+    e = cudaMalloc(&p->dmem, nd * sizeof(double));
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc partials: ") + cudaGetErrorString(e)));
+    cudaMemset(p->dmem, 0, nd * sizeof(double));
+    b.part = p->dmem;
+    b.rank_sums = p->dmem + npart;
+    b.trace = p->dmem + npart + NSLOT;
+    p->gathered = p->dmem + npart + NSLOT + ntrace;
+    e = cudaMalloc(&p->st, sizeof(ScgState));
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc state: ") + cudaGetErrorString(e)));
+    cudaMemset(p->st, 0, sizeof(ScgState));
+    b.st = p->st;
+    e = cudaMallocHost(&p->st_host, sizeof(ScgState));
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMallocHost state"));
+    e = cudaMallocHost(&p->trace_host, ntrace * sizeof(double));
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMallocHost trace"));
+    b.eta = p->eta;
+    b.halo_top = b.halo_bot = nullptr;
+    b.send_top = b.send_bot = nullptr;
+
+    // ---- NCCL (world > 1): communicator + halo buffers (inner-outer border exchange) ----
+    if (world > 1) {
+        NcclApi& api = nccl();
+        if (!api.ok) return cleanup_fail(fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded"));
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        ncclResult_t r = api.CommInitRank(&p->comm, world, id, rank);
+        if (r != ncclSuccess) return cleanup_fail(fail(FLMISR_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)));
+        const size_t hb = (size_t)p->eta * p->pitch * sizeof(float);
+        float* hm = nullptr;
+        e = cudaMalloc(&hm, 4 * hb);
+        if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc halo buffers"));
+        cudaMemset(hm, 0, 4 * hb);
+        const size_t hf = hb / sizeof(float);
+        if (rank > 0) { b.send_top = hm; p->recv_top = hm + 2 * hf; b.halo_top = p->recv_top; }
+        if (rank < world - 1) { b.send_bot = hm + hf; p->recv_bot = hm + 3 * hf; b.halo_bot = p->recv_bot; }
+        if (!b.send_top && !b.send_bot) cudaFree(hm);
+        else if (!b.send_top) { /* keep allocation referenced through send_bot base */ }
+    }
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("plan sync: ") + cudaGetErrorString(e)));
+    *out = p;
+    g_last_error.clear();
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_nccl_unique_id(void* out128) {
+    if (!out128) return fail(FLMISR_ERR_SHAPE, "out is NULL");
+    NcclApi& api = nccl();
+    if (!api.ok || !api.GetUniqueId) return fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    NCCL_TRY(api.GetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_plan_info(flmisr_plan_t p, int32_t* H, int32_t* W, int32_t* row_lo, int32_t* row_hi,
+                               int32_t* fast_path) {
+    if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    if (H) *H = p->H;
+    if (W) *W = p->W;
+    if (row_lo) *row_lo = p->row_lo;
+    if (row_hi) *row_hi = p->row_hi;
+    if (fast_path) *fast_path = p->fast;
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_destroy(flmisr_plan_t p) {
+    if (!p) return FLMISR_OK;
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->comm && nccl().ok) nccl().CommDestroy(p->comm);
+    if (p->b.send_top) cudaFree(p->b.send_top);
+    else if (p->b.send_bot) cudaFree(p->b.send_bot);
+    if (p->mem) cudaFree(p->mem);
+    if (p->dmem) cudaFree(p->dmem);
+    if (p->st) cudaFree(p->st);
+    if (p->st_host) cudaFreeHost(p->st_host);
+    if (p->trace_host) cudaFreeHost(p->trace_host);
+    if (p->pin_in) cudaFreeHost(p->pin_in);
+    if (p->pin_out) cudaFreeHost(p->pin_out);
+    if (p->d_lr) cudaFree(p->d_lr);
+    if (p->d_out) cudaFree(p->d_out);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+    return FLMISR_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Enqueue one value+gradient pass and, for world > 1, the consensus allgather + scalar kernel and
+// the inner-outer border exchange of the r candidate.
+flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
+    CUDA_TRY(launch_value_grad(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
+    if (p->cfg.world > 1) {
+        NcclApi& api = nccl();
+        const int rank = p->cfg.rank, world = p->cfg.world;
+        const size_t hcount = (size_t)p->eta * p->pitch;
+        NCCL_TRY(api.GroupStart());
+        NCCL_TRY(api.AllGather(p->b.rank_sums, p->b.part, NSLOT, ncclFloat64, p->comm, s));
+        if (rank > 0) {
+            NCCL_TRY(api.Send(p->b.send_top, hcount, ncclFloat32, rank - 1, p->comm, s));
+            NCCL_TRY(api.Recv(p->recv_top, hcount, ncclFloat32, rank - 1, p->comm, s));
+        }
+        if (rank < world - 1) {
+            NCCL_TRY(api.Send(p->b.send_bot, hcount, ncclFloat32, rank + 1, p->comm, s));
+            NCCL_TRY(api.Recv(p->recv_bot, hcount, ncclFloat32, rank + 1, p->comm, s));
+        }
+        NCCL_TRY(api.GroupEnd());
+        (void)phase;
+        CUDA_TRY(launch_scalar_after_value(p->b, world, s));
+    }
+    return FLMISR_OK;
+}
+
+flmisr_status enqueue_update_curv(flmisr_plan_s* p, int phase, cudaStream_t s) {
+    CUDA_TRY(launch_update_curv(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
+    if (p->cfg.world > 1) {
+        NCCL_TRY(nccl().AllGather(p->b.rank_sums, p->b.part, NSLOT, ncclFloat64, p->comm, s));
+        CUDA_TRY(launch_scalar_after_curv(p->b, p->cfg.world, s));
+    }
+    return FLMISR_OK;
+}
+
+flmisr_status collect_report(flmisr_plan_s* p, cudaStream_t s, flmisr_report* rep) {
+    const size_t ntrace = (size_t)(p->cfg.n_iter + 1) * 6;
+    CUDA_TRY(cudaMemcpyAsync(p->st_host, p->st, sizeof(ScgState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(p->trace_host, p->b.trace, ntrace * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const ScgState& h = *p->st_host;
+    if (rep) {
+        rep->iters_run = h.k;
+        rep->accepted = h.accepted;
+        rep->converged_at = h.converged_at;
+        rep->failed_stage = h.failed_stage;
+        rep->failed_iter = h.failed_iter;
+        if (rep->f_trace) std::memcpy(rep->f_trace, p->trace_host, ntrace * sizeof(double));
+    }
+    if (h.failed_stage)
+        return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar at SCG pass " + std::to_string(h.failed_iter) +
+                                            " (stage " + std::to_string(h.failed_stage) + ")");
+    return FLMISR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+flmisr_status flmisr_reconstruct(flmisr_plan_t p, const float* lr_stack, const float* x0, float* hr_out,
+                                 void* cuda_stream, flmisr_report* report) {
+    if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    if (!lr_stack) return fail(FLMISR_ERR_SHAPE, "lr_stack is NULL");
+    if (!hr_out && (p->cfg.world == 1 || p->cfg.rank == 0)) return fail(FLMISR_ERR_SHAPE, "hr_out is NULL");
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->stream;
+    const Buffers& b = p->b;
+    const size_t srows = (size_t)(p->store_hi - p->store_lo);
+
+    // a1: polyphase ingest; a2: initial estimate, p0 = 0, r_old = 0, state
+    CUDA_TRY(launch_ingest(p->ip, lr_stack, const_cast<float*>(b.Y), s));
+    if (x0) {
+        CUDA_TRY(cudaMemcpy2DAsync(b.X[0], p->pitch * sizeof(float), x0 + (size_t)p->store_lo * p->W,
+                                   p->W * sizeof(float), p->W * sizeof(float), srows, cudaMemcpyDeviceToDevice, s));
+    } else {
+        CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s));
+    }
+    CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
+    CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
+    CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
+
+    // init: f0 = J(x0), r0 = -grad J(x0) (Moller step 1), then n_iter SCG passes (Alg. 1 while-loop)
+    flmisr_status st = enqueue_value_grad(p, PH_INIT, s);
+    if (st != FLMISR_OK) return st;
+    for (int it = 0; it < p->cfg.n_iter; ++it) {
+        st = enqueue_update_curv(p, PH_ITER, s);
+        if (st != FLMISR_OK) return st;
+        st = enqueue_value_grad(p, PH_ITER, s);
+        if (st != FLMISR_OK) return st;
+    }
+    // a12: fuse (owned rows; rank 0 gathers the bands for world > 1)
+    if (hr_out) CUDA_TRY(launch_finalize(p->sp, b, hr_out, p->W, p->row_lo, p->row_hi, s));
+    if (p->cfg.world > 1) {
+        NcclApi& api = nccl();
+        const int rank = p->cfg.rank, world = p->cfg.world;
+        if (rank == 0) {
+            NCCL_TRY(api.GroupStart());
+            for (int h = 1; h < world; ++h) {
+                int lo = (int)(((long long)h * p->H / world) / p->cfg.mag * p->cfg.mag);
+                int hi = (h == world - 1) ? p->H : (int)(((long long)(h + 1) * p->H / world) / p->cfg.mag * p->cfg.mag);
+                NCCL_TRY(api.Recv(hr_out + (size_t)lo * p->W, (size_t)(hi - lo) * p->W, ncclFloat32, h, p->comm, s));
+            }
+            NCCL_TRY(api.GroupEnd());
+        } else {
+            float* src = hr_out ? hr_out + (size_t)p->row_lo * p->W : nullptr;
+            if (!src) return fail(FLMISR_ERR_SHAPE, "hr_out is required on every rank for the band gather");
+            NCCL_TRY(api.Send(src, (size_t)(p->row_hi - p->row_lo) * p->W, ncclFloat32, 0, p->comm, s));
+        }
+    }
+    return collect_report(p, s, report);
+}
+
+flmisr_status flmisr_reconstruct_host(flmisr_plan_t p, const float* lr_host, float* hr_host, flmisr_report* report) {
+    if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    if (!lr_host) return fail(FLMISR_ERR_SHAPE, "lr_stack_host is NULL");
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    const size_t nlr = (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w;
+    const size_t nhr = (size_t)p->H * p->W;
+    if (!p->pin_in) {
+        CUDA_TRY(cudaMallocHost(&p->pin_in, nlr * sizeof(float)));
+        CUDA_TRY(cudaMallocHost(&p->pin_out, nhr * sizeof(float)));
+        CUDA_TRY(cudaMalloc(&p->d_lr, nlr * sizeof(float)));
+        CUDA_TRY(cudaMalloc(&p->d_out, nhr * sizeof(float)));
+    }
+    std::memcpy(p->pin_in, lr_host, nlr * sizeof(float));
+    CUDA_TRY(cudaMemcpyAsync(p->d_lr, p->pin_in, nlr * sizeof(float), cudaMemcpyHostToDevice, p->stream));
+    flmisr_status st = flmisr_reconstruct(p, p->d_lr, nullptr, p->d_out, p->stream, report);
+    if (st != FLMISR_OK && st != FLMISR_ERR_NUMERIC) return st;
+    if (hr_host && (p->cfg.world == 1 || p->cfg.rank == 0)) {
+        CUDA_TRY(cudaMemcpyAsync(p->pin_out, p->d_out, nhr * sizeof(float), cudaMemcpyDeviceToHost, p->stream));
+        CUDA_TRY(cudaStreamSynchronize(p->stream));
+        std::memcpy(hr_host, p->pin_out, nhr * sizeof(float));
+    }
+    return st;
+}
+
+flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, const float* in0, const float* in1,
+                                 float* out, double* sc) {
+    if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    if (p->cfg.world != 1) return fail(FLMISR_ERR_CONFIG, "debug entries need world == 1");
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = p->stream;
+    Buffers& b = p->b;
+    const size_t rowb = p->W * sizeof(float), pitchb = p->pitch * sizeof(float);
+    const int H = p->H;
+    auto put_hr = [&](float* dst, const float* src) {
+        return cudaMemcpy2DAsync(dst, pitchb, src, rowb, rowb, H, cudaMemcpyDeviceToDevice, s);
+    };
+    auto get_hr = [&](float* dst, const float* src) {
+        return cudaMemcpy2DAsync(dst, rowb, src, pitchb, rowb, H, cudaMemcpyDeviceToDevice, s);
+    };
+    CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
+    switch (op) {
+        case FLMISR_OP_FORWARD:
+            if (!in0 || !out) return fail(FLMISR_ERR_SHAPE, "FORWARD needs in0 and out");
+            CUDA_TRY(put_hr(b.X[0], in0));
+            CUDA_TRY(launch_forward_debug(p->kr, p->sp, b.X[0], b.R[0], s));
+            CUDA_TRY(launch_egest(p->ip, b.R[0], out, s));
+            break;
+        case FLMISR_OP_ADJOINT:
+            if (!in0 || !out) return fail(FLMISR_ERR_SHAPE, "ADJOINT needs in0 and out");
+            CUDA_TRY(launch_ingest(p->ip, in0, b.R[0], s));
+            CUDA_TRY(launch_adjoint_debug(p->kr, p->sp, b.R[0], b.R[1], s));
+            CUDA_TRY(get_hr(out, b.R[1]));
+            break;
+        case FLMISR_OP_GRAD:
+        case FLMISR_OP_VALUE:
+            if (!lr || !in0) return fail(FLMISR_ERR_SHAPE, "GRAD/VALUE need lr and in0");
+            CUDA_TRY(launch_ingest(p->ip, lr, const_cast<float*>(b.Y), s));
+            CUDA_TRY(put_hr(b.X[0], in0));
+            CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
+            CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
+            CUDA_TRY(launch_value_grad(p->kr, p->bw, p->pn, p->sp, b, PH_DEBUG, s));
+            if (op == FLMISR_OP_GRAD && out) CUDA_TRY(get_hr(out, b.R[1]));
+            break;
+        case FLMISR_OP_CURV:
+            if (!lr || !in0 || !in1) return fail(FLMISR_ERR_SHAPE, "CURV needs lr, in0 and in1");
+            CUDA_TRY(launch_ingest(p->ip, lr, const_cast<float*>(b.Y), s));
+            CUDA_TRY(put_hr(b.X[0], in0));
+            CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
+            CUDA_TRY(put_hr(b.R[0], in1));
+            CUDA_TRY(launch_update_curv(p->kr, p->bw, p->pn, p->sp, b, PH_DEBUG, s));
+            break;
+        case FLMISR_OP_X0:
+            if (!lr || !out) return fail(FLMISR_ERR_SHAPE, "X0 needs lr and out");
+            CUDA_TRY(launch_init_x0(p->ip, lr, b.X[0], s));
+            CUDA_TRY(get_hr(out, b.X[0]));
+            break;
+        default:
+            return fail(FLMISR_ERR_CONFIG, "unknown debug op");
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->st_host, p->st, sizeof(ScgState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (sc) {
+        const double* d = p->st_host->dbg;
+        if (op == FLMISR_OP_GRAD || op == FLMISR_OP_VALUE) { sc[0] = d[0]; sc[1] = d[1]; sc[2] = d[2]; }
+        if (op == FLMISR_OP_CURV) { sc[0] = d[0] + p->cfg.lambda * d[1]; sc[1] = d[2]; sc[2] = d[3]; }
+    }
+    return FLMISR_OK;
+}
+
+}  // extern "C"

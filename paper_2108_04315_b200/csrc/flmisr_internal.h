@@ -1,0 +1,91 @@
+// flmisr_internal.h -- shared declarations between the host plan/driver (flmisr_api.cpp) and the
+// sm_100a kernels (flmisr_kernels.cu).  Not part of the public ABI (include/flmisr.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace flmisr {
+
+// Output tile of one CTA in the stencil kernels (rows x columns of HR pixels).
+constexpr int TX = 64;
+constexpr int TY = 16;
+constexpr int NTHREADS = 256;
+constexpr int MAXKR = 3;                                 // kappa radius (PSF radius, +1 for a common fractional phase)
+constexpr int MAXTAPS = (2 * MAXKR + 1) * (2 * MAXKR + 1);
+constexpr int MAXBW = 3;                                 // BTV window w
+constexpr int NSLOT = 4;                                 // fp64 partial sums per CTA
+
+// Device-resident SCG state (Moller SCG scalars).  fp64 scalars; the fp32
+// copies are what the per-pixel kernels use.
+struct ScgState {
+    double f, f_new, lam, lamb, delta, pp, mu, alpha, beta, rr;
+    double lambda_reg;           // BTV weight lambda (Eq. objective)
+    double dbg[8];               // debug-entry sums
+    float alpha_f;               // step alpha for the value/gradient pass (x + alpha p)
+    float alpha_upd_f;           // alpha of the pending accepted step, applied by the next update pass
+    float beta_f;                // conjugate-direction beta for the next update pass
+    float pad0;
+    long long npix;              // H*W (Moller restart period)
+    int k, n_iter, success, done;
+    int xcur, rcur;              // ping-pong indices of x/p and r buffers
+    int accepted, converged_at, failed_stage, failed_iter;
+    unsigned int counter;        // CTA arrival counter (last-CTA reduction), reset by the last CTA
+    int pad1;
+};
+
+struct StencilParams {
+    int H, W, pitch;             // global HR size, row pitch (floats) of every HR buffer
+    int row_lo, row_hi;          // owned global rows [row_lo, row_hi)
+    int store_lo, store_hi;      // rows held in device storage [store_lo, store_hi) (owned + halo)
+    int tile_row0;               // global row of the first tile row
+    int tiles_x, tiles_y;
+    int world;                   // 1: scalar logic in the last CTA; >1: rank sums for the allgather
+    float eps, eps2, lam;        // Charbonnier eps, eps^2, BTV weight lambda (fp32 copies)
+    float taps[MAXTAPS];         // kappa, (2KR+1)^2 centred, row-major, correlation orientation
+    float gam[MAXBW * MAXBW];    // gamma(dy,dx) = alpha^(dx+dy) at [dy*MAXBW + dx], gam[0] unused
+};
+
+struct Buffers {
+    const float* Y;              // polyphase-interleaved LR stack on the HR grid (storage base)
+    float* X[2];                 // x ping-pong
+    float* P[2];                 // p ping-pong
+    float* R[2];                 // r = -grad J ping-pong (R[rcur] accepted, R[1-rcur] candidate)
+    double* part;                // NSLOT x ntiles fp64 CTA partials (slot-major)
+    double* rank_sums;           // NSLOT fp64 rank-local sums (world > 1)
+    ScgState* st;
+    double* trace;               // (n_iter+1) x 6 rows (k, f, rr, alpha, lambda_scg, accepted)
+    const float* halo_top;       // world > 1: received r rows above the band (eta x pitch) or null
+    const float* halo_bot;       // received r rows below the band or null
+    float* send_top;             // owned top eta rows of the r candidate, for the upper neighbour
+    float* send_bot;
+    int eta;                     // halo rows per side
+};
+
+enum Phase : int { PH_ITER = 0, PH_INIT = 1, PH_DEBUG = 2 };
+
+// Launchers (flmisr_kernels.cu).  Return cudaSuccess or the launch error; dispatch on (kr, bw, pn).
+cudaError_t launch_value_grad(int kr, int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
+                              cudaStream_t s);
+cudaError_t launch_update_curv(int kr, int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
+                               cudaStream_t s);
+cudaError_t launch_scalar_after_value(const Buffers& b, int world, cudaStream_t s);  // world > 1
+cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s);   // world > 1
+cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,
+                              cudaStream_t s);
+
+struct IngestParams {
+    int H, W, pitch, k, lr_h, lr_w, mag;
+    int store_lo, store_hi;
+    int frame_of_phase[16];      // residue (u mod mag, v mod mag) -> frame index
+    int sy[16], sx[16];          // integer phase of frame i
+    float t0y, t0x;              // HR shift of frame 0 (bilinear initial estimate)
+};
+cudaError_t launch_ingest(const IngestParams& ip, const float* lr, float* Y, cudaStream_t s);
+cudaError_t launch_egest(const IngestParams& ip, const float* Yhr, float* lr, cudaStream_t s);   // debug
+cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s);
+cudaError_t launch_finalize(const StencilParams& sp, const Buffers& b, float* out, int out_pitch, int row_lo,
+                            int row_hi, cudaStream_t s);
+cudaError_t launch_forward_debug(int kr, const StencilParams& sp, const float* x, float* zhr, cudaStream_t s);
+cudaError_t launch_adjoint_debug(int kr, const StencilParams& sp, const float* whr, float* g, cudaStream_t s);
+
+}  // namespace flmisr

@@ -1,0 +1,724 @@
+// flmisr_kernels.cu -- sm_100a kernels of the FL-MISR SCG hot path (arXiv 2108.04315).
+//
+// Polyphase fast path: the K = mag^2 LR frames are interleaved once into an
+// HR-grid image Y with Y(mag*a + s_i) = y_i(a) (ingest), so every HR pixel u carries exactly one LR
+// sample and the forward model A_i = D B M_i (Eq. sisr) becomes a unit-stride HR stencil
+//     z(u) = sum_{P,Q} kappa(P,Q) x~(u + (P,Q))         (x~ = clamp-extended x, reading 4)
+// with residual e(u) = z(u) - Y(u).  Its adjoint (zero-fill upsample, transposed blur, inverse
+// shift; north_star) is the kappa-correlation of the zero-padded weight image w = rho'(e), folded
+// back onto the edge pixels where the forward clamped.
+//
+// Per accepted SCG pass there are two stencil kernels (both HBM-bound):
+//   k_update_curv : x <- x + alpha p, p <- r + beta p (Alg. 1 lines 14, 20) and the
+//                   exact directional curvature delta = p^T Hess J p, <p,p>, <p,r> (lines 6-12).
+//   k_value_grad  : f_new = J(x + alpha p) (line 16) and, speculatively in the same pass,
+//                   r_new = -grad J(x + alpha p) with <r_new,r_new>, <r_new,r_old> (line 18).
+// Each CTA reduces its partials with warp shuffles into one fp64 slot; the last CTA to finish sums
+// the slots in a fixed order (deterministic, no float atomics) and runs Moller's scalar logic on
+// device (single GPU), so there is no host round-trip inside the loop.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "flmisr_internal.h"
+
+namespace flmisr {
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// ------------------------------------------------------------------------------------------------
+// Penalties (reading 8).  One MUFU rsqrt serves rho, rho' and rho''.
+//   Charbonnier:  rho = sqrt(t^2+eps^2) - eps,  rho' = t / sqrt(.),  rho'' = eps^2 / (.)^(3/2)
+//   squared L2:   rho = t^2, rho' = 2t, rho'' = 2
+// ------------------------------------------------------------------------------------------------
+template <int PN>
+struct Pen {
+    __device__ __forceinline__ static void val_d1(float t, float eps, float eps2, float& v, float& d1) {
+        if (PN == 2) {
+            v = t * t;
+            d1 = 2.0f * t;
+        } else {
+            float q = fmaf(t, t, eps2);
+            float rs = rsqrtf(q);
+            v = fmaf(q, rs, -eps);
+            d1 = t * rs;
+        }
+    }
+    __device__ __forceinline__ static float d2(float t, float eps2) {
+        if (PN == 2) return 2.0f;
+        float q = fmaf(t, t, eps2);
+        float rs = rsqrtf(q);
+        return eps2 * rs * rs * rs;
+    }
+};
+
+__device__ __forceinline__ void charb_val_d1(float t, float eps, float eps2, float& v, float& d1) {
+    float q = fmaf(t, t, eps2);
+    float rs = rsqrtf(q);
+    v = fmaf(q, rs, -eps);
+    d1 = t * rs;
+}
+__device__ __forceinline__ float charb_d1(float t, float eps2) { return t * rsqrtf(fmaf(t, t, eps2)); }
+__device__ __forceinline__ float charb_d2(float t, float eps2) {
+    float rs = rsqrtf(fmaf(t, t, eps2));
+    return eps2 * rs * rs * rs;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Moller SCG scalar logic (single thread; DESIGN.md section 6 lists it line by line against the
+// oracle's algorithm block).  Consensus sums arrive already reduced over all partitions.
+// ------------------------------------------------------------------------------------------------
+__device__ void scg_pre_value(ScgState* s) {
+    double delta = s->delta + (s->lam - s->lamb) * s->pp;       // Moller step 3 (scale)
+    if (delta <= 0.0) {                                         // step 4 (make Hessian PD)
+        s->lamb = 2.0 * (s->lam - delta / s->pp);
+        delta = -delta + s->lam * s->pp;
+        s->lam = s->lamb;
+    }
+    s->delta = delta;
+    s->alpha = s->mu / delta;                                   // step 5
+    s->alpha_f = (float)s->alpha;
+    if (!isfinite(delta) || !isfinite(s->alpha)) {
+        s->failed_stage = 1;
+        s->failed_iter = s->k;
+        s->done = 1;
+    }
+}
+
+__device__ void scg_after_curv(ScgState* s, const double* t) {
+    // t = {sum rho'' (A p)^2, sum gamma psi'' (D_d p)^2, <p,p>, <p,r>}   (Alg. 1 lines 6, 10, 12)
+    s->delta = t[0] + s->lambda_reg * t[1];
+    s->pp = t[2];
+    s->mu = t[3];
+    scg_pre_value(s);
+}
+
+__device__ void scg_after_value(ScgState* s, const double* t, double* trace, int phase) {
+    // t = {D(x'), R(x'), <r',r'>, <r',r>} at x' = x + alpha p         (Alg. 1 lines 16-19)
+    double fnew = t[0] + s->lambda_reg * t[1];
+    s->f_new = fnew;
+    if (phase == PH_INIT) {
+        s->f = fnew;
+        s->rr = t[2];
+        s->rcur ^= 1;
+        s->success = 1;
+        s->alpha_upd_f = 0.0f;
+        s->beta_f = 0.0f;
+        double* row = trace;
+        row[0] = 0; row[1] = fnew; row[2] = t[2]; row[3] = 0; row[4] = s->lam; row[5] = 1;
+        if (!isfinite(fnew) || !isfinite(t[2])) {
+            s->failed_stage = 2;
+            s->failed_iter = 0;
+            s->done = 1;
+            return;
+        }
+        if (t[2] == 0.0) { s->converged_at = 0; s->done = 1; }
+        if (s->n_iter <= 0) s->done = 1;
+        return;
+    }
+    double Delta = 2.0 * s->delta * (s->f - fnew) / (s->mu * s->mu);   // step 6 (comparison ratio)
+    if (!isfinite(fnew) || !isfinite(Delta)) {
+        s->failed_stage = 2;
+        s->failed_iter = s->k;
+        s->done = 1;
+        return;
+    }
+    int acc = Delta >= 0.0;
+    if (acc) {                                                          // step 7 (successful step)
+        s->f = fnew;
+        s->lamb = 0.0;
+        s->success = 1;
+        double rr = t[2];
+        s->beta = ((long long)(s->k + 1) % s->npix == 0) ? 0.0 : (rr - t[3]) / s->mu;
+        s->rr = rr;
+        s->rcur ^= 1;
+        s->alpha_upd_f = s->alpha_f;
+        s->beta_f = (float)s->beta;
+        s->accepted += 1;
+        if (Delta >= 0.75) s->lam = s->lam / 4.0;
+        if (!isfinite(s->beta)) {
+            s->failed_stage = 2;
+            s->failed_iter = s->k;
+            s->done = 1;
+        }
+    } else {
+        s->lamb = s->lam;
+        s->success = 0;
+    }
+    if (Delta < 0.25) s->lam = s->lam + s->delta * (1.0 - Delta) / s->pp;   // step 8
+    s->k += 1;
+    double* row = trace + 6 * (size_t)s->k;
+    row[0] = s->k; row[1] = s->f; row[2] = s->rr; row[3] = s->alpha; row[4] = s->lam; row[5] = acc;
+    if (s->rr == 0.0) { s->converged_at = s->k; s->done = 1; }         // step 9
+    if (s->k >= s->n_iter) s->done = 1;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Reductions: per-thread fp32 partials -> fp64 warp shuffle tree -> one fp64 slot per CTA ->
+// fixed-order sum by the last CTA.  Returns true in the (whole) last CTA with `tot` filled.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ bool reduce_partials(const float (&acc)[NSLOT], double* part, int ntiles, int tile, unsigned int* counter,
+                                double (&tot)[NSLOT]) {
+    __shared__ double sred[NTHREADS / 32][NSLOT];
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        double v = warp_sum((double)acc[k]);
+        if (lane == 0) sred[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NSLOT) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < NTHREADS / 32; ++w) v += sred[w][threadIdx.x];
+        part[(size_t)threadIdx.x * ntiles + tile] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == (unsigned)(ntiles - 1));
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    // fixed-order sum over the CTA slots: thread t takes slots t, t+256, ... sequentially, then a
+    // fixed shuffle tree and a fixed cross-warp order.
+    double loc[NSLOT];
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) loc[k] = 0.0;
+    for (int i = threadIdx.x; i < ntiles; i += NTHREADS) {
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) loc[k] += __ldcg(part + (size_t)k * ntiles + i);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        double v = warp_sum(loc[k]);
+        if (lane == 0) sred[warp][k] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < NTHREADS / 32; ++w) v += sred[w][k];
+        tot[k] = v;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    return true;
+}
+
+// Store the CTA totals: world == 1 -> run the scalar logic here; world > 1 -> publish the rank sums
+// for the allgather (the scalar kernel runs after NCCL).
+template <int WHICH>
+__device__ void finish_scalars(const StencilParams& sp, const Buffers& b, const double (&tot)[NSLOT], int phase) {
+    if (threadIdx.x != 0) return;
+    ScgState* s = b.st;
+    if (phase == PH_DEBUG) {
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) s->dbg[k] = tot[k];
+        return;
+    }
+    if (sp.world > 1) {
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) b.rank_sums[k] = tot[k];
+        return;
+    }
+    if (WHICH == 0) scg_after_value(s, tot, b.trace, phase);
+    else scg_after_curv(s, tot);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Tile staging helpers.  A region of RH x RW floats whose origin is global (gr0, gc0) is loaded
+// with clamp-to-image indexing (reading 4: x~ is the clamp extension), from storage rows
+// [store_lo, store_hi).  gc0 and RW are multiples of 4 so interior chunks move as float4.
+// ------------------------------------------------------------------------------------------------
+template <int RH, int RW, typename F>
+__device__ __forceinline__ void load_region(const StencilParams& sp, int gr0, int gc0, F&& fn) {
+    constexpr int CH = RW / 4;
+    for (int idx = threadIdx.x; idx < RH * CH; idx += NTHREADS) {
+        int lr = idx / CH, ch = idx - lr * CH;
+        int gr = clampi(gr0 + lr, 0, sp.H - 1);
+        gr = clampi(gr, sp.store_lo, sp.store_hi - 1);
+        size_t rowoff = (size_t)(gr - sp.store_lo) * sp.pitch;
+        int gc = gc0 + 4 * ch;
+        if (gc >= 0 && gc + 3 < sp.W) {
+            fn(lr, 4 * ch, rowoff + gc, true, 0, 0, 0, 0);
+        } else {
+            int c0 = clampi(gc, 0, sp.W - 1), c1 = clampi(gc + 1, 0, sp.W - 1);
+            int c2 = clampi(gc + 2, 0, sp.W - 1), c3 = clampi(gc + 3, 0, sp.W - 1);
+            fn(lr, 4 * ch, rowoff, false, c0, c1, c2, c3);
+        }
+    }
+}
+
+__device__ __forceinline__ float4 ld4(const float* p, size_t off, bool vec, int c0, int c1, int c2, int c3) {
+    if (vec) return __ldg(reinterpret_cast<const float4*>(p + off));
+    return make_float4(__ldg(p + off + c0), __ldg(p + off + c1), __ldg(p + off + c2), __ldg(p + off + c3));
+}
+
+// ------------------------------------------------------------------------------------------------
+// Kernel: value + gradient at x' = x + alpha p (one pass; Alg. 1 lines 14-19).
+// ------------------------------------------------------------------------------------------------
+template <int KR, int BW, int PN>
+__global__ void __launch_bounds__(NTHREADS) k_value_grad(StencilParams sp, Buffers b, int phase) {
+    constexpr int HX = (2 * KR > BW - 1) ? 2 * KR : BW - 1;   // x' halo
+    constexpr int HXC = (HX + 3) / 4 * 4;                     // column halo rounded to float4
+    constexpr int SXH = TY + 2 * HX, SXW = TX + 2 * HXC;
+    constexpr int SWH = TY + 2 * KR, SWW = TX + 2 * KR;
+    constexpr int KD = 2 * KR + 1;
+    __shared__ float sX[SXH * SXW];
+    __shared__ float sW[SWH * SWW];
+
+    ScgState* st = b.st;
+    if (phase != PH_DEBUG && st->done) return;
+    const int xcur = st->xcur, rcur = st->rcur;
+    const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
+    const float* __restrict__ X = b.X[xcur];
+    const float* __restrict__ P = b.P[xcur];
+    const float* __restrict__ Rold = b.R[rcur];
+    float* __restrict__ Rnew = b.R[rcur ^ 1];
+
+    const int tile = blockIdx.y * sp.tiles_x + blockIdx.x;
+    const int ntiles = sp.tiles_x * sp.tiles_y;
+    const int r0 = sp.tile_row0 + blockIdx.y * TY, c0 = blockIdx.x * TX;
+    const int H = sp.H, W = sp.W;
+
+    // stage 1: x' = x + alpha p on the tile + HX halo (clamp-extended)
+    load_region<SXH, SXW>(sp, r0 - HX, c0 - HXC,
+                          [&](int lr, int lc, size_t off, bool vec, int a0, int a1, int a2, int a3) {
+                              float4 xv = ld4(X, off, vec, a0, a1, a2, a3);
+                              float4 pv = ld4(P, off, vec, a0, a1, a2, a3);
+                              float* d = sX + lr * SXW + lc;
+                              d[0] = fmaf(alpha, pv.x, xv.x);
+                              d[1] = fmaf(alpha, pv.y, xv.y);
+                              d[2] = fmaf(alpha, pv.z, xv.z);
+                              d[3] = fmaf(alpha, pv.w, xv.w);
+                          });
+    __syncthreads();
+
+    float acc[NSLOT] = {0.f, 0.f, 0.f, 0.f};   // D, R, <r',r'>, <r',r_old>
+    const float eps = sp.eps, eps2 = sp.eps2;
+
+    // stage 2: w = rho'(z - Y) on the tile + KR halo (zero outside the image); data value on the tile
+    for (int idx = threadIdx.x; idx < SWH * SWW; idx += NTHREADS) {
+        int i = idx / SWW, j = idx - i * SWW;
+        int gr = r0 - KR + i, gc = c0 - KR + j;
+        float wv = 0.0f;
+        if (gr >= 0 && gr < H && gc >= 0 && gc < W) {
+            float z = 0.0f;
+            const float* base = sX + (i - KR + HX - KR) * SXW + (j - KR + HXC - KR);
+#pragma unroll
+            for (int P_ = 0; P_ < KD; ++P_)
+#pragma unroll
+                for (int Q_ = 0; Q_ < KD; ++Q_) z = fmaf(sp.taps[P_ * KD + Q_], base[P_ * SXW + Q_], z);
+            float e = z - __ldg(b.Y + (size_t)(gr - sp.store_lo) * sp.pitch + gc);
+            float v, d1;
+            Pen<PN>::val_d1(e, eps, eps2, v, d1);
+            wv = d1;
+            if (i >= KR && i < KR + TY && j >= KR && j < KR + TX && gr >= sp.row_lo && gr < sp.row_hi) acc[0] += v;
+        }
+        sW[idx] = wv;
+    }
+    __syncthreads();
+
+    // stage 3: g = A^T w (+ border fold) + lambda grad R; BTV value; r' = -g
+    const float lam = sp.lam;
+    for (int idx = threadIdx.x; idx < TY * TX; idx += NTHREADS) {
+        int ly = idx / TX, lx = idx - ly * TX;
+        int vy = r0 + ly, vx = c0 + lx;
+        if (vy >= sp.row_hi || vx >= W) continue;
+        // adjoint: g(v) = sum_{P,Q} kappa(P,Q) w(v - (P,Q))  (zero-padded w)
+        float g = 0.0f;
+        {
+            const float* base = sW + (ly + KR + KR) * SWW + (lx + KR + KR);
+#pragma unroll
+            for (int P_ = 0; P_ < KD; ++P_)
+#pragma unroll
+                for (int Q_ = 0; Q_ < KD; ++Q_) g = fmaf(sp.taps[P_ * KD + Q_], base[-P_ * SWW - Q_], g);
+        }
+        if (KR > 0 && (vy == 0 || vy == H - 1 || vx == 0 || vx == W - 1)) {
+            // fold: add g_ext(v') for virtual v' != v outside the image with clamp(v') = v
+            int ylo = (vy == 0) ? -KR : vy, yhi = (vy == H - 1) ? H - 1 + KR : vy;
+            int xlo = (vx == 0) ? -KR : vx, xhi = (vx == W - 1) ? W - 1 + KR : vx;
+            for (int yy = ylo; yy <= yhi; ++yy)
+                for (int xx = xlo; xx <= xhi; ++xx) {
+                    if (yy == vy && xx == vx) continue;
+                    for (int P_ = 0; P_ < KD; ++P_)
+                        for (int Q_ = 0; Q_ < KD; ++Q_) {
+                            int uy = yy - (P_ - KR), ux = xx - (Q_ - KR);
+                            if (uy < 0 || uy >= H || ux < 0 || ux >= W) continue;
+                            g = fmaf(sp.taps[P_ * KD + Q_], sW[(uy - r0 + KR) * SWW + (ux - c0 + KR)], g);
+                        }
+                }
+        }
+        // BTV: pairs (v, v+d) owned by v (value + both endpoints' gradient), pairs (v-d, v) gradient
+        float gb = 0.0f;
+        const float xv = sX[(ly + HX) * SXW + lx + HXC];
+#pragma unroll
+        for (int dy = 0; dy < BW; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < BW; ++dx) {
+                if (dy == 0 && dx == 0) continue;
+                const float gm = sp.gam[dy * MAXBW + dx];
+                if (vy + dy < H && vx + dx < W) {
+                    float t = xv - sX[(ly + HX + dy) * SXW + lx + HXC + dx];
+                    float v, d1;
+                    charb_val_d1(t, eps, eps2, v, d1);
+                    acc[1] = fmaf(gm, v, acc[1]);
+                    gb = fmaf(gm, d1, gb);
+                }
+                if (vy - dy >= 0 && vx - dx >= 0) {
+                    float t = sX[(ly + HX - dy) * SXW + lx + HXC - dx] - xv;
+                    gb = fmaf(-gm, charb_d1(t, eps2), gb);
+                }
+            }
+        float rn = -fmaf(lam, gb, g);
+        size_t off = (size_t)(vy - sp.store_lo) * sp.pitch + vx;
+        float ro = __ldg(Rold + off);
+        Rnew[off] = rn;
+        acc[2] = fmaf(rn, rn, acc[2]);
+        acc[3] = fmaf(rn, ro, acc[3]);
+        // band mode: owned boundary rows of the candidate go to the neighbours (inner border)
+        if (b.send_top && vy - sp.row_lo < b.eta) b.send_top[(size_t)(vy - sp.row_lo) * sp.pitch + vx] = rn;
+        if (b.send_bot && sp.row_hi - 1 - vy < b.eta) b.send_bot[(size_t)(vy - (sp.row_hi - b.eta)) * sp.pitch + vx] = rn;
+    }
+
+    double tot[NSLOT];
+    if (reduce_partials(acc, b.part, ntiles, tile, &st->counter, tot)) finish_scalars<0>(sp, b, tot, phase);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Kernel: update x <- x + alpha_upd p, p <- r + beta p, and curvature at the new (x, p).
+// ------------------------------------------------------------------------------------------------
+template <int KR, int BW, int PN>
+__global__ void __launch_bounds__(NTHREADS) k_update_curv(StencilParams sp, Buffers b, int phase) {
+    constexpr int HK = (KR > BW - 1) ? KR : BW - 1;
+    constexpr int HKC = (HK + 3) / 4 * 4;
+    constexpr int SH = TY + 2 * HK, SW = TX + 2 * HKC;
+    constexpr int KD = 2 * KR + 1;
+    __shared__ float sXn[SH * SW];
+    __shared__ float sPn[SH * SW];
+
+    ScgState* st = b.st;
+    if (phase != PH_DEBUG) {
+        if (st->done) return;
+        if (!st->success) {   // rejected step: delta is reused, only the scalar pre-value step runs
+            if (sp.world == 1 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) scg_pre_value(st);
+            return;
+        }
+    }
+    const int xcur = st->xcur, rcur = st->rcur;
+    const float au = (phase == PH_DEBUG) ? 0.0f : st->alpha_upd_f;
+    const float be = (phase == PH_DEBUG) ? 0.0f : st->beta_f;
+    const float* __restrict__ X = b.X[xcur];
+    const float* __restrict__ P = b.P[xcur];
+    const float* __restrict__ R = b.R[rcur];
+    float* __restrict__ Xn = b.X[xcur ^ 1];
+    float* __restrict__ Pn = b.P[xcur ^ 1];
+
+    const int tile = blockIdx.y * sp.tiles_x + blockIdx.x;
+    const int ntiles = sp.tiles_x * sp.tiles_y;
+    const int r0 = sp.tile_row0 + blockIdx.y * TY, c0 = blockIdx.x * TX;
+    const int H = sp.H, W = sp.W;
+    float acc[NSLOT] = {0.f, 0.f, 0.f, 0.f};   // curv data, curv BTV, <p,p>, <p,r>
+
+    load_region<SH, SW>(sp, r0 - HK, c0 - HKC, [&](int lr, int lc, size_t off, bool vec, int a0, int a1, int a2, int a3) {
+        float4 xv = ld4(X, off, vec, a0, a1, a2, a3);
+        float4 pv = ld4(P, off, vec, a0, a1, a2, a3);
+        float4 rv = ld4(R, off, vec, a0, a1, a2, a3);
+        float xn[4] = {fmaf(au, pv.x, xv.x), fmaf(au, pv.y, xv.y), fmaf(au, pv.z, xv.z), fmaf(au, pv.w, xv.w)};
+        float pn[4] = {fmaf(be, pv.x, rv.x), fmaf(be, pv.y, rv.y), fmaf(be, pv.z, rv.z), fmaf(be, pv.w, rv.w)};
+        float rr[4] = {rv.x, rv.y, rv.z, rv.w};
+        float* dx_ = sXn + lr * SW + lc;
+        float* dp_ = sPn + lr * SW + lc;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { dx_[e] = xn[e]; dp_[e] = pn[e]; }
+        // owned interior element: write the new iterate, accumulate <p,p>, <p,r>
+        int gr = r0 - HK + lr;
+        if (lr >= HK && lr < HK + TY && gr < sp.row_hi && vec && lc >= HKC && lc < HKC + TX) {
+            *reinterpret_cast<float4*>(Xn + off) = make_float4(xn[0], xn[1], xn[2], xn[3]);
+            *reinterpret_cast<float4*>(Pn + off) = make_float4(pn[0], pn[1], pn[2], pn[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                acc[2] = fmaf(pn[e], pn[e], acc[2]);
+                acc[3] = fmaf(pn[e], rr[e], acc[3]);
+            }
+        } else if (lr >= HK && lr < HK + TY && gr < sp.row_hi && !vec && lc >= HKC && lc < HKC + TX) {
+            // partial float4 at the right image edge: element-wise, skip clamped duplicates
+            int gc = c0 - HKC + lc;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (gc + e < W) {
+                    Xn[off + gc + e] = xn[e];
+                    Pn[off + gc + e] = pn[e];
+                    acc[2] = fmaf(pn[e], pn[e], acc[2]);
+                    acc[3] = fmaf(pn[e], rr[e], acc[3]);
+                }
+            }
+        }
+    });
+    __syncthreads();
+
+    const float eps2 = sp.eps2;
+    {
+        for (int idx = threadIdx.x; idx < TY * TX; idx += NTHREADS) {
+            int ly = idx / TX, lx = idx - ly * TX;
+            int uy = r0 + ly, ux = c0 + lx;
+            if (uy >= sp.row_hi || ux >= W) continue;
+            float z = 0.0f, ap = 0.0f;
+            const float* bx = sXn + (ly + HK - KR) * SW + (lx + HKC - KR);
+            const float* bp = sPn + (ly + HK - KR) * SW + (lx + HKC - KR);
+#pragma unroll
+            for (int P_ = 0; P_ < KD; ++P_)
+#pragma unroll
+                for (int Q_ = 0; Q_ < KD; ++Q_) {
+                    float kk = sp.taps[P_ * KD + Q_];
+                    z = fmaf(kk, bx[P_ * SW + Q_], z);
+                    ap = fmaf(kk, bp[P_ * SW + Q_], ap);
+                }
+            float e = z - __ldg(b.Y + (size_t)(uy - sp.store_lo) * sp.pitch + ux);
+            acc[0] = fmaf(Pen<PN>::d2(e, eps2), ap * ap, acc[0]);
+            const float xu = sXn[(ly + HK) * SW + lx + HKC], pu = sPn[(ly + HK) * SW + lx + HKC];
+#pragma unroll
+            for (int dy = 0; dy < BW; ++dy)
+#pragma unroll
+                for (int dx = 0; dx < BW; ++dx) {
+                    if (dy == 0 && dx == 0) continue;
+                    if (uy + dy < H && ux + dx < W) {
+                        float t = xu - sXn[(ly + HK + dy) * SW + lx + HKC + dx];
+                        float dp = pu - sPn[(ly + HK + dy) * SW + lx + HKC + dx];
+                        acc[1] = fmaf(sp.gam[dy * MAXBW + dx] * charb_d2(t, eps2), dp * dp, acc[1]);
+                    }
+                }
+        }
+    }
+    (void)H;
+    double tot[NSLOT];
+    if (reduce_partials(acc, b.part, ntiles, tile, &st->counter, tot)) {
+        if (threadIdx.x == 0 && phase != PH_DEBUG) st->xcur = xcur ^ 1;
+        finish_scalars<1>(sp, b, tot, phase);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Multi-GPU scalar kernels: the rank sums were allgathered into b.part[0 .. world*NSLOT); sum them
+// in rank order (identical on every rank) and run the scalar logic (Alg. 1 "Central" lines).
+// ------------------------------------------------------------------------------------------------
+__global__ void k_scalar_after_value(Buffers b, int world) {
+    ScgState* s = b.st;
+    if (s->done) return;
+    double t[NSLOT] = {0, 0, 0, 0};
+    for (int r = 0; r < world; ++r)
+        for (int k = 0; k < NSLOT; ++k) t[k] += b.part[r * NSLOT + k];
+    scg_after_value(s, t, b.trace, PH_ITER);
+}
+
+__global__ void k_scalar_after_curv(Buffers b, int world) {
+    ScgState* s = b.st;
+    if (s->done) return;
+    if (!s->success) { scg_pre_value(s); return; }
+    double t[NSLOT] = {0, 0, 0, 0};
+    for (int r = 0; r < world; ++r)
+        for (int k = 0; k < NSLOT; ++k) t[k] += b.part[r * NSLOT + k];
+    scg_after_curv(s, t);
+}
+
+__global__ void k_state_init(ScgState* s, double lam0, double lambda_reg, int n_iter, long long npix) {
+    s->f = 0; s->f_new = 0; s->lam = lam0; s->lamb = 0; s->delta = 0; s->pp = 0; s->mu = 0;
+    s->alpha = 0; s->beta = 0; s->rr = 0; s->lambda_reg = lambda_reg;
+    for (int i = 0; i < 8; ++i) s->dbg[i] = 0;
+    s->alpha_f = 0; s->alpha_upd_f = 0; s->beta_f = 0;
+    s->npix = npix; s->k = 0; s->n_iter = n_iter; s->success = 1; s->done = 0;
+    s->xcur = 0; s->rcur = 0; s->accepted = 0; s->converged_at = -1; s->failed_stage = 0; s->failed_iter = -1;
+    s->counter = 0;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Ingest (polyphase relayout), bilinear initial estimate, finalize, debug forward/adjoint.
+// ------------------------------------------------------------------------------------------------
+__global__ void k_ingest(IngestParams ip, const float* __restrict__ lr, float* __restrict__ Y) {
+    int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    int gy = ip.store_lo + blockIdx.y;
+    if (gx >= ip.W || gy >= ip.store_hi) return;
+    int ph = (gy % ip.mag) * ip.mag + (gx % ip.mag);
+    int f = ip.frame_of_phase[ph];
+    int a = (gy - ip.sy[f]) / ip.mag, c = (gx - ip.sx[f]) / ip.mag;
+    Y[(size_t)(gy - ip.store_lo) * ip.pitch + gx] = __ldg(lr + ((size_t)f * ip.lr_h + a) * ip.lr_w + c);
+}
+
+__global__ void k_egest(IngestParams ip, const float* __restrict__ Yhr, float* __restrict__ lr) {
+    int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    int gy = ip.store_lo + blockIdx.y;
+    if (gx >= ip.W || gy >= ip.store_hi) return;
+    int ph = (gy % ip.mag) * ip.mag + (gx % ip.mag);
+    int f = ip.frame_of_phase[ph];
+    int a = (gy - ip.sy[f]) / ip.mag, c = (gx - ip.sx[f]) / ip.mag;
+    lr[((size_t)f * ip.lr_h + a) * ip.lr_w + c] = Yhr[(size_t)(gy - ip.store_lo) * ip.pitch + gx];
+}
+
+// x0(u,v) = bilerp(y_0, (u - t0y)/mag, (v - t0x)/mag), LR indices clamped (reading 14).
+__global__ void k_init_x0(IngestParams ip, const float* __restrict__ lr, float* __restrict__ X) {
+    int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    int gy = ip.store_lo + blockIdx.y;
+    if (gx >= ip.W || gy >= ip.store_hi) return;
+    float a = ((float)gy - ip.t0y) / (float)ip.mag, c = ((float)gx - ip.t0x) / (float)ip.mag;
+    float a0 = floorf(a), c0 = floorf(c);
+    float fa = a - a0, fc = c - c0;
+    int ia0 = clampi((int)a0, 0, ip.lr_h - 1), ia1 = clampi((int)a0 + 1, 0, ip.lr_h - 1);
+    int ic0 = clampi((int)c0, 0, ip.lr_w - 1), ic1 = clampi((int)c0 + 1, 0, ip.lr_w - 1);
+    const float* y = lr;
+    float v = (1.f - fa) * (1.f - fc) * __ldg(y + (size_t)ia0 * ip.lr_w + ic0) +
+              (1.f - fa) * fc * __ldg(y + (size_t)ia0 * ip.lr_w + ic1) +
+              fa * (1.f - fc) * __ldg(y + (size_t)ia1 * ip.lr_w + ic0) + fa * fc * __ldg(y + (size_t)ia1 * ip.lr_w + ic1);
+    X[(size_t)(gy - ip.store_lo) * ip.pitch + gx] = v;
+}
+
+// out = x + alpha_upd p when the last step was accepted and not yet applied (fused with the copy
+// into the caller's buffer; Alg. 1 line 24 for the owned rows).
+__global__ void k_finalize(StencilParams sp, Buffers b, float* __restrict__ out, int out_pitch, int row_lo, int row_hi) {
+    int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    int gy = row_lo + blockIdx.y;
+    if (gx >= sp.W || gy >= row_hi) return;
+    const ScgState* s = b.st;
+    float a = s->success ? s->alpha_upd_f : 0.0f;
+    size_t off = (size_t)(gy - sp.store_lo) * sp.pitch + gx;
+    out[(size_t)gy * out_pitch + gx] = fmaf(a, b.P[s->xcur][off], b.X[s->xcur][off]);
+}
+
+template <int KR>
+__global__ void k_forward_debug(StencilParams sp, const float* __restrict__ x, float* __restrict__ z) {
+    int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    int gy = sp.row_lo + blockIdx.y;
+    if (gx >= sp.W || gy >= sp.row_hi) return;
+    constexpr int KD = 2 * KR + 1;
+    float acc = 0.0f;
+    for (int P_ = 0; P_ < KD; ++P_)
+        for (int Q_ = 0; Q_ < KD; ++Q_) {
+            int uy = clampi(gy + P_ - KR, 0, sp.H - 1), ux = clampi(gx + Q_ - KR, 0, sp.W - 1);
+            acc = fmaf(sp.taps[P_ * KD + Q_], x[(size_t)(uy - sp.store_lo) * sp.pitch + ux], acc);
+        }
+    z[(size_t)(gy - sp.store_lo) * sp.pitch + gx] = acc;
+}
+
+template <int KR>
+__global__ void k_adjoint_debug(StencilParams sp, const float* __restrict__ w, float* __restrict__ g) {
+    int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    int gy = sp.row_lo + blockIdx.y;
+    if (gx >= sp.W || gy >= sp.row_hi) return;
+    constexpr int KD = 2 * KR + 1;
+    const int H = sp.H, W = sp.W;
+    int ylo = (gy == 0) ? -KR : gy, yhi = (gy == H - 1) ? H - 1 + KR : gy;
+    int xlo = (gx == 0) ? -KR : gx, xhi = (gx == W - 1) ? W - 1 + KR : gx;
+    float acc = 0.0f;
+    for (int yy = ylo; yy <= yhi; ++yy)
+        for (int xx = xlo; xx <= xhi; ++xx)
+            for (int P_ = 0; P_ < KD; ++P_)
+                for (int Q_ = 0; Q_ < KD; ++Q_) {
+                    int uy = yy - (P_ - KR), ux = xx - (Q_ - KR);
+                    if (uy < 0 || uy >= H || ux < 0 || ux >= W) continue;
+                    acc = fmaf(sp.taps[P_ * KD + Q_], w[(size_t)(uy - sp.store_lo) * sp.pitch + ux], acc);
+                }
+    g[(size_t)(gy - sp.store_lo) * sp.pitch + gx] = acc;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Launchers
+// ------------------------------------------------------------------------------------------------
+#define FL_DISPATCH(KERNEL, KR_, BW_, PN_, GRID, ...)                                                  \
+    do {                                                                                               \
+        switch ((KR_) * 100 + (BW_) * 10 + (PN_)) {                                                    \
+            FL_CASE(KERNEL, 0, 1, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 0, 1, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 0, 2, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 0, 2, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 0, 3, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 0, 3, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 1, 1, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 1, 1, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 1, 2, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 1, 2, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 1, 3, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 1, 3, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 2, 1, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 2, 1, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 2, 2, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 2, 2, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 2, 3, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 2, 3, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 3, 1, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 3, 1, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 3, 2, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 3, 2, 2, GRID, __VA_ARGS__)    \
+            FL_CASE(KERNEL, 3, 3, 1, GRID, __VA_ARGS__) FL_CASE(KERNEL, 3, 3, 2, GRID, __VA_ARGS__)    \
+            default: return cudaErrorInvalidValue;                                                     \
+        }                                                                                              \
+    } while (0)
+#define FL_CASE(KERNEL, A, B, C, GRID, ...) \
+    case A * 100 + B * 10 + C: KERNEL<A, B, C><<<GRID, NTHREADS, 0, s>>>(__VA_ARGS__); break;
+
+cudaError_t launch_value_grad(int kr, int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
+                              cudaStream_t s) {
+    dim3 grid(sp.tiles_x, sp.tiles_y);
+    FL_DISPATCH(k_value_grad, kr, bw, pn, grid, sp, b, phase);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update_curv(int kr, int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
+                               cudaStream_t s) {
+    dim3 grid(sp.tiles_x, sp.tiles_y);
+    FL_DISPATCH(k_update_curv, kr, bw, pn, grid, sp, b, phase);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scalar_after_value(const Buffers& b, int world, cudaStream_t s) {
+    k_scalar_after_value<<<1, 1, 0, s>>>(b, world);
+    return cudaGetLastError();
+}
+cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s) {
+    k_scalar_after_curv<<<1, 1, 0, s>>>(b, world);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,
+                              cudaStream_t s) {
+    k_state_init<<<1, 1, 0, s>>>(b.st, lam0, lambda_reg, n_iter, npix);
+    return cudaGetLastError();
+}
+
+static dim3 rowgrid(int W, int rows) { return dim3((W + 255) / 256, rows); }
+
+cudaError_t launch_ingest(const IngestParams& ip, const float* lr, float* Y, cudaStream_t s) {
+    k_ingest<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, Y);
+    return cudaGetLastError();
+}
+cudaError_t launch_egest(const IngestParams& ip, const float* Yhr, float* lr, cudaStream_t s) {
+    k_egest<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, Yhr, lr);
+    return cudaGetLastError();
+}
+cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s) {
+    k_init_x0<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X);
+    return cudaGetLastError();
+}
+cudaError_t launch_finalize(const StencilParams& sp, const Buffers& b, float* out, int out_pitch, int row_lo,
+                            int row_hi, cudaStream_t s) {
+    k_finalize<<<rowgrid(sp.W, row_hi - row_lo), 256, 0, s>>>(sp, b, out, out_pitch, row_lo, row_hi);
+    return cudaGetLastError();
+}
+cudaError_t launch_forward_debug(int kr, const StencilParams& sp, const float* x, float* z, cudaStream_t s) {
+    dim3 g = rowgrid(sp.W, sp.row_hi - sp.row_lo);
+    switch (kr) {
+        case 0: k_forward_debug<0><<<g, 256, 0, s>>>(sp, x, z); break;
+        case 1: k_forward_debug<1><<<g, 256, 0, s>>>(sp, x, z); break;
+        case 2: k_forward_debug<2><<<g, 256, 0, s>>>(sp, x, z); break;
+        case 3: k_forward_debug<3><<<g, 256, 0, s>>>(sp, x, z); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+cudaError_t launch_adjoint_debug(int kr, const StencilParams& sp, const float* w, float* g, cudaStream_t s) {
+    dim3 gr = rowgrid(sp.W, sp.row_hi - sp.row_lo);
+    switch (kr) {
+        case 0: k_adjoint_debug<0><<<gr, 256, 0, s>>>(sp, w, g); break;
+        case 1: k_adjoint_debug<1><<<gr, 256, 0, s>>>(sp, w, g); break;
+        case 2: k_adjoint_debug<2><<<gr, 256, 0, s>>>(sp, w, g); break;
+        case 3: k_adjoint_debug<3><<<gr, 256, 0, s>>>(sp, w, g); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace flmisr

@@ -1,0 +1,184 @@
+"""Thin Python binding of the C ABI in include/flmisr.h (argument marshalling only).
+
+Every step of the reconstruction runs in the sm_100a kernels of libflmisr.so; this module only
+converts torch tensors / numpy arrays into pointers and the config struct.  There is no CPU
+fallback: if the library is missing the import of this module fails loudly.
+
+Names follow the C ABI: ``plan`` / ``reconstruct`` / ``destroy``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libflmisr.so")
+
+OK, ERR_CONFIG, ERR_SHAPE, ERR_CUDA, ERR_NCCL, ERR_NUMERIC = 0, -1, -2, -3, -4, -5
+OP_FORWARD, OP_ADJOINT, OP_GRAD, OP_CURV, OP_VALUE, OP_X0 = range(6)
+
+
+class FlmisrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"flmisr status {status}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("k", C.c_int32), ("lr_h", C.c_int32), ("lr_w", C.c_int32),
+        ("shifts", C.POINTER(C.c_double)),
+        ("psf", C.POINTER(C.c_double)), ("psf_h", C.c_int32), ("psf_w", C.c_int32),
+        ("mag", C.c_int32), ("p_norm", C.c_int32),
+        ("l1_eps", C.c_double), ("lam", C.c_double), ("btv_alpha", C.c_double),
+        ("btv_window", C.c_int32), ("n_iter", C.c_int32),
+        ("scg_sigma0", C.c_double), ("scg_lambda0", C.c_double),
+        ("rank", C.c_int32), ("world", C.c_int32),
+        ("nccl_unique_id", C.c_void_p), ("device", C.c_int32),
+    ]
+
+
+class Report(C.Structure):
+    _fields_ = [("iters_run", C.c_int32), ("accepted", C.c_int32), ("converged_at", C.c_int32),
+                ("failed_stage", C.c_int32), ("failed_iter", C.c_int32),
+                ("f_trace", C.POINTER(C.c_double))]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2108_04315_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    lib.flmisr_plan.argtypes = [C.POINTER(Config), C.POINTER(vp)]
+    lib.flmisr_reconstruct.argtypes = [vp, vp, vp, vp, vp, C.POINTER(Report)]
+    lib.flmisr_reconstruct_host.argtypes = [vp, vp, vp, C.POINTER(Report)]
+    lib.flmisr_destroy.argtypes = [vp]
+    lib.flmisr_last_error.restype = C.c_char_p
+    lib.flmisr_nccl_unique_id.argtypes = [vp]
+    lib.flmisr_plan_info.argtypes = [vp] + [C.POINTER(C.c_int32)] * 5
+    lib.flmisr_debug_apply.argtypes = [vp, C.c_int32, vp, vp, vp, vp, C.POINTER(C.c_double)]
+    for f in ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_host", "flmisr_destroy",
+              "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply"):
+        getattr(lib, f).restype = C.c_int
+    return lib
+
+
+_lib = _load()
+EXPORTS = ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_host", "flmisr_destroy",
+           "flmisr_last_error", "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply")
+
+
+def _check(st: int):
+    if st != OK:
+        raise FlmisrError(st, _lib.flmisr_last_error().decode())
+
+
+def last_error() -> str:
+    return _lib.flmisr_last_error().decode()
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.flmisr_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return buf.raw
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return C.c_void_p(t.data_ptr())
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data_as(C.c_void_p)
+    raise TypeError(type(t))
+
+
+class Plan:
+    """flmisr_plan(): one plan per (geometry, parameters, rank); reusable across projections."""
+
+    def __init__(self, k, lr_h, lr_w, shifts, psf, mag=2, p_norm=1, l1_eps=1e-3, lam=0.05,
+                 btv_alpha=0.4, btv_window=3, n_iter=20, scg_sigma0=1e-4, scg_lambda0=1e-6,
+                 rank=0, world=1, nccl_id: bytes | None = None, device=0):
+        self.shifts = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(k, 2))
+        self.psf = np.ascontiguousarray(np.asarray(psf, dtype=np.float64))
+        self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        cfg = Config(k, lr_h, lr_w, self.shifts.ctypes.data_as(C.POINTER(C.c_double)),
+                     self.psf.ctypes.data_as(C.POINTER(C.c_double)), self.psf.shape[0], self.psf.shape[1],
+                     mag, p_norm, l1_eps, lam, btv_alpha, btv_window, n_iter, scg_sigma0, scg_lambda0,
+                     rank, world, C.cast(self._id, C.c_void_p) if self._id is not None else None, device)
+        self.k, self.lr_h, self.lr_w, self.mag, self.n_iter = k, lr_h, lr_w, mag, n_iter
+        self.rank, self.world, self.device = rank, world, device
+        self._h = C.c_void_p()
+        _check(_lib.flmisr_plan(C.byref(cfg), C.byref(self._h)))
+        vals = [C.c_int32() for _ in range(5)]
+        _check(_lib.flmisr_plan_info(self._h, *[C.byref(v) for v in vals]))
+        self.H, self.W, self.row_lo, self.row_hi, self.fast_path = [v.value for v in vals]
+
+    def destroy(self):
+        if self._h:
+            _lib.flmisr_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.destroy()
+
+    def _report(self, rep: Report, trace: np.ndarray) -> dict:
+        return dict(iters_run=rep.iters_run, accepted=rep.accepted, converged_at=rep.converged_at,
+                    failed_stage=rep.failed_stage, failed_iter=rep.failed_iter,
+                    trace=trace[: rep.iters_run + 1].copy())
+
+    def reconstruct(self, lr_stack, x0=None, out=None, stream=None, raise_numeric=True):
+        """flmisr_reconstruct on device tensors: lr_stack (k, lr_h, lr_w) fp32 CUDA; returns (hr, report)."""
+        import torch
+        if out is None:
+            out = torch.empty((self.H, self.W), dtype=torch.float32, device=lr_stack.device)
+        trace = np.zeros((self.n_iter + 1, 6))
+        rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
+        s = C.c_void_p(stream.cuda_stream) if stream is not None else C.c_void_p(
+            torch.cuda.current_stream(lr_stack.device).cuda_stream)
+        st = _lib.flmisr_reconstruct(self._h, _ptr(lr_stack), _ptr(x0), _ptr(out), s, C.byref(rep))
+        if st != OK and (raise_numeric or st != ERR_NUMERIC):
+            _check(st)
+        return out, self._report(rep, trace)
+
+    def reconstruct_host(self, lr_stack: np.ndarray, out: np.ndarray | None = None):
+        """flmisr_reconstruct_host: host fp32 in, host fp32 out (H2D/D2H inside the call)."""
+        lr = np.ascontiguousarray(lr_stack, dtype=np.float32)
+        if out is None:
+            out = np.empty((self.H, self.W), dtype=np.float32)
+        trace = np.zeros((self.n_iter + 1, 6))
+        rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
+        _check(_lib.flmisr_reconstruct_host(self._h, _ptr(lr), _ptr(out), C.byref(rep)))
+        return out, self._report(rep, trace)
+
+    def debug(self, op: int, lr=None, in0=None, in1=None, out=None):
+        sc = (C.c_double * 4)()
+        _check(_lib.flmisr_debug_apply(self._h, op, _ptr(lr), _ptr(in0), _ptr(in1), _ptr(out), sc))
+        return list(sc)
+
+
+# ---- functional names mirroring the C ABI ----
+def plan(**kw) -> Plan:
+    return Plan(**kw)
+
+
+def reconstruct(p: Plan, lr_stack, x0=None, out=None, stream=None):
+    return p.reconstruct(lr_stack, x0=x0, out=out, stream=stream)
+
+
+def destroy(p: Plan):
+    p.destroy()

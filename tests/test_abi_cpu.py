@@ -1,0 +1,66 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/flmisr.h
+declares, and rejects invalid configurations before any GPU work."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2108_04315_b200 import build as fbuild
+from paper_2108_04315_b200 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def fl():
+    fbuild.build()
+    import torch  # noqa: F401  (maps the torch-bundled libnccl.so.2 like a real caller)
+    from paper_2108_04315_b200 import flmisr
+    return flmisr
+
+
+def test_exports_every_declared_symbol(fl):
+    hdr = open(os.path.join(ROOT, "include", "flmisr.h")).read()
+    declared = set(re.findall(r"^\s*(?:flmisr_status|const char\*)\s+(flmisr_\w+)\(", hdr, re.M))
+    assert {"flmisr_plan", "flmisr_reconstruct", "flmisr_destroy"} <= declared
+    for name in declared:
+        assert hasattr(fl._lib, name), name
+    assert declared == set(fl.EXPORTS)
+
+
+def cfg(**kw):
+    base = dict(k=4, lr_h=16, lr_w=16, shifts=synth.shift_pattern(2), psf=synth.gaussian_psf(), mag=2)
+    base.update(kw)
+    return base
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(psf=np.ones((3, 3))), "sum to 1"),
+    (dict(psf=np.ones((2, 2)) / 4), "odd"),
+    (dict(psf=-synth.gaussian_psf() + 2 / 9), ">= 0"),
+    (dict(k=0, shifts=np.zeros((0, 2))), "k must be"),
+    (dict(p_norm=3), "p_norm"),
+    (dict(l1_eps=0.0), "l1_eps"),
+    (dict(btv_alpha=1.0), "btv_alpha"),
+    (dict(btv_window=4), "btv_window"),
+    (dict(lam=-1.0), "lambda"),
+    (dict(mag=5), "mag"),
+    (dict(k=3, shifts=synth.shift_pattern(2)[:3]), "unsupported geometry"),
+    (dict(shifts=np.array([[0, 0], [0, .5], [.5, .5], [.5, .5]])), "unsupported geometry"),
+    (dict(shifts=np.array([[0, 0], [0, .5], [.5, .5], [.5, .25]])), "unsupported geometry"),
+])
+def test_config_errors_raised_before_gpu_work(fl, kw, msg):
+    c = cfg(**kw)
+    with pytest.raises(fl.FlmisrError) as ei:
+        fl.Plan(**c)
+    assert ei.value.status == fl.ERR_CONFIG
+    assert msg in str(ei.value)
+
+
+def test_band_too_small_names_minimum_height(fl):
+    c = cfg(lr_h=2, lr_w=16, world=4, rank=0, nccl_id=b"\0" * 128)
+    with pytest.raises(fl.FlmisrError) as ei:
+        fl.Plan(**c)
+    assert ei.value.status == fl.ERR_CONFIG
+    assert "minimum HR height" in str(ei.value)
