@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""FL-MISR SCG reconstruction benchmark (BASELINE.json metric: HR projections/sec and SCG iter/s
+at 1/2/4/8 B200; % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl flmisr|reference] [--config C3]
+
+A step is one whole reconstruction of one HR projection (every SURVEY 8(a) row: ingest, initial
+estimate, init value/gradient, n_iter SCG passes of update+curvature and value+gradient with the
+on-device scalar logic, output) from an LR stack already resident in HBM.  Workload (default C3):
+K=4 LR 2048x2048 -> x2 SR 4096x4096 (16.8 MP HR), 20 SCG passes, synthetic phantom (DESIGN.md
+section 4).  L2 (126 MB) is flushed before every timed step by a 512 MiB device write.
+
+--impl reference times the fp64 CPU oracle (oracle/) as it stands on this host on a bounded row-band
+sample of the same workload; under torchrun only rank 0 runs it.
+Multi-GPU (torchrun, N > 1): every rank runs its own projection (replicas; SURVEY 8(e) "Replicas")
+until the partitioned row-band path is enabled with --mode partitioned.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2108_04315_b200 import synth  # noqa: E402
+
+METRIC = "HR projections/sec and SCG iter/s at 1/2/4/8 B200; % of HBM roofline"
+WORKLOADS = {
+    "C2": "C2: K=4 LR 1024x1024 -> x2 SR 2048x2048 (4.2 MP HR), 50 SCG passes",
+    "C3": "C3: K=4 LR 2048x2048 -> x2 SR 4096x4096 (16.8 MP HR), 20 SCG passes",
+    "C4": "C4: K=9 LR 2048x2048 -> x3 SR 6144x6144 (37.7 MP HR), 20 SCG passes",
+}
+# algorithmic HBM bytes per HR pixel per launch
+BYTES_VALUE_GRAD = 20   # read x, p, Y, r_old; write r_new
+BYTES_UPDATE_CURV = 24  # read x, p, r, Y; write x, p
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev, self.proc, self.out = dev, None, ""
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.dev), "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+_INPUTS = {}
+
+
+def make_inputs(cfg: str):
+    if cfg not in _INPUTS:
+        c = synth.CONFIGS[cfg]
+        y, sh, _ = synth.make_stack(c["lr"], c["mag"], seed=c["seed"])
+        _INPUTS[cfg] = (y, sh, c)
+    return _INPUTS[cfg]
+
+
+# ------------------------------------------------------------------------------------------ oracle
+def oracle_band_sample(cfg: str, rows: int, n_iter: int, seed_off: int = 0):
+    """Time the fp64 oracle (single-threaded C) on an HR row band of the workload: returns seconds."""
+    from oracle import oracle as orc
+    c = synth.CONFIGS[cfg]
+    mag = c["mag"]
+    lr_rows = rows // mag
+    y, sh, _ = make_inputs(cfg)
+    yb = np.ascontiguousarray(y[:, :lr_rows, :]).astype(np.float64)
+    pb = orc.Problem(k=len(sh), lr_h=lr_rows, lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=mag)
+    t = time.perf_counter()
+    orc.scg(pb, yb, n_iter)
+    return time.perf_counter() - t
+
+
+def cpu_baseline(cfg: str, n_iter_full: int):
+    """cpu_baseline leg: oracle on a half-height band, init (0 passes) and 2 passes -> extrapolated proj/s."""
+    c = synth.CONFIGS[cfg]
+    H = c["lr"] * c["mag"]
+    rows = H // 2
+    t0 = oracle_band_sample(cfg, rows, 0)
+    t2 = oracle_band_sample(cfg, rows, 2)
+    t_pass = (t2 - t0) / 2.0
+    t_proj = (H / rows) * (t0 + n_iter_full * t_pass)
+    return {"value": 1.0 / t_proj, "unit": "proj/s", "cores": 1, "kind": "oracle",
+            "sample": f"{cfg} HR band {rows}x{H} (1/{H // rows} of the projection): init {t0:.2f}s, "
+                      f"2 SCG passes {t2 - t0:.2f}s; projection = {H // rows} x (init + {n_iter_full} passes), "
+                      f"extrapolated; single-threaded fp64 C"}
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    cfg = args.config
+    c = synth.CONFIGS[cfg]
+    H = c["lr"] * c["mag"]
+    rows = 128
+    n_full = c["n_iter"]
+    import oracle.oracle as orc
+    orc.build()
+    t_init = [oracle_band_sample(cfg, rows, 0) for _ in range(max(args.warmup, 1))]
+    t0 = statistics.median(t_init)
+    steps = []
+    tr0 = time.perf_counter()
+    for _ in range(args.steps):
+        steps.append(oracle_band_sample(cfg, rows, 1))
+    wall = time.perf_counter() - tr0
+    t_step = statistics.mean(steps)
+    t_pass = max(t_step - t0, 1e-9)
+    t_proj = (H / rows) * (t0 + n_full * t_pass)
+    val = 1.0 / t_proj
+    sample = (f"{cfg} HR row band {rows}x{H} (1/{H // rows} of the projection); warm-up steps time init, "
+              f"each timed step = init + 1 SCG pass ({t_step:.3f}s); projection = {H // rows} x (init + "
+              f"{n_full} passes), extrapolated; single-threaded fp64 C oracle")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "proj/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOADS[cfg], "n_iter": n_full, "l2": "n/a (CPU)"},
+            "cpu_baseline": {"value": val, "unit": "proj/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "proj/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "scg_iters_per_s": n_full * val, "wall_s": wall}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ GPU arm
+def run_flmisr(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2108_04315_b200 import flmisr
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = args.config
+    y, sh, c = make_inputs(cfg)
+    k, lr, mag, n_iter = len(sh), c["lr"], c["mag"], c["n_iter"]
+    H = W = lr * mag
+    npx = H * W
+    pl = flmisr.Plan(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, p_norm=1,
+                     l1_eps=1e-3, lam=0.05, btv_alpha=0.4, btv_window=3, n_iter=n_iter, device=local)
+    dev = torch.device("cuda", local)
+    y_d = torch.from_numpy(y).to(dev)
+    out_d = torch.empty((H, W), dtype=torch.float32, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    s = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        pl.reconstruct(y_d, out=out_d)
+    torch.cuda.synchronize()
+
+    pl.profile(1)
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    accepted = []
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(s)
+        pl.reconstruct_async(y_d, out_d, stream=s)
+        ev[i][1].record(s)
+        rep = pl.finish()
+        accepted.append(rep["accepted"])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    prof = pl.profile(0)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = world * args.steps / (tot_ms / 1000.0)   # replicas: every rank finished `steps` projections
+
+    # e2e through the public host API: pinned host LR stack in, pinned host HR image out
+    y_h = torch.from_numpy(y).pin_memory()
+    o_h = torch.empty((H, W), dtype=torch.float32).pin_memory()
+    y_np, o_np = y_h.numpy(), o_h.numpy()
+    pl.reconstruct_host(y_np, o_np)
+    e2e_steps = max(3, min(args.steps, 20))
+    if world > 1:
+        dist.barrier()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        pl.reconstruct_host(y_np, o_np)
+    e2e_s = time.perf_counter() - t
+    if world > 1:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e = {"value": world * e2e_steps / e2e_s, "unit": "proj/s", "h2d_bytes_per_step": int(y.nbytes),
+           "d2h_bytes_per_step": int(npx * 4)}
+
+    peak, peak_src = load_peaks()
+    vg = prof["value_grad"]
+    uc = prof["update_curv"]
+    vg_ms = vg["ms"] / max(vg["launches"], 1)
+    uc_ms = uc["ms"] / max(uc["launches"], 1)
+    achieved = BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(cfg, {}).get("value_grad")
+    launches_per_step = 5 + 2 * n_iter
+    line = {
+        "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[cfg], "n_iter": n_iter, "hr": [H, W], "p_norm": 1, "lambda": 0.05,
+                   "btv_alpha": 0.4, "btv_window": 3, "psf": "3x3 Gaussian sigma 0.5",
+                   "l2": "flushed before every timed step (512 MiB device write)",
+                   "parallelism": "single GPU" if world == 1 else f"replicas x{world}"},
+        "scg_iters_per_s": value * n_iter,
+        "accepted_fraction": float(np.mean(accepted)) / n_iter if n_iter else None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_value_grad",
+                     "algorithmic_bytes_per_launch": BYTES_VALUE_GRAD * npx, "avg_launch_ms": vg_ms,
+                     "peak_source": peak_src},
+        "kernels": {"value_grad": {"avg_ms": vg_ms, "launches": vg["launches"],
+                                   "gbs": BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9},
+                    "update_curv": {"avg_ms": uc_ms, "launches": uc["launches"],
+                                    "gbs_if_full": BYTES_UPDATE_CURV * npx / (uc_ms / 1000.0) / 1e9 if uc_ms else None},
+                    "setup_finalize_ms_per_step": prof["setup_finalize"]["ms"] / max(prof["setup_finalize"]["launches"], 1)},
+        "clocks": clocks,
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as orc
+        orc.build()
+        line["cpu_baseline"] = cpu_baseline(cfg, n_iter)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    pl.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="flmisr", choices=["flmisr", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "flmisr" else args.warmup
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_flmisr(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

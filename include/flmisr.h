@@ -102,7 +102,26 @@ flmisr_status flmisr_reconstruct(flmisr_plan_t plan, const float* lr_stack, cons
                                  void* cuda_stream, flmisr_report* report);
 
 /*
- * flmisr_reconstruct_host: flmisr_reconstruct for HOST buffers (end-to-end path): lr_stack_host
+ * flmisr_reconstruct_async / flmisr_finish: the two halves of flmisr_reconstruct.  _async enqueues the
+ * whole reconstruction (same arguments and errors as flmisr_reconstruct) plus the status read-back and
+ * returns without synchronising; flmisr_finish waits for it and fills `report` (nullable).  Exactly one
+ * _finish per _async; the caller's buffers must stay valid until _finish returns.  Used for streamed
+ * acquisition and for timing the device work without host latency.
+ */
+flmisr_status flmisr_reconstruct_async(flmisr_plan_t plan, const float* lr_stack, const float* x0, float* hr_out,
+                                       void* cuda_stream);
+flmisr_status flmisr_finish(flmisr_plan_t plan, flmisr_report* report);
+
+/*
+ * flmisr_profile: per-kernel CUDA-event timing on the launching stream.  enable = 1 turns it on and
+ * resets the counters, 0 turns it off and resets, -1 only reads.  out8 (nullable, host, 8 doubles)
+ * receives {launches, total ms} for: [0] value+gradient kernel, [1] update+curvature kernel,
+ * [2] setup+finalize (ingest, x0, state, output), [3] whole reconstructions.
+ */
+flmisr_status flmisr_profile(flmisr_plan_t plan, int32_t enable, double* out8);
+
+/*
+ * flmisr_reconstruct_host:flmisr_reconstruct for HOST buffers (end-to-end path): lr_stack_host
  * (k x lr_h x lr_w fp32) is staged through the plan's pinned buffer and copied H2D, hr_out_host
  * (H x W fp32; rank 0 / world 1) receives the D2H copy.  Same errors as flmisr_reconstruct.
  */

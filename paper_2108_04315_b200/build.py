@@ -12,8 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libflmisr.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("flmisr_kernels.cu", "flmisr_api.cpp")]
-HEADERS = [os.path.join(CSRC, "flmisr_internal.h"), os.path.join(ROOT, "include", "flmisr.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("flmisr_kernels.cu", "flmisr_stream.cu", "flmisr_api.cpp")]
+HEADERS = [os.path.join(CSRC, "flmisr_internal.h"), os.path.join(CSRC, "flmisr_common.cuh"), os.path.join(ROOT, "include", "flmisr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

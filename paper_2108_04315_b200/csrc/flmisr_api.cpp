@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -85,12 +86,21 @@ NcclApi& nccl() {
 
 }  // namespace
 
+// Optional per-kernel timing with CUDA events on the launching stream (bench.py roofline).
+struct Prof {
+    bool enabled = false;
+    std::vector<cudaEvent_t> ev;
+    double ms[4] = {0, 0, 0, 0};   // value_grad, update_curv, other (setup + finalize), whole call
+    long long n[4] = {0, 0, 0, 0};
+};
+
 struct flmisr_plan_s {
     flmisr_config cfg{};
     std::vector<double> shifts, psf;
     int H = 0, W = 0, pitch = 0, kr = 0, bw = 0, pn = 1, eta = 0;
     int row_lo = 0, row_hi = 0, store_lo = 0, store_hi = 0;
     int fast = 0;
+    int stream_path = 0;   // 1: register-streaming kernels (flmisr_stream.cu), 0: tiled kernels
     StencilParams sp{};
     IngestParams ip{};
     Buffers b{};
@@ -109,6 +119,11 @@ struct flmisr_plan_s {
     float* recv_top = nullptr;
     float* recv_bot = nullptr;
     double* gathered = nullptr;
+    cudaEvent_t done_ev = nullptr;
+    cudaStream_t last_stream = nullptr;
+    int pending = 0;
+    int prof_marks = 0;
+    Prof prof;
 };
 
 namespace {
@@ -274,6 +289,60 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
         for (int dy = 0; dy < c.btv_window; ++dy)
             for (int dx = 0; dx < c.btv_window; ++dx)
                 if (dy || dx) sp.gam[dy * MAXBW + dx] = (float)std::pow(c.btv_alpha, dx + dy);
+        for (int cl = 0; cl < 4; ++cl) sp.gcls[cl] = std::pow(c.btv_alpha, cl + 1);
+        // identity affine correction (tiled kernels compute complete values)
+        for (int k = 0; k < NSLOT; ++k) {
+            sp.aff_vg[k] = 1.0; sp.aff_vg[NSLOT + k] = 0.0;
+            sp.aff_uc[k] = 1.0; sp.aff_uc[NSLOT + k] = 0.0;
+        }
+        // ---- streaming path (flmisr_stream.cu): separable kappa with KR <= 1, W % 4 == 0 ----
+        std::vector<double> K3(9, 0.0);   // kappa as a centred 3x3 (KR <= 1)
+        if (kr <= 1) {   // fp64 kappa (offsets [-R, R+1]) -> centred 3x3
+            const int KD = 2 * R + 2;
+            for (int P = -1; P <= 1; ++P)
+                for (int Q = -1; Q <= 1; ++Q)
+                    if (P + R >= 0 && P + R < KD && Q + R >= 0 && Q + R < KD)
+                        K3[(P + 1) * 3 + (Q + 1)] = kap0[(size_t)(P + R) * KD + (Q + R)];
+        }
+        int pm = 0;
+        for (int i = 1; i < 9; ++i)
+            if (std::fabs(K3[i]) > std::fabs(K3[pm])) pm = i;
+        const int Pm = pm / 3, Qm = pm % 3;
+        double a3[3], b3[3], err = 0.0;
+        for (int i = 0; i < 3; ++i) { a3[i] = K3[i * 3 + Qm]; b3[i] = K3[Pm * 3 + i] / K3[pm]; }
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) err = std::max(err, std::fabs(K3[i * 3 + j] - a3[i] * b3[j]));
+        const bool separable = kr <= 1 && err <= 1e-12 * std::fabs(K3[pm]);
+        p->stream_path = separable && (p->W % 4 == 0) && p->W >= 8 && p->H >= 4 &&
+                         std::getenv("FLMISR_FORCE_TILED") == nullptr;
+        if (p->stream_path) {
+            for (int i = 0; i < 3; ++i) { sp.ka[i] = (float)a3[i]; sp.kb[i] = (float)b3[i]; }
+            sp.wpb = 8;
+            sp.nstrips = 1 + (p->W > SCOLS - SHALO ? (p->W - (SCOLS - SHALO) + SSTEP - 1) / SSTEP : 0);
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
+            const long long cap = (long long)nsm * 2 * sp.wpb;   // 2 CTAs of 8 warps per SM
+            const int rows = p->row_hi - p->row_lo;
+            int S = 16;
+            while (S < rows && (long long)sp.nstrips * ((rows + S - 1) / S) > cap) S += 3;
+            if (S > rows) S = rows + ((1 - rows % 3) + 3) % 3;   // smallest >= rows with S = 1 mod 3
+            sp.seg_rows = S;
+            sp.nsegs = (rows + S - 1) / S;
+            // hoisted constants: D = sum q rs - eps N, R = sum gamma q rs - eps sum_d gamma_d n_d,
+            // curvature sums carry eps^2 (p = 1) or 2 (p = 2)
+            const double eps = c.l1_eps;
+            double npairs_g = 0.0;
+            for (int dy = 0; dy < c.btv_window; ++dy)
+                for (int dx = 0; dx < c.btv_window; ++dx) {
+                    if (!dy && !dx) continue;
+                    const long long nr = std::max(0, std::min(p->row_hi, p->H - dy) - p->row_lo);
+                    npairs_g += std::pow(c.btv_alpha, dx + dy) * (double)nr * (double)(p->W - dx);
+                }
+            sp.aff_vg[NSLOT + 0] = c.p_norm == 1 ? -eps * (double)rows * p->W : 0.0;
+            sp.aff_vg[NSLOT + 1] = -eps * npairs_g;
+            sp.aff_uc[0] = c.p_norm == 1 ? eps * eps : 2.0;
+            sp.aff_uc[1] = eps * eps;
+        }
     }
     IngestParams& ip = p->ip;
     ip.H = p->H; ip.W = p->W; ip.pitch = p->pitch; ip.k = K; ip.lr_h = c.lr_h; ip.lr_w = c.lr_w; ip.mag = mag;
@@ -301,7 +370,8 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
     b.X[0] = p->mem + 1 * fl; b.X[1] = p->mem + 2 * fl;
     b.P[0] = p->mem + 3 * fl; b.P[1] = p->mem + 4 * fl;
     b.R[0] = p->mem + 5 * fl; b.R[1] = p->mem + 6 * fl;
-    const size_t ntiles = (size_t)sp.tiles_x * sp.tiles_y;
+    const size_t nsblk = p->stream_path ? ((size_t)sp.nstrips * sp.nsegs + sp.wpb - 1) / sp.wpb : 0;
+    const size_t ntiles = std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk);
     const size_t npart = std::max<size_t>(NSLOT * ntiles, (size_t)NSLOT * world);
     const size_t ntrace = (size_t)(c.n_iter + 1) * 6;
     const size_t nd = npart + NSLOT + ntrace + (size_t)NSLOT * world;
@@ -316,6 +386,8 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc state: ") + cudaGetErrorString(e)));
     cudaMemset(p->st, 0, sizeof(ScgState));
     b.st = p->st;
+    e = cudaEventCreateWithFlags(&p->done_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaEventCreate"));
     e = cudaMallocHost(&p->st_host, sizeof(ScgState));
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMallocHost state"));
     e = cudaMallocHost(&p->trace_host, ntrace * sizeof(double));
@@ -367,7 +439,7 @@ flmisr_status flmisr_plan_info(flmisr_plan_t p, int32_t* H, int32_t* W, int32_t*
     if (W) *W = p->W;
     if (row_lo) *row_lo = p->row_lo;
     if (row_hi) *row_hi = p->row_hi;
-    if (fast_path) *fast_path = p->fast;
+    if (fast_path) *fast_path = p->fast ? (p->stream_path ? 2 : 1) : 0;
     return FLMISR_OK;
 }
 
@@ -386,6 +458,8 @@ flmisr_status flmisr_destroy(flmisr_plan_t p) {
     if (p->pin_out) cudaFreeHost(p->pin_out);
     if (p->d_lr) cudaFree(p->d_lr);
     if (p->d_out) cudaFree(p->d_out);
+    for (auto e : p->prof.ev) cudaEventDestroy(e);
+    if (p->done_ev) cudaEventDestroy(p->done_ev);
     if (p->stream) cudaStreamDestroy(p->stream);
     delete p;
     return FLMISR_OK;
@@ -398,7 +472,8 @@ namespace {
 // Enqueue one value+gradient pass and, for world > 1, the consensus allgather + scalar kernel and
 // the inner-outer border exchange of the r candidate.
 flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
-    CUDA_TRY(launch_value_grad(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
+    CUDA_TRY(p->stream_path ? launch_value_grad_stream(p->bw, p->pn, p->sp, p->b, phase, s)
+                            : launch_value_grad(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
     if (p->cfg.world > 1) {
         NcclApi& api = nccl();
         const int rank = p->cfg.rank, world = p->cfg.world;
@@ -421,7 +496,8 @@ flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
 }
 
 flmisr_status enqueue_update_curv(flmisr_plan_s* p, int phase, cudaStream_t s) {
-    CUDA_TRY(launch_update_curv(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
+    CUDA_TRY(p->stream_path ? launch_update_curv_stream(p->bw, p->pn, p->sp, p->b, phase, s)
+                            : launch_update_curv(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
     if (p->cfg.world > 1) {
         NCCL_TRY(nccl().AllGather(p->b.rank_sums, p->b.part, NSLOT, ncclFloat64, p->comm, s));
         CUDA_TRY(launch_scalar_after_curv(p->b, p->cfg.world, s));
@@ -429,41 +505,28 @@ flmisr_status enqueue_update_curv(flmisr_plan_s* p, int phase, cudaStream_t s) {
     return FLMISR_OK;
 }
 
-flmisr_status collect_report(flmisr_plan_s* p, cudaStream_t s, flmisr_report* rep) {
-    const size_t ntrace = (size_t)(p->cfg.n_iter + 1) * 6;
-    CUDA_TRY(cudaMemcpyAsync(p->st_host, p->st, sizeof(ScgState), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(p->trace_host, p->b.trace, ntrace * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    const ScgState& h = *p->st_host;
-    if (rep) {
-        rep->iters_run = h.k;
-        rep->accepted = h.accepted;
-        rep->converged_at = h.converged_at;
-        rep->failed_stage = h.failed_stage;
-        rep->failed_iter = h.failed_iter;
-        if (rep->f_trace) std::memcpy(rep->f_trace, p->trace_host, ntrace * sizeof(double));
-    }
-    if (h.failed_stage)
-        return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar at SCG pass " + std::to_string(h.failed_iter) +
-                                            " (stage " + std::to_string(h.failed_stage) + ")");
-    return FLMISR_OK;
-}
-
 }  // namespace
 
 extern "C" {
 
-flmisr_status flmisr_reconstruct(flmisr_plan_t p, const float* lr_stack, const float* x0, float* hr_out,
-                                 void* cuda_stream, flmisr_report* report) {
+flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, const float* x0, float* hr_out,
+                                       void* cuda_stream) {
     if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
     if (!lr_stack) return fail(FLMISR_ERR_SHAPE, "lr_stack is NULL");
     if (!hr_out && (p->cfg.world == 1 || p->cfg.rank == 0)) return fail(FLMISR_ERR_SHAPE, "hr_out is NULL");
+    if (p->cfg.world > 1 && !hr_out) return fail(FLMISR_ERR_SHAPE, "hr_out is required on every rank for the band gather");
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->stream;
+    p->last_stream = s;
     const Buffers& b = p->b;
     const size_t srows = (size_t)(p->store_hi - p->store_lo);
+    Prof& pr = p->prof;
+    const bool prof = pr.enabled;
+    int ev = 0;
+    auto mark = [&]() -> cudaError_t { return prof ? cudaEventRecord(pr.ev[ev++], s) : cudaSuccess; };
 
     // a1: polyphase ingest; a2: initial estimate, p0 = 0, r_old = 0, state
+    CUDA_TRY(mark());
     CUDA_TRY(launch_ingest(p->ip, lr_stack, const_cast<float*>(b.Y), s));
     if (x0) {
         CUDA_TRY(cudaMemcpy2DAsync(b.X[0], p->pitch * sizeof(float), x0 + (size_t)p->store_lo * p->W,
@@ -474,15 +537,19 @@ flmisr_status flmisr_reconstruct(flmisr_plan_t p, const float* lr_stack, const f
     CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
     CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
     CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
+    CUDA_TRY(mark());  // ev1: end of setup
 
     // init: f0 = J(x0), r0 = -grad J(x0) (Moller step 1), then n_iter SCG passes (Alg. 1 while-loop)
     flmisr_status st = enqueue_value_grad(p, PH_INIT, s);
     if (st != FLMISR_OK) return st;
+    CUDA_TRY(mark());  // ev2
     for (int it = 0; it < p->cfg.n_iter; ++it) {
         st = enqueue_update_curv(p, PH_ITER, s);
         if (st != FLMISR_OK) return st;
+        CUDA_TRY(mark());
         st = enqueue_value_grad(p, PH_ITER, s);
         if (st != FLMISR_OK) return st;
+        CUDA_TRY(mark());
     }
     // a12: fuse (owned rows; rank 0 gathers the bands for world > 1)
     if (hr_out) CUDA_TRY(launch_finalize(p->sp, b, hr_out, p->W, p->row_lo, p->row_hi, s));
@@ -498,12 +565,79 @@ flmisr_status flmisr_reconstruct(flmisr_plan_t p, const float* lr_stack, const f
             }
             NCCL_TRY(api.GroupEnd());
         } else {
-            float* src = hr_out ? hr_out + (size_t)p->row_lo * p->W : nullptr;
-            if (!src) return fail(FLMISR_ERR_SHAPE, "hr_out is required on every rank for the band gather");
-            NCCL_TRY(api.Send(src, (size_t)(p->row_hi - p->row_lo) * p->W, ncclFloat32, 0, p->comm, s));
+            NCCL_TRY(api.Send(hr_out + (size_t)p->row_lo * p->W, (size_t)(p->row_hi - p->row_lo) * p->W, ncclFloat32,
+                              0, p->comm, s));
         }
     }
-    return collect_report(p, s, report);
+    CUDA_TRY(mark());  // last
+    const size_t ntrace = (size_t)(p->cfg.n_iter + 1) * 6;
+    CUDA_TRY(cudaMemcpyAsync(p->st_host, p->st, sizeof(ScgState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(p->trace_host, p->b.trace, ntrace * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(p->done_ev, s));
+    p->pending = 1;
+    p->prof_marks = ev;
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_finish(flmisr_plan_t p, flmisr_report* rep) {
+    if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    if (!p->pending) return fail(FLMISR_ERR_SHAPE, "no reconstruction in flight");
+    p->pending = 0;
+    CUDA_TRY(cudaEventSynchronize(p->done_ev));
+    const size_t ntrace = (size_t)(p->cfg.n_iter + 1) * 6;
+    const ScgState& h = *p->st_host;
+    if (rep) {
+        rep->iters_run = h.k;
+        rep->accepted = h.accepted;
+        rep->converged_at = h.converged_at;
+        rep->failed_stage = h.failed_stage;
+        rep->failed_iter = h.failed_iter;
+        if (rep->f_trace) std::memcpy(rep->f_trace, p->trace_host, ntrace * sizeof(double));
+    }
+    Prof& pr = p->prof;
+    if (pr.enabled && p->prof_marks >= 4) {
+        // marks: 0 start, 1 setup end, 2 init value/grad end, then (curv end, value end) per pass, last
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr.ev[0], pr.ev[1]); pr.ms[2] += ms;
+        cudaEventElapsedTime(&ms, pr.ev[1], pr.ev[2]); pr.ms[0] += ms; pr.n[0] += 1;
+        int m = 2;
+        for (int it = 0; it < p->cfg.n_iter; ++it) {
+            cudaEventElapsedTime(&ms, pr.ev[m], pr.ev[m + 1]); pr.ms[1] += ms; pr.n[1] += 1;
+            cudaEventElapsedTime(&ms, pr.ev[m + 1], pr.ev[m + 2]); pr.ms[0] += ms; pr.n[0] += 1;
+            m += 2;
+        }
+        cudaEventElapsedTime(&ms, pr.ev[m], pr.ev[m + 1]); pr.ms[2] += ms;
+        cudaEventElapsedTime(&ms, pr.ev[0], pr.ev[m + 1]); pr.ms[3] += ms; pr.n[3] += 1;
+        pr.n[2] += 1;
+    }
+    if (h.failed_stage)
+        return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar at SCG pass " + std::to_string(h.failed_iter) +
+                                            " (stage " + std::to_string(h.failed_stage) + ")");
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_reconstruct(flmisr_plan_t p, const float* lr_stack, const float* x0, float* hr_out,
+                                 void* cuda_stream, flmisr_report* report) {
+    flmisr_status st = flmisr_reconstruct_async(p, lr_stack, x0, hr_out, cuda_stream);
+    if (st != FLMISR_OK) return st;
+    return flmisr_finish(p, report);
+}
+
+flmisr_status flmisr_profile(flmisr_plan_t p, int32_t enable, double* out8) {
+    if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    Prof& pr = p->prof;
+    if (out8) {
+        for (int i = 0; i < 4; ++i) { out8[2 * i] = (double)pr.n[i]; out8[2 * i + 1] = pr.ms[i]; }
+    }
+    if (enable >= 0) {
+        for (int i = 0; i < 4; ++i) { pr.n[i] = 0; pr.ms[i] = 0.0; }
+        if (enable && pr.ev.empty()) {
+            pr.ev.resize((size_t)2 * p->cfg.n_iter + 8);
+            for (auto& e : pr.ev) CUDA_TRY(cudaEventCreate(&e));
+        }
+        pr.enabled = enable != 0;
+    }
+    return FLMISR_OK;
 }
 
 flmisr_status flmisr_reconstruct_host(flmisr_plan_t p, const float* lr_host, float* hr_host, flmisr_report* report) {
@@ -512,21 +646,36 @@ flmisr_status flmisr_reconstruct_host(flmisr_plan_t p, const float* lr_host, flo
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     const size_t nlr = (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w;
     const size_t nhr = (size_t)p->H * p->W;
-    if (!p->pin_in) {
-        CUDA_TRY(cudaMallocHost(&p->pin_in, nlr * sizeof(float)));
-        CUDA_TRY(cudaMallocHost(&p->pin_out, nhr * sizeof(float)));
+    if (!p->d_lr) {
         CUDA_TRY(cudaMalloc(&p->d_lr, nlr * sizeof(float)));
         CUDA_TRY(cudaMalloc(&p->d_out, nhr * sizeof(float)));
     }
-    std::memcpy(p->pin_in, lr_host, nlr * sizeof(float));
-    CUDA_TRY(cudaMemcpyAsync(p->d_lr, p->pin_in, nlr * sizeof(float), cudaMemcpyHostToDevice, p->stream));
-    flmisr_status st = flmisr_reconstruct(p, p->d_lr, nullptr, p->d_out, p->stream, report);
-    if (st != FLMISR_OK && st != FLMISR_ERR_NUMERIC) return st;
-    if (hr_host && (p->cfg.world == 1 || p->cfg.rank == 0)) {
-        CUDA_TRY(cudaMemcpyAsync(p->pin_out, p->d_out, nhr * sizeof(float), cudaMemcpyDeviceToHost, p->stream));
-        CUDA_TRY(cudaStreamSynchronize(p->stream));
-        std::memcpy(hr_host, p->pin_out, nhr * sizeof(float));
+    // page-locked caller buffers are DMA'd directly; pageable ones are staged through pinned memory
+    auto pinned = [](const void* ptr) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) { cudaGetLastError(); return false; }
+        return a.type == cudaMemoryTypeHost;
+    };
+    const float* src = lr_host;
+    if (!pinned(lr_host)) {
+        if (!p->pin_in) CUDA_TRY(cudaMallocHost(&p->pin_in, nlr * sizeof(float)));
+        std::memcpy(p->pin_in, lr_host, nlr * sizeof(float));
+        src = p->pin_in;
     }
+    CUDA_TRY(cudaMemcpyAsync(p->d_lr, src, nlr * sizeof(float), cudaMemcpyHostToDevice, p->stream));
+    flmisr_status st = flmisr_reconstruct_async(p, p->d_lr, nullptr, p->d_out, p->stream);
+    if (st != FLMISR_OK) return st;
+    const bool root = p->cfg.world == 1 || p->cfg.rank == 0;
+    float* dst = hr_host;
+    const bool direct = hr_host && pinned(hr_host);
+    if (hr_host && root) {
+        if (!direct && !p->pin_out) CUDA_TRY(cudaMallocHost(&p->pin_out, nhr * sizeof(float)));
+        dst = direct ? hr_host : p->pin_out;
+        CUDA_TRY(cudaMemcpyAsync(dst, p->d_out, nhr * sizeof(float), cudaMemcpyDeviceToHost, p->stream));
+        CUDA_TRY(cudaEventRecord(p->done_ev, p->stream));
+    }
+    st = flmisr_finish(p, report);
+    if (hr_host && root && !direct) std::memcpy(hr_host, p->pin_out, nhr * sizeof(float));
     return st;
 }
 
@@ -566,7 +715,8 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
             CUDA_TRY(put_hr(b.X[0], in0));
             CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
             CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
-            CUDA_TRY(launch_value_grad(p->kr, p->bw, p->pn, p->sp, b, PH_DEBUG, s));
+            CUDA_TRY(p->stream_path ? launch_value_grad_stream(p->bw, p->pn, p->sp, b, PH_DEBUG, s)
+                                    : launch_value_grad(p->kr, p->bw, p->pn, p->sp, b, PH_DEBUG, s));
             if (op == FLMISR_OP_GRAD && out) CUDA_TRY(get_hr(out, b.R[1]));
             break;
         case FLMISR_OP_CURV:
@@ -575,7 +725,8 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
             CUDA_TRY(put_hr(b.X[0], in0));
             CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
             CUDA_TRY(put_hr(b.R[0], in1));
-            CUDA_TRY(launch_update_curv(p->kr, p->bw, p->pn, p->sp, b, PH_DEBUG, s));
+            CUDA_TRY(p->stream_path ? launch_update_curv_stream(p->bw, p->pn, p->sp, b, PH_DEBUG, s)
+                                    : launch_update_curv(p->kr, p->bw, p->pn, p->sp, b, PH_DEBUG, s));
             break;
         case FLMISR_OP_X0:
             if (!lr || !out) return fail(FLMISR_ERR_SHAPE, "X0 needs lr and out");

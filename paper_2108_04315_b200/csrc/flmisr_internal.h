@@ -43,7 +43,18 @@ struct StencilParams {
     float eps, eps2, lam;        // Charbonnier eps, eps^2, BTV weight lambda (fp32 copies)
     float taps[MAXTAPS];         // kappa, (2KR+1)^2 centred, row-major, correlation orientation
     float gam[MAXBW * MAXBW];    // gamma(dy,dx) = alpha^(dx+dy) at [dy*MAXBW + dx], gam[0] unused
+    // streaming (separable-kappa) kernels, flmisr_stream.cu
+    float ka[3], kb[3];          // kappa(P,Q) = ka[P+1] * kb[Q+1] (KR <= 1; KR = 0 zero-padded)
+    int nstrips, nsegs, seg_rows, wpb;   // 128-column warp strips (step 124), row segments, warps/CTA
+    double gcls[4];              // gamma of BTV class dx+dy = 1..4 (fp64, applied to the CTA sums)
+    // affine correction of the raw CTA sums before the scalar logic: tot = raw * aff[k] + aff[4+k]
+    double aff_vg[2 * NSLOT], aff_uc[2 * NSLOT];
 };
+
+// Streaming kernels (flmisr_stream.cu): strips of SCOLS columns per warp, stepping by SSTEP.
+constexpr int SCOLS = 128;
+constexpr int SHALO = 2;
+constexpr int SSTEP = SCOLS - 2 * SHALO;
 
 struct Buffers {
     const float* Y;              // polyphase-interleaved LR stack on the HR grid (storage base)
@@ -68,6 +79,10 @@ cudaError_t launch_value_grad(int kr, int bw, int pn, const StencilParams& sp, c
                               cudaStream_t s);
 cudaError_t launch_update_curv(int kr, int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
                                cudaStream_t s);
+cudaError_t launch_value_grad_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
+                                     cudaStream_t s);
+cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
+                                      cudaStream_t s);
 cudaError_t launch_scalar_after_value(const Buffers& b, int world, cudaStream_t s);  // world > 1
 cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s);   // world > 1
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,

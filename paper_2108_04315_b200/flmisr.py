@@ -46,6 +46,11 @@ class Report(C.Structure):
                 ("f_trace", C.POINTER(C.c_double))]
 
 
+EXPORTS = ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_async", "flmisr_finish",
+           "flmisr_profile", "flmisr_reconstruct_host", "flmisr_destroy", "flmisr_last_error",
+           "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply")
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2108_04315_b200.build` "
@@ -55,20 +60,22 @@ def _load():
     lib.flmisr_plan.argtypes = [C.POINTER(Config), C.POINTER(vp)]
     lib.flmisr_reconstruct.argtypes = [vp, vp, vp, vp, vp, C.POINTER(Report)]
     lib.flmisr_reconstruct_host.argtypes = [vp, vp, vp, C.POINTER(Report)]
+    lib.flmisr_reconstruct_async.argtypes = [vp, vp, vp, vp, vp]
+    lib.flmisr_finish.argtypes = [vp, C.POINTER(Report)]
+    lib.flmisr_profile.argtypes = [vp, C.c_int32, C.POINTER(C.c_double)]
     lib.flmisr_destroy.argtypes = [vp]
     lib.flmisr_last_error.restype = C.c_char_p
     lib.flmisr_nccl_unique_id.argtypes = [vp]
     lib.flmisr_plan_info.argtypes = [vp] + [C.POINTER(C.c_int32)] * 5
     lib.flmisr_debug_apply.argtypes = [vp, C.c_int32, vp, vp, vp, vp, C.POINTER(C.c_double)]
-    for f in ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_host", "flmisr_destroy",
-              "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply"):
+    for f in EXPORTS:
+        if f == "flmisr_last_error":
+            continue
         getattr(lib, f).restype = C.c_int
     return lib
 
 
 _lib = _load()
-EXPORTS = ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_host", "flmisr_destroy",
-           "flmisr_last_error", "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply")
 
 
 def _check(st: int):
@@ -84,6 +91,14 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.flmisr_nccl_unique_id(C.cast(buf, C.c_void_p)))
     return buf.raw
+
+
+def _stream_handle(stream, device):
+    """cudaStream_t for the C ABI.  torch's default stream has handle 0, which the ABI reads as 'the
+    plan's own stream'; map it to cudaStreamLegacy (0x1) so the work stays ordered with torch ops."""
+    import torch
+    h = stream.cuda_stream if stream is not None else torch.cuda.current_stream(device).cuda_stream
+    return C.c_void_p(h if h else 1)
 
 
 def _ptr(t):
@@ -148,12 +163,31 @@ class Plan:
             out = torch.empty((self.H, self.W), dtype=torch.float32, device=lr_stack.device)
         trace = np.zeros((self.n_iter + 1, 6))
         rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
-        s = C.c_void_p(stream.cuda_stream) if stream is not None else C.c_void_p(
-            torch.cuda.current_stream(lr_stack.device).cuda_stream)
+        s = _stream_handle(stream, lr_stack.device)
         st = _lib.flmisr_reconstruct(self._h, _ptr(lr_stack), _ptr(x0), _ptr(out), s, C.byref(rep))
         if st != OK and (raise_numeric or st != ERR_NUMERIC):
             _check(st)
         return out, self._report(rep, trace)
+
+    def reconstruct_async(self, lr_stack, out, x0=None, stream=None):
+        """flmisr_reconstruct_async: enqueue only; pair with finish()."""
+        s = _stream_handle(stream, lr_stack.device)
+        _check(_lib.flmisr_reconstruct_async(self._h, _ptr(lr_stack), _ptr(x0), _ptr(out), s))
+
+    def finish(self, raise_numeric=True):
+        trace = np.zeros((self.n_iter + 1, 6))
+        rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
+        st = _lib.flmisr_finish(self._h, C.byref(rep))
+        if st != OK and (raise_numeric or st != ERR_NUMERIC):
+            _check(st)
+        return self._report(rep, trace)
+
+    def profile(self, enable: int = -1) -> dict:
+        """flmisr_profile: enable=1 on+reset, 0 off+reset, -1 read.  Returns the counters before the call."""
+        out = (C.c_double * 8)()
+        _check(_lib.flmisr_profile(self._h, enable, out))
+        names = ("value_grad", "update_curv", "setup_finalize", "reconstruct")
+        return {n: dict(launches=int(out[2 * i]), ms=out[2 * i + 1]) for i, n in enumerate(names)}
 
     def reconstruct_host(self, lr_stack: np.ndarray, out: np.ndarray | None = None):
         """flmisr_reconstruct_host: host fp32 in, host fp32 out (H2D/D2H inside the call)."""

@@ -31,6 +31,12 @@ CASES = {
     "p2_psf5": (40, 41, 2, synth.gaussian_psf(0.9, 5), synth.shift_pattern(2), 2, 0.3, 2),
     "frac_common": (33, 34, 2, synth.gaussian_psf(), synth.shift_pattern(2) + 0.2, 1, 0.05, 3),
     "w1_delta": (19, 21, 2, synth.delta_psf(), synth.shift_pattern(2), 1, 0.05, 1),
+    # streaming path (separable kappa, W % 4 == 0): several 124-column strips and row segments,
+    # ragged last strip / segment
+    "strips": (150, 300, 2, synth.gaussian_psf(), synth.shift_pattern(2), 1, 0.05, 3),
+    "ragged_s": (37, 50, 2, synth.gaussian_psf(), synth.shift_pattern(2), 1, 0.05, 3),
+    "strips_p2_w2": (61, 130, 2, synth.gaussian_psf(0.7), synth.shift_pattern(2), 2, 0.2, 2),
+    "delta_mag3": (20, 44, 3, synth.delta_psf(), synth.shift_pattern(3), 1, 0.05, 3),
 }
 
 
@@ -104,7 +110,7 @@ def test_initial_estimate(orc, name):
     assert rel(out.cpu().numpy(), orc.init_x0(pb, y.astype(np.float64))) <= 1e-6
 
 
-@pytest.mark.parametrize("name", ["c1", "ragged", "mag3", "p2_psf5"])
+@pytest.mark.parametrize("name", ["c1", "ragged", "mag3", "p2_psf5", "strips", "ragged_s", "strips_p2_w2"])
 def test_reconstruct_matches_oracle(orc, name):
     """Final fp32 image after 20 SCG passes vs the oracle: relative L2 <= 1e-3 (north_star)."""
     lr_h, lr_w, mag, psf, sh, pn, lam, w = CASES[name]
@@ -171,3 +177,22 @@ def test_numeric_failure_is_reported(orc):
     with pytest.raises(flmisr.FlmisrError) as ei:
         pl.reconstruct(dev(y))
     assert ei.value.status == flmisr.ERR_NUMERIC
+
+
+@pytest.mark.parametrize("name", ["c1", "strips", "ragged_s"])
+def test_tiled_and_streaming_paths_agree(orc, name, monkeypatch):
+    """The generic tiled kernels (FLMISR_FORCE_TILED) and the streaming kernels both match the oracle."""
+    lr_h, lr_w, mag, psf, sh, pn, lam, w = CASES[name]
+    y = synth.random_fields((len(sh), lr_h, lr_w), 50)
+    x = synth.random_fields((mag * lr_h, mag * lr_w), 51)
+    outs = []
+    for force in (False, True):
+        if force:
+            monkeypatch.setenv("FLMISR_FORCE_TILED", "1")
+        pl, pb = make(orc, name)
+        out = torch.zeros((pb.H, pb.W), device="cuda")
+        pl.debug(flmisr.OP_GRAD, lr=dev(y), in0=dev(x), out=out)
+        outs.append(out.cpu().numpy())
+    g = orc.grad(pb, x.astype(np.float64), y.astype(np.float64))
+    for o in outs:
+        assert rel(o, -g) <= 1e-5
