@@ -290,6 +290,7 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
             for (int dx = 0; dx < c.btv_window; ++dx)
                 if (dy || dx) sp.gam[dy * MAXBW + dx] = (float)std::pow(c.btv_alpha, dx + dy);
         for (int cl = 0; cl < 4; ++cl) sp.gcls[cl] = std::pow(c.btv_alpha, cl + 1);
+        for (int i = 0; i < MAXBW * MAXBW; ++i) sp.lgam[i] = (float)(c.lambda * (double)sp.gam[i]);
         // identity affine correction (tiled kernels compute complete values)
         for (int k = 0; k < NSLOT; ++k) {
             sp.aff_vg[k] = 1.0; sp.aff_vg[NSLOT + k] = 0.0;
@@ -352,6 +353,7 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
     for (int i = 0; i < K; ++i) { ip.sy[i] = sy[i]; ip.sx[i] = sx[i]; }
     ip.t0y = (float)(mag * c.shifts[0]);
     ip.t0x = (float)(mag * c.shifts[1]);
+    ip.perm = sp.perm = p->stream_path;
 
     // ---- device memory ----
     auto cleanup_fail = [&](flmisr_status st) { flmisr_destroy(p); return st; };
@@ -361,9 +363,12 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e)));
     p->hr_bytes = (size_t)srows * p->pitch * sizeof(float);
     const int nhr = 7;  // Y, X0, X1, P0, P1, R0, R1
-    e = cudaMalloc(&p->mem, p->hr_bytes * nhr);
+    // + 4 padding rows: interior streaming warps may prefetch one row past the band's storage
+    // (values only feed non-output rows), which must stay inside the allocation
+    const size_t pad = (size_t)8 * p->pitch * sizeof(float);   // also covers the L2 prefetch distance
+    e = cudaMalloc(&p->mem, p->hr_bytes * nhr + pad);
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc HR buffers: ") + cudaGetErrorString(e)));
-    cudaMemset(p->mem, 0, p->hr_bytes * nhr);
+    cudaMemset(p->mem, 0, p->hr_bytes * nhr + pad);
     const size_t fl = p->hr_bytes / sizeof(float);
     Buffers& b = p->b;
     b.Y = p->mem;
@@ -406,7 +411,8 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
         if (r != ncclSuccess) return cleanup_fail(fail(FLMISR_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)));
         const size_t hb = (size_t)p->eta * p->pitch * sizeof(float);
         float* hm = nullptr;
-        e = cudaMalloc(&hm, 4 * hb);
+        // + 1 row: the bulk copies of a right-border strip read up to 512 B past a row's end
+        e = cudaMalloc(&hm, 4 * hb + (size_t)p->pitch * sizeof(float));
         if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc halo buffers"));
         cudaMemset(hm, 0, 4 * hb);
         const size_t hf = hb / sizeof(float);
@@ -529,8 +535,8 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
     CUDA_TRY(mark());
     CUDA_TRY(launch_ingest(p->ip, lr_stack, const_cast<float*>(b.Y), s));
     if (x0) {
-        CUDA_TRY(cudaMemcpy2DAsync(b.X[0], p->pitch * sizeof(float), x0 + (size_t)p->store_lo * p->W,
-                                   p->W * sizeof(float), p->W * sizeof(float), srows, cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(launch_hr_copy(x0 + (size_t)p->store_lo * p->W, p->W, 0, b.X[0], p->pitch, p->sp.perm, (int)srows,
+                                p->W, s));
     } else {
         CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s));
     }
@@ -686,27 +692,32 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     cudaStream_t s = p->stream;
     Buffers& b = p->b;
-    const size_t rowb = p->W * sizeof(float), pitchb = p->pitch * sizeof(float);
-    const int H = p->H;
+    const int H = p->H, perm = p->sp.perm;
+    // HR copies between the caller's natural layout and the plan's buffer layout (perm: streaming path)
     auto put_hr = [&](float* dst, const float* src) {
-        return cudaMemcpy2DAsync(dst, pitchb, src, rowb, rowb, H, cudaMemcpyDeviceToDevice, s);
+        return launch_hr_copy(src, p->W, 0, dst, p->pitch, perm, H, p->W, s);
     };
     auto get_hr = [&](float* dst, const float* src) {
-        return cudaMemcpy2DAsync(dst, rowb, src, pitchb, rowb, H, cudaMemcpyDeviceToDevice, s);
+        return launch_hr_copy(src, p->pitch, perm, dst, p->W, 0, H, p->W, s);
     };
+    // FORWARD / ADJOINT run the tap-by-tap debug stencils on natural-layout scratch
+    IngestParams ip0 = p->ip;
+    ip0.perm = 0;
+    StencilParams sp0 = p->sp;
+    sp0.perm = 0;
     CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
     switch (op) {
         case FLMISR_OP_FORWARD:
             if (!in0 || !out) return fail(FLMISR_ERR_SHAPE, "FORWARD needs in0 and out");
-            CUDA_TRY(put_hr(b.X[0], in0));
-            CUDA_TRY(launch_forward_debug(p->kr, p->sp, b.X[0], b.R[0], s));
-            CUDA_TRY(launch_egest(p->ip, b.R[0], out, s));
+            CUDA_TRY(launch_hr_copy(in0, p->W, 0, b.X[0], p->pitch, 0, H, p->W, s));
+            CUDA_TRY(launch_forward_debug(p->kr, sp0, b.X[0], b.R[0], s));
+            CUDA_TRY(launch_egest(ip0, b.R[0], out, s));
             break;
         case FLMISR_OP_ADJOINT:
             if (!in0 || !out) return fail(FLMISR_ERR_SHAPE, "ADJOINT needs in0 and out");
-            CUDA_TRY(launch_ingest(p->ip, in0, b.R[0], s));
-            CUDA_TRY(launch_adjoint_debug(p->kr, p->sp, b.R[0], b.R[1], s));
-            CUDA_TRY(get_hr(out, b.R[1]));
+            CUDA_TRY(launch_ingest(ip0, in0, b.R[0], s));
+            CUDA_TRY(launch_adjoint_debug(p->kr, sp0, b.R[0], b.R[1], s));
+            CUDA_TRY(launch_hr_copy(b.R[1], p->pitch, 0, out, p->W, 0, H, p->W, s));
             break;
         case FLMISR_OP_GRAD:
         case FLMISR_OP_VALUE:

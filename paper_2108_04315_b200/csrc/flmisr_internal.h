@@ -40,11 +40,13 @@ struct StencilParams {
     int tile_row0;               // global row of the first tile row
     int tiles_x, tiles_y;
     int world;                   // 1: scalar logic in the last CTA; >1: rank sums for the allgather
+    int perm;                    // HR buffers use the permuted column layout (streaming path)
     float eps, eps2, lam;        // Charbonnier eps, eps^2, BTV weight lambda (fp32 copies)
     float taps[MAXTAPS];         // kappa, (2KR+1)^2 centred, row-major, correlation orientation
     float gam[MAXBW * MAXBW];    // gamma(dy,dx) = alpha^(dx+dy) at [dy*MAXBW + dx], gam[0] unused
     // streaming (separable-kappa) kernels, flmisr_stream.cu
     float ka[3], kb[3];          // kappa(P,Q) = ka[P+1] * kb[Q+1] (KR <= 1; KR = 0 zero-padded)
+    float lgam[MAXBW * MAXBW];   // lambda * gamma(dy,dx)
     int nstrips, nsegs, seg_rows, wpb;   // 128-column warp strips (step 124), row segments, warps/CTA
     double gcls[4];              // gamma of BTV class dx+dy = 1..4 (fp64, applied to the CTA sums)
     // affine correction of the raw CTA sums before the scalar logic: tot = raw * aff[k] + aff[4+k]
@@ -94,7 +96,16 @@ struct IngestParams {
     int frame_of_phase[16];      // residue (u mod mag, v mod mag) -> frame index
     int sy[16], sx[16];          // integer phase of frame i
     float t0y, t0x;              // HR shift of frame 0 (bilinear initial estimate)
+    int perm;                    // 1: HR buffers use the streaming path's permuted column layout
 };
+
+// Streaming-path column layout: each aligned group of 4 columns is stored as (c0, c2, c1, c3).
+__host__ __device__ __forceinline__ int phys_col(int c, int perm) {
+    return perm ? ((c & ~3) | ((c & 1) << 1) | ((c >> 1) & 1)) : c;
+}
+// pitched HR copy between the natural layout (dst_perm = 0) and a buffer layout (perm)
+cudaError_t launch_hr_copy(const float* src, int src_pitch, int src_perm, float* dst, int dst_pitch, int dst_perm,
+                           int rows, int W, cudaStream_t s);
 cudaError_t launch_ingest(const IngestParams& ip, const float* lr, float* Y, cudaStream_t s);
 cudaError_t launch_egest(const IngestParams& ip, const float* Yhr, float* lr, cudaStream_t s);   // debug
 cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s);

@@ -340,7 +340,8 @@ __global__ void k_ingest(IngestParams ip, const float* __restrict__ lr, float* _
     int ph = (gy % ip.mag) * ip.mag + (gx % ip.mag);
     int f = ip.frame_of_phase[ph];
     int a = (gy - ip.sy[f]) / ip.mag, c = (gx - ip.sx[f]) / ip.mag;
-    Y[(size_t)(gy - ip.store_lo) * ip.pitch + gx] = __ldg(lr + ((size_t)f * ip.lr_h + a) * ip.lr_w + c);
+    Y[(size_t)(gy - ip.store_lo) * ip.pitch + phys_col(gx, ip.perm)] =
+        __ldg(lr + ((size_t)f * ip.lr_h + a) * ip.lr_w + c);
 }
 
 __global__ void k_egest(IngestParams ip, const float* __restrict__ Yhr, float* __restrict__ lr) {
@@ -350,7 +351,15 @@ __global__ void k_egest(IngestParams ip, const float* __restrict__ Yhr, float* _
     int ph = (gy % ip.mag) * ip.mag + (gx % ip.mag);
     int f = ip.frame_of_phase[ph];
     int a = (gy - ip.sy[f]) / ip.mag, c = (gx - ip.sx[f]) / ip.mag;
-    lr[((size_t)f * ip.lr_h + a) * ip.lr_w + c] = Yhr[(size_t)(gy - ip.store_lo) * ip.pitch + gx];
+    lr[((size_t)f * ip.lr_h + a) * ip.lr_w + c] = Yhr[(size_t)(gy - ip.store_lo) * ip.pitch + phys_col(gx, ip.perm)];
+}
+
+__global__ void k_hr_copy(const float* __restrict__ src, int sp_, int sperm, float* __restrict__ dst, int dp, int dperm,
+                          int W) {
+    int gx = blockIdx.x * blockDim.x + threadIdx.x;
+    int gy = blockIdx.y;
+    if (gx >= W) return;
+    dst[(size_t)gy * dp + phys_col(gx, dperm)] = src[(size_t)gy * sp_ + phys_col(gx, sperm)];
 }
 
 // x0(u,v) = bilerp(y_0, (u - t0y)/mag, (v - t0x)/mag), LR indices clamped (reading 14).
@@ -367,7 +376,7 @@ __global__ void k_init_x0(IngestParams ip, const float* __restrict__ lr, float* 
     float v = (1.f - fa) * (1.f - fc) * __ldg(y + (size_t)ia0 * ip.lr_w + ic0) +
               (1.f - fa) * fc * __ldg(y + (size_t)ia0 * ip.lr_w + ic1) +
               fa * (1.f - fc) * __ldg(y + (size_t)ia1 * ip.lr_w + ic0) + fa * fc * __ldg(y + (size_t)ia1 * ip.lr_w + ic1);
-    X[(size_t)(gy - ip.store_lo) * ip.pitch + gx] = v;
+    X[(size_t)(gy - ip.store_lo) * ip.pitch + phys_col(gx, ip.perm)] = v;
 }
 
 // out = x + alpha_upd p when the last step was accepted and not yet applied (fused with the copy
@@ -378,7 +387,7 @@ __global__ void k_finalize(StencilParams sp, Buffers b, float* __restrict__ out,
     if (gx >= sp.W || gy >= row_hi) return;
     const ScgState* s = b.st;
     float a = s->success ? s->alpha_upd_f : 0.0f;
-    size_t off = (size_t)(gy - sp.store_lo) * sp.pitch + gx;
+    size_t off = (size_t)(gy - sp.store_lo) * sp.pitch + phys_col(gx, sp.perm);
     out[(size_t)gy * out_pitch + gx] = fmaf(a, pick(b.P, s->xcur)[off], pick(b.X, s->xcur)[off]);
 }
 
@@ -479,6 +488,12 @@ cudaError_t launch_ingest(const IngestParams& ip, const float* lr, float* Y, cud
 }
 cudaError_t launch_egest(const IngestParams& ip, const float* Yhr, float* lr, cudaStream_t s) {
     k_egest<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, Yhr, lr);
+    return cudaGetLastError();
+}
+cudaError_t launch_hr_copy(const float* src, int src_pitch, int src_perm, float* dst, int dst_pitch, int dst_perm,
+                           int rows, int W, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    k_hr_copy<<<rowgrid(W, rows), 256, 0, s>>>(src, src_pitch, src_perm, dst, dst_pitch, dst_perm, W);
     return cudaGetLastError();
 }
 cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s) {

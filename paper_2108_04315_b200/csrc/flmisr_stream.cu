@@ -2,16 +2,27 @@
 // composed kernel kappa is separable (kappa(P,Q) = a(P) b(Q): every Gaussian PSF) and KR <= 1
 // (PSF up to 3x3 with integer HR phases) -- this covers all BASELINE configs.
 //
-// Work decomposition: one warp owns a strip of 128 HR columns (4 per lane,
-// float4 I/O) and a segment of S rows, and streams down the rows with 3-row register windows
-// (x' = x + alpha p, the horizontal kappa pass of x', pending rows of -grad J).  Horizontal
-// neighbours move by warp shuffles; strips overlap by SHALO = 2 columns per side (the reach of the
-// fused operator: 2 KR for the data term's forward+adjoint chain, w-1 for BTV), so no shared
-// memory is needed.  Each BTV pair (u, u+d) is evaluated once and its psi' goes to both endpoints
-// (pending rows below, the right lane for columns to the right) -> 8 rsqrt per pixel.  The data
-// gradient is scattered the same way (adjoint = transposed correlation, P:251 A^T).
-// Image borders (clamped forward reads, folded adjoint, valid-pairs-only BTV; readings 4, 5) run in
-// a separate instantiation selected per warp (warp-uniform), so interior warps carry no masks.
+// Work decomposition: one warp owns a strip of 128 HR columns (4 per lane)
+// and a segment of S rows, and streams down the rows with 3-row register windows (x' = x + alpha p,
+// the horizontal kappa pass of x', pending rows of -grad J).  Horizontal neighbours move by warp
+// shuffles; strips overlap by SHALO = 2 columns per side (the reach of the fused operator: 2 KR for
+// the data term's forward+adjoint chain, w-1 for BTV).  Each BTV pair (u, u+d) is evaluated once and
+// its psi' goes to both endpoints (pending rows below, the right lane for columns to the right)
+// -> 8 rsqrt per pixel.  The data gradient is scattered the same way (transposed correlation).
+//
+// Memory: the input rows of a step (512 B per array) are staged by the bulk-copy engine
+// (cp.async.bulk, TMA 1D) into a per-warp NST-stage shared-memory ring completed by mbarriers, so
+// the HBM latency is hidden NST-1 steps deep without registers.
+//
+// Packed fp32x2: a lane's columns c0..c3 are processed as the pairs A = (c0, c2), B = (c1, c3)
+// with Blackwell's FFMA2 / FADD2 / FMUL2 (PTX f32x2), halving the FP32 issue slots.  To read the
+// pairs with one 16-byte access, every HR buffer of the streaming path stores each aligned group
+// of four columns as (c0, c2, c1, c3) ("permuted column layout"); ingest,
+// initial estimate, output and the debug copies convert.  Reductions accumulate both pairs into
+// one float2 whose .x holds columns c0+c1 and .y columns c2+c3, which is exactly the granularity
+// of the strip's output-column masks.
+// Image borders (clamped forward reads, folded adjoint, valid-pairs-only BTV; readings 4, 5) and
+// band edges run in a separate instantiation selected per warp (warp-uniform).
 // Constant terms (eps of every Charbonnier term, eps^2 of rho''/psi'') are hoisted into the affine
 // correction of the CTA sums (StencilParams::aff_*).
 #include <cstdint>
@@ -24,6 +35,104 @@ namespace flmisr {
 namespace {
 
 constexpr int SWPB = 8;   // warps per CTA
+
+// ---- packed fp32x2 helpers (PTX f32x2 -> SASS FFMA2 / FADD2 / FMUL2 on sm_100a) ----
+__device__ __forceinline__ float2 F2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}\n"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}\n"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}\n"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float2 fma2s(float s, float2 b, float2 c) { return fma2(F2(s, s), b, c); }
+__device__ __forceinline__ float2 mul2s(float s, float2 b) { return mul2(F2(s, s), b); }
+__device__ __forceinline__ float2 rsq2(float2 q) { return F2(rsq(q.x), rsq(q.y)); }
+__device__ __forceinline__ float2 lo2(const float4& v) { return F2(v.x, v.y); }   // (c0, c2)
+__device__ __forceinline__ float2 hi2(const float4& v) { return F2(v.z, v.w); }   // (c1, c3)
+
+// ---- per-warp TMA ring: cp.async.bulk (1D bulk copy engine) row segments -> shared memory ----
+constexpr int NST = 4;            // stages per warp
+constexpr int NARR = 4;           // rows per stage (4 arrays)
+constexpr int RING_FLOATS = NST * NARR * SCOLS;
+constexpr size_t RING_BYTES_PER_WARP = (size_t)RING_FLOATS * 4 + NST * 8;
+constexpr size_t RING_SMEM = SWPB * RING_BYTES_PER_WARP;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const float* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    return ok != 0;
+}
+
+struct Ring {
+    const float* ptr;   // this warp's ring (generic pointer into shared memory)
+    uint32_t data;      // shared address of this warp's ring
+    uint32_t bars;      // shared address of its NST mbarriers
+    __device__ __forceinline__ void init(unsigned char* smem, int warp, int lane) {
+        unsigned char* base = smem + (size_t)warp * RING_BYTES_PER_WARP;
+        ptr = reinterpret_cast<const float*>(base);
+        data = smem_u32(base);
+        bars = smem_u32(base + (size_t)RING_FLOATS * 4);
+        if (lane == 0) {
+            for (int s = 0; s < NST; ++s) mbar_init(bars + 8 * s);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    // lane 0: stage s <- four 512-byte row segments
+    __device__ __forceinline__ void issue(int s, const float* a0, const float* a1, const float* a2,
+                                          const float* a3) const {
+        const uint32_t bar = bars + 8 * s;
+        mbar_expect_tx(bar, NARR * SCOLS * 4);
+        const uint32_t d = data + (uint32_t)(s * NARR * SCOLS * 4);
+        bulk_g2s(d, a0, SCOLS * 4, bar);
+        bulk_g2s(d + SCOLS * 4, a1, SCOLS * 4, bar);
+        bulk_g2s(d + 2 * SCOLS * 4, a2, SCOLS * 4, bar);
+        bulk_g2s(d + 3 * SCOLS * 4, a3, SCOLS * 4, bar);
+    }
+    __device__ __forceinline__ void wait(int s, uint32_t parity) const {
+        while (!mbar_try(bars + 8 * s, parity)) {
+        }
+    }
+    __device__ __forceinline__ float4 get(int s, int a, int lane) const {
+        return *reinterpret_cast<const float4*>(ptr + (s * NARR + a) * SCOLS + 4 * lane);
+    }
+    // all lanes: the stage's rows are consumed; order the generic-proxy reads before the async
+    // proxy refills the stage
+    __device__ __forceinline__ void release() const {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+    }
+};
 
 __device__ __forceinline__ const float* rowp(const float* base, const StencilParams& sp, int row) {
     int r = min(max(row, sp.store_lo), sp.store_hi - 1);
@@ -47,28 +156,28 @@ __device__ __forceinline__ const float* rrowp(const Buffers& b, const float* R, 
 template <bool BORDER>
 __device__ __forceinline__ float4 ld4(const float* rp, int col, int W) {
     if (!BORDER || col + 3 < W) return __ldg(reinterpret_cast<const float4*>(rp + col));
-    // right image border (W % 4 == 0): a chunk is either inside or wholly outside -> replicate col W-1
+    // right image border (W % 4 == 0): a group is either inside or wholly outside -> replicate col W-1
+    // (column W-1 is the c3 slot of the last group, at the same physical place)
     float v = __ldg(rp + (W - 1));
     return make_float4(v, v, v, v);
 }
 
-__device__ __forceinline__ void st4(float* rp, int col, float a, float b, float c, float d, bool full,
-                                    const bool (&m)[4]) {
-    if (full) {
-        *reinterpret_cast<float4*>(rp + col) = make_float4(a, b, c, d);
+// store a lane's 4 columns given as the pairs A = (c0, c2), B = (c1, c3) in the permuted layout;
+// partial lanes (strip overlap) write only the output half (.x: c0,c1 / .y: c2,c3)
+__device__ __forceinline__ void stp(float* rp, float2 A, float2 B, bool olo, bool ohi) {
+    if (olo && ohi) {
+        *reinterpret_cast<float4*>(rp) = make_float4(A.x, A.y, B.x, B.y);
     } else {
-        if (m[0]) rp[col] = a;
-        if (m[1]) rp[col + 1] = b;
-        if (m[2]) rp[col + 2] = c;
-        if (m[3]) rp[col + 3] = d;
+        if (olo) { rp[0] = A.x; rp[2] = B.x; }
+        if (ohi) { rp[1] = A.y; rp[3] = B.y; }
     }
 }
 
 struct Geo {
-    int lane, col0, r_lo, r_hi, w_lo, w_hi;
-    bool strip0, live, full, border;
-    bool outc[4];   // this lane's column j is an output column of the strip
-    bool cv[6];     // column col0 + j (j = 0..5) lies inside the image
+    int lane, cbase, col0, r_lo, r_hi, w_lo, w_hi, llast;
+    bool strip0, live, border, rstrip;
+    bool olo, ohi;   // columns (c0, c1) / (c2, c3) of this lane are output columns of the strip
+    bool cv0, cv4;   // the lane's group / the right neighbour group lies inside the image
 };
 
 __device__ __forceinline__ Geo geometry(const StencilParams& sp) {
@@ -78,19 +187,18 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp) {
     const int gw = blockIdx.x * SWPB + warp;
     g.live = gw < sp.nstrips * sp.nsegs;
     const int strip = g.live ? gw % sp.nstrips : 0, seg = g.live ? gw / sp.nstrips : 0;
-    const int cbase = strip * SSTEP;
-    g.col0 = cbase + 4 * g.lane;
+    g.cbase = strip * SSTEP;
+    g.col0 = g.cbase + 4 * g.lane;
     g.strip0 = strip == 0;
-    const int oc_lo = g.strip0 ? 0 : cbase + SHALO;
-    const int oc_hi = (strip == sp.nstrips - 1) ? sp.W : min(cbase + SCOLS - SHALO, sp.W);
-    g.full = true;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        g.outc[j] = g.live && g.col0 + j >= oc_lo && g.col0 + j < oc_hi;
-        g.full = g.full && g.outc[j];
-    }
-#pragma unroll
-    for (int j = 0; j < 6; ++j) g.cv[j] = g.col0 + j < sp.W;
+    const int oc_lo = g.strip0 ? 0 : g.cbase + SHALO;
+    const int oc_hi = (strip == sp.nstrips - 1) ? sp.W : min(g.cbase + SCOLS - SHALO, sp.W);
+    // strip bounds are at even offsets and W % 4 == 0, so (c0, c1) and (c2, c3) share their masks
+    g.olo = g.live && g.col0 >= oc_lo && g.col0 + 1 < oc_hi;
+    g.ohi = g.live && g.col0 + 2 >= oc_lo && g.col0 + 3 < oc_hi;
+    g.cv0 = g.col0 < sp.W;
+    g.cv4 = g.col0 + 4 < sp.W;
+    g.rstrip = g.cbase + SCOLS > sp.W;
+    g.llast = min(max((sp.W - 1 - g.cbase) >> 2, 0), 31);
     g.r_lo = sp.row_lo + seg * sp.seg_rows;
     g.r_hi = min(g.r_lo + sp.seg_rows, sp.row_hi);
     if (!g.live) g.r_hi = g.r_lo;
@@ -101,126 +209,153 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp) {
     g.w_hi = g.r_hi;
     if (g.live && seg == 0 && sp.row_lo > 0) g.w_lo = sp.store_lo;
     if (g.live && seg == sp.nsegs - 1 && sp.row_hi < sp.H) g.w_hi = sp.store_hi;
-    g.border = g.strip0 || cbase + SCOLS > sp.W || g.r_lo < 3 || g.r_hi > sp.H - 3;
+    // interior warps: no image border, every row they touch (r_lo - 2 .. r_hi + 2) is an owned row of
+    // the band, so they need no clamps, no halo buffers and no masks beyond the strip's output columns
+    g.border = g.strip0 || g.rstrip || g.r_lo < sp.row_lo + 3 || g.r_hi > sp.row_hi - 3;
     return g;
 }
 
 __device__ __forceinline__ float shup(float v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ float shdn(float v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ float msum(float2 a, const Geo& g) { return (g.olo ? a.x : 0.f) + (g.ohi ? a.y : 0.f); }
+
+// right-border strip: lanes past the image take the replicated column W-1 (clamp, reading 4)
+template <bool BORDER>
+__device__ __forceinline__ float4 fixr(float4 v, const Geo& g) {
+    if (BORDER && g.rstrip) {
+        const float r = __shfl_sync(0xffffffffu, v.w, g.llast);
+        if (!g.cv0) v = make_float4(r, r, r, r);
+    }
+    return v;
+}
 
 // ------------------------------------------------------------------------------------------------
 // value + gradient at x' = x + alpha p (Alg. 1 lines 14-19), streaming.
-//   step t: x'(t+2) -> HZ(t+2); w(t+1) = rho'(kappa x' - Y) -> horizontal adjoint pass hw(t+1),
-//   scattered into the pending rows t, t+1, t+2 of r = -grad J; BTV pairs of row t scattered into
-//   rows t..t+2; row t is then complete and stored.
+//   step t (ring stage = x,p(t+2), Y(t+1), r_old(t)): x'(t+2) -> horizontal kappa pass;
+//   w(t+1) = rho'(kappa x' - Y) -> horizontal adjoint pass hw(t+1), scattered into the pending rows
+//   t, t+1, t+2 of r = -grad J; BTV pairs of row t scattered into rows t..t+2; row t is complete.
 // ------------------------------------------------------------------------------------------------
 template <int BW, int PN, bool BORDER>
 struct VG {
-    float X[3][6];    // x' at columns 0 .. 5 relative to col0 (rows t, t+1, t+2 in slots (t+k)%3)
-    float HZ[3][4];   // horizontal kappa pass of x'
-    float G[3][6];    // pending r = -grad J of rows t, t+1, t+2 at columns 0 .. 5
-    float4 fx, fp, fy, fr;   // prefetched rows: x/p (t+2), Y (t+1), r_old (t)
-    float acc_d, vb[4], rr, rro;
+    float2 XA[3], XB[3];            // x' pairs (c0,c2), (c1,c3) of rows t, t+1, t+2 (slot (t+k)%3)
+    float X4[3], X5[3];             // x' at c4, c5 (the right lane's c0, c1)
+    float2 HA[3], HB[3];            // horizontal kappa pass of x'
+    float2 GA[3], GB[3], GD[3], GE[3];   // pending r at (c0,c2), (c1,c3), (c2,c4), (c3,c5)
+    float2 accd, vb[4], rr, rro;    // .x: columns c0+c1, .y: columns c2+c3
+    const float *ix, *ip, *iy, *ir; // interior warps: next rows to stage (strip start column)
+    int t0, nstep;
 
     const StencilParams& sp;
     const Buffers& b;
     const Geo& g;
+    const Ring& ring;
     const float* X0;
     const float* P0;
     const float* Rold;
     float* Rnew;
     float alpha;
 
-    __device__ __forceinline__ VG(const StencilParams& sp_, const Buffers& b_, const Geo& g_, const float* x,
-                                  const float* p, const float* ro, float* rn, float al)
-        : sp(sp_), b(b_), g(g_), X0(x), P0(p), Rold(ro), Rnew(rn), alpha(al) {}
+    __device__ __forceinline__ VG(const StencilParams& sp_, const Buffers& b_, const Geo& g_, const Ring& ring_,
+                                  const float* x, const float* p, const float* ro, float* rn, float al)
+        : sp(sp_), b(b_), g(g_), ring(ring_), X0(x), P0(p), Rold(ro), Rnew(rn), alpha(al) {}
 
-    __device__ __forceinline__ void load_xp(int row, float4& xv, float4& pv) {
-        xv = ld4<BORDER>(rowp(X0, sp, row), g.col0, sp.W);
-        pv = ld4<BORDER>(rowp(P0, sp, row), g.col0, sp.W);
+    // lane 0: stage the rows of step tt (x, p at tt+2; Y at tt+1; r_old at tt)
+    __device__ __forceinline__ void issue(int tt) {
+        const int s = (tt - t0) % NST;
+        if (BORDER) {
+            ring.issue(s, rowp(X0, sp, tt + 2) + g.cbase, rowp(P0, sp, tt + 2) + g.cbase,
+                       rowp(b.Y, sp, tt + 1) + g.cbase, rowp(Rold, sp, tt) + g.cbase);
+        } else {
+            ring.issue(s, ix, ip, iy, ir);
+            ix += sp.pitch; ip += sp.pitch; iy += sp.pitch; ir += sp.pitch;
+        }
     }
 
     // x'(row) into slot s, right neighbours, and the horizontal kappa pass
     __device__ __forceinline__ void set_x(int s, const float4& xv, const float4& pv) {
-        X[s][0] = fmaf(alpha, pv.x, xv.x);
-        X[s][1] = fmaf(alpha, pv.y, xv.y);
-        X[s][2] = fmaf(alpha, pv.z, xv.z);
-        X[s][3] = fmaf(alpha, pv.w, xv.w);
-        float xm1 = shup(X[s][3]);
-        X[s][4] = shdn(X[s][0]);
-        X[s][5] = shdn(X[s][1]);
+        XA[s] = fma2s(alpha, lo2(pv), lo2(xv));
+        XB[s] = fma2s(alpha, hi2(pv), hi2(xv));
+        float xm1 = shup(XB[s].y);
+        X4[s] = shdn(XA[s].x);
+        X5[s] = shdn(XB[s].x);
         if (BORDER) {
-            if (g.strip0 && g.lane == 0) xm1 = X[s][0];                  // clamp at column 0
-            if (!g.cv[4]) { X[s][4] = X[s][3]; X[s][5] = X[s][3]; }      // clamp at column W-1
+            if (g.strip0 && g.lane == 0) xm1 = XA[s].x;                  // clamp at column 0
+            if (!g.cv4) { X4[s] = XB[s].y; X5[s] = XB[s].y; }            // clamp at column W-1
         }
-        HZ[s][0] = fmaf(sp.kb[0], xm1, fmaf(sp.kb[1], X[s][0], sp.kb[2] * X[s][1]));
-#pragma unroll
-        for (int j = 1; j < 4; ++j)
-            HZ[s][j] = fmaf(sp.kb[0], X[s][j - 1], fmaf(sp.kb[1], X[s][j], sp.kb[2] * X[s][j + 1]));
+        // hz(j) = b(-1) x(j-1) + b(0) x(j) + b(1) x(j+1)
+        HA[s] = fma2s(sp.kb[0], F2(xm1, XB[s].x), fma2s(sp.kb[1], XA[s], mul2s(sp.kb[2], XB[s])));
+        HB[s] = fma2s(sp.kb[0], XA[s], fma2s(sp.kb[1], XB[s], mul2s(sp.kb[2], F2(XA[s].y, X4[s]))));
     }
 
     template <int PH>
     __device__ __forceinline__ void step(int t) {
         constexpr int s0 = PH % 3, s1 = (PH + 1) % 3, sa = (PH + 2) % 3;
-        const float eps2 = sp.eps2;
-        // A: x'(t+2) from the prefetch, then prefetch x/p(t+3)
+        const float2 e2 = F2(sp.eps2, sp.eps2);
+        const int rs_ = (t - t0) % NST;
+        ring.wait(rs_, ((t - t0) / NST) & 1);
+        const float4 fx = fixr<BORDER>(ring.get(rs_, 0, g.lane), g);
+        const float4 fp = fixr<BORDER>(ring.get(rs_, 1, g.lane), g);
+        const float4 fy = fixr<BORDER>(ring.get(rs_, 2, g.lane), g);
+        const float4 fr = fixr<BORDER>(ring.get(rs_, 3, g.lane), g);
+
+        // A: x'(t+2)
         set_x(sa, fx, fp);
-        load_xp(t + 3, fx, fp);
 
         // B: w(t+1) = rho'(z - Y), data value, adjoint (transposed kappa) scattered into rows t..t+2
         {
             const int tw = t + 1;
-            float w[4];
-            const float yv[4] = {fy.x, fy.y, fy.z, fy.w};
-            fy = ld4<BORDER>(rowp(b.Y, sp, t + 2), g.col0, sp.W);
+            const float2 yA = lo2(fy), yB = hi2(fy);
             const bool orow = tw >= g.r_lo && tw < g.r_hi;
-            const bool vrow = !BORDER || (tw >= 0 && tw < sp.H);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float z = fmaf(sp.ka[0], HZ[s0][j], fmaf(sp.ka[1], HZ[s1][j], sp.ka[2] * HZ[sa][j]));
-                float e = z - yv[j];
-                float vr, wj;
-                if (PN == 2) {
-                    vr = e * e;
-                    wj = 2.0f * e;
-                } else {
-                    float q = fmaf(e, e, eps2);
-                    float rs = rsqrtf(q);
-                    vr = q * rs;          // rho + eps (eps * N is subtracted by the affine correction)
-                    wj = e * rs;
+            const float2 zA = fma2s(sp.ka[0], HA[s0], fma2s(sp.ka[1], HA[s1], mul2s(sp.ka[2], HA[sa])));
+            const float2 zB = fma2s(sp.ka[0], HB[s0], fma2s(sp.ka[1], HB[s1], mul2s(sp.ka[2], HB[sa])));
+            const float2 eA = sub2(zA, yA), eB = sub2(zB, yB);
+            float2 wA, wB;
+            if (PN == 2) {
+                if (orow) {
+                    accd = fma2(eA, eA, accd);
+                    accd = fma2(eB, eB, accd);
                 }
-                if (orow && g.outc[j]) acc_d += vr;
-                if (BORDER && !(vrow && g.cv[j])) wj = 0.0f;   // zero-padded adjoint outside the image
-                w[j] = wj;
+                wA = fma2s(1.0f, eA, eA);
+                wB = fma2s(1.0f, eB, eB);
+            } else {
+                const float2 qA = fma2(eA, eA, e2), qB = fma2(eB, eB, e2);
+                const float2 rA = rsq2(qA), rB = rsq2(qB);
+                if (orow) {   // rho + eps = q rs (eps * N is subtracted by the affine correction)
+                    accd = fma2(qA, rA, accd);
+                    accd = fma2(qB, rB, accd);
+                }
+                wA = mul2(eA, rA);
+                wB = mul2(eB, rB);
             }
-            float wm1 = shup(w[3]), w4 = shdn(w[0]);
+            if (BORDER && !(tw >= 0 && tw < sp.H && g.cv0)) { wA = F2(0.f, 0.f); wB = wA; }   // zero-padded
+            float wm1 = shup(wB.y), w4 = shdn(wA.x);
             if (BORDER) {
                 if (g.strip0 && g.lane == 0) wm1 = 0.0f;
-                if (!g.cv[4]) w4 = 0.0f;
+                if (!g.cv4) w4 = 0.0f;
             }
-            float hw[4];
-            hw[0] = fmaf(sp.kb[0], w[1], fmaf(sp.kb[1], w[0], sp.kb[2] * wm1));
-            hw[1] = fmaf(sp.kb[0], w[2], fmaf(sp.kb[1], w[1], sp.kb[2] * w[0]));
-            hw[2] = fmaf(sp.kb[0], w[3], fmaf(sp.kb[1], w[2], sp.kb[2] * w[1]));
-            hw[3] = fmaf(sp.kb[0], w4, fmaf(sp.kb[1], w[3], sp.kb[2] * w[2]));
+            // hw(j) = b(-1) w(j+1) + b(0) w(j) + b(1) w(j-1)
+            float2 hA = fma2s(sp.kb[0], wB, fma2s(sp.kb[1], wA, mul2s(sp.kb[2], F2(wm1, wB.x))));
+            float2 hB = fma2s(sp.kb[0], F2(wA.y, w4), fma2s(sp.kb[1], wB, mul2s(sp.kb[2], wA)));
             if (BORDER) {   // fold the clamped columns back onto the edge pixels (adjoint of clamp)
-                if (g.strip0 && g.lane == 0) hw[0] = fmaf(sp.kb[0], w[0], hw[0]);
-                if (g.cv[3] && !g.cv[4]) hw[3] = fmaf(sp.kb[2], w[3], hw[3]);
+                if (g.strip0 && g.lane == 0) hA.x = fmaf(sp.kb[0], wA.x, hA.x);
+                if (g.cv0 && !g.cv4) hB.y = fmaf(sp.kb[2], wB.y, hB.y);
             }
             // g(v) = sum_P a(P) hw(v - P): hw(t+1) feeds rows t (P=-1), t+1 (P=0), t+2 (P=+1)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                G[s0][j] = fmaf(-sp.ka[0], hw[j], G[s0][j]);
-                G[s1][j] = fmaf(-sp.ka[1], hw[j], G[s1][j]);
-                G[sa][j] = fmaf(-sp.ka[2], hw[j], G[sa][j]);
-            }
+            GA[s0] = fma2s(-sp.ka[0], hA, GA[s0]);
+            GB[s0] = fma2s(-sp.ka[0], hB, GB[s0]);
+            GA[s1] = fma2s(-sp.ka[1], hA, GA[s1]);
+            GB[s1] = fma2s(-sp.ka[1], hB, GB[s1]);
+            GA[sa] = fma2s(-sp.ka[2], hA, GA[sa]);
+            GB[sa] = fma2s(-sp.ka[2], hB, GB[sa]);
             if (BORDER) {   // fold the clamped rows: row -1 onto row 0, row H onto row H-1
-                if (tw == 0)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) G[s1][j] = fmaf(-sp.ka[0], hw[j], G[s1][j]);
-                if (tw == sp.H - 1)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) G[s1][j] = fmaf(-sp.ka[2], hw[j], G[s1][j]);
+                if (tw == 0) {
+                    GA[s1] = fma2s(-sp.ka[0], hA, GA[s1]);
+                    GB[s1] = fma2s(-sp.ka[0], hB, GB[s1]);
+                }
+                if (tw == sp.H - 1) {
+                    GA[s1] = fma2s(-sp.ka[2], hA, GA[s1]);
+                    GB[s1] = fma2s(-sp.ka[2], hB, GB[s1]);
+                }
             }
         }
 
@@ -235,73 +370,105 @@ struct VG {
 #pragma unroll
                 for (int dx = 0; dx < BW; ++dx) {
                     if (dy == 0 && dx == 0) continue;
-                    const float lg = sp.lam * sp.gam[dy * MAXBW + dx];
+                    const float lg = sp.lgam[dy * MAXBW + dx];
                     const int cls = dx + dy - 1;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        float d = X[s0][j] - X[sq][j + dx];
-                        float q = fmaf(d, d, eps2);
-                        float rs = rsqrtf(q);
-                        float u = d * rs;
-                        if (BORDER && !g.cv[j + dx]) u = 0.0f;
-                        if (orow && g.outc[j] && (!BORDER || g.cv[j + dx])) vb[cls] = fmaf(q, rs, vb[cls]);
-                        G[s0][j] = fmaf(-lg, u, G[s0][j]);
-                        G[sq][j + dx] = fmaf(lg, u, G[sq][j + dx]);
+                    const float2 D = F2(XA[sq].y, X4[sq]), E = F2(XB[sq].y, X5[sq]);
+                    const float2 pA = dx == 0 ? XA[sq] : (dx == 1 ? XB[sq] : D);
+                    const float2 pB = dx == 0 ? XB[sq] : (dx == 1 ? D : E);
+                    const float2 dA = sub2(XA[s0], pA), dB = sub2(XB[s0], pB);
+                    const float2 qA = fma2(dA, dA, e2), qB = fma2(dB, dB, e2);
+                    const float2 rA = rsq2(qA), rB = rsq2(qB);
+                    float2 uA = mul2(dA, rA), uB = mul2(dB, rB);
+                    if (BORDER) {
+                        // in the last in-image group (cv0 && !cv4) the partners c2+dx (dx = 2) and
+                        // c3+dx (dx >= 1) fall outside the image; c0+dx, c1+dx never do
+                        if (!g.cv0) { uA = F2(0.f, 0.f); uB = uA; }
+                        if (!g.cv4) {
+                            if (dx >= 2) uA.y = 0.f;
+                            if (dx >= 1) uB.y = 0.f;
+                        }
+                        if (orow) {
+                            float2 vA = mul2(qA, rA), vB = mul2(qB, rB);
+                            if (!g.cv0) { vA = F2(0.f, 0.f); vB = vA; }
+                            if (!g.cv4) {
+                                if (dx >= 2) vA.y = 0.f;
+                                if (dx >= 1) vB.y = 0.f;
+                            }
+                            vb[cls] = fma2s(1.0f, vA, vb[cls]);
+                            vb[cls] = fma2s(1.0f, vB, vb[cls]);
+                        }
+                    } else if (orow) {
+                        vb[cls] = fma2(qA, rA, vb[cls]);
+                        vb[cls] = fma2(qB, rB, vb[cls]);
+                    }
+                    GA[s0] = fma2s(-lg, uA, GA[s0]);
+                    GB[s0] = fma2s(-lg, uB, GB[s0]);
+                    if (dx == 0) {
+                        GA[sq] = fma2s(lg, uA, GA[sq]);
+                        GB[sq] = fma2s(lg, uB, GB[sq]);
+                    } else if (dx == 1) {
+                        GB[sq] = fma2s(lg, uA, GB[sq]);
+                        GD[sq] = fma2s(lg, uB, GD[sq]);
+                    } else {
+                        GD[sq] = fma2s(lg, uA, GD[sq]);
+                        GE[sq] = fma2s(lg, uB, GE[sq]);
                     }
                 }
             }
         }
 
-        // E: row t is complete once the right-spilled columns of the left lane arrive
+        // E: row t is complete once the (c2,c4)/(c3,c5) pairs are folded and the right-spilled
+        // columns of the left lane arrive
         {
-            float c4 = shup(G[s0][4]), c5 = shup(G[s0][5]);
+            GA[s0].y += GD[s0].x;
+            GB[s0].y += GE[s0].x;
+            const float c4 = shup(GD[s0].y), c5 = shup(GE[s0].y);
             if (g.lane > 0) {
-                G[s0][0] += c4;
-                G[s0][1] += c5;
+                GA[s0].x += c4;
+                GB[s0].x += c5;
             }
-            const float ro[4] = {fr.x, fr.y, fr.z, fr.w};
-            fr = ld4<BORDER>(rowp(Rold, sp, t + 1), g.col0, sp.W);
             if (orow) {
-                float* rp = Rnew + (size_t)(t - sp.store_lo) * sp.pitch;
-                st4(rp, g.col0, G[s0][0], G[s0][1], G[s0][2], G[s0][3], g.full, g.outc);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (g.outc[j]) {
-                        rr = fmaf(G[s0][j], G[s0][j], rr);
-                        rro = fmaf(G[s0][j], ro[j], rro);
-                    }
-                }
+                stp(Rnew + (size_t)(t - sp.store_lo) * sp.pitch + g.col0, GA[s0], GB[s0], g.olo, g.ohi);
+                rr = fma2(GA[s0], GA[s0], rr);
+                rr = fma2(GB[s0], GB[s0], rr);
+                rro = fma2(GA[s0], lo2(fr), rro);
+                rro = fma2(GB[s0], hi2(fr), rro);
                 // band mode: owned boundary rows of the candidate go to the neighbours
                 if (b.send_top && t - sp.row_lo < b.eta)
-                    st4(b.send_top + (size_t)(t - sp.row_lo) * sp.pitch, g.col0, G[s0][0], G[s0][1], G[s0][2],
-                        G[s0][3], g.full, g.outc);
+                    stp(b.send_top + (size_t)(t - sp.row_lo) * sp.pitch + g.col0, GA[s0], GB[s0], g.olo, g.ohi);
                 if (b.send_bot && sp.row_hi - 1 - t < b.eta)
-                    st4(b.send_bot + (size_t)(t - (sp.row_hi - b.eta)) * sp.pitch, g.col0, G[s0][0], G[s0][1],
-                        G[s0][2], G[s0][3], g.full, g.outc);
+                    stp(b.send_bot + (size_t)(t - (sp.row_hi - b.eta)) * sp.pitch + g.col0, GA[s0], GB[s0], g.olo,
+                        g.ohi);
             }
-#pragma unroll
-            for (int j = 0; j < 6; ++j) G[s0][j] = 0.0f;
+            GA[s0] = GB[s0] = GD[s0] = GE[s0] = F2(0.f, 0.f);
         }
+
+        // the stage is consumed: refill it with the rows of step t + NST
+        ring.release();
+        if (g.lane == 0 && t + NST < t0 + nstep) issue(t + NST);
     }
 
     __device__ __forceinline__ void run() {
-        acc_d = 0.f; rr = 0.f; rro = 0.f;
+        const float2 z = F2(0.f, 0.f);
+        accd = rr = rro = z;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) vb[c] = 0.f;
+        for (int c = 0; c < 4; ++c) vb[c] = z;
 #pragma unroll
-        for (int s = 0; s < 3; ++s)
-#pragma unroll
-            for (int j = 0; j < 6; ++j) G[s][j] = 0.f;
-        const int t0 = g.r_lo - 2;
-        float4 xv, pv;
-        load_xp(t0, xv, pv);
-        set_x(0, xv, pv);
-        load_xp(t0 + 1, xv, pv);
-        set_x(1, xv, pv);
-        load_xp(t0 + 2, fx, fp);
-        fy = ld4<BORDER>(rowp(b.Y, sp, t0 + 1), g.col0, sp.W);
-        fr = ld4<BORDER>(rowp(Rold, sp, t0), g.col0, sp.W);
-        const int nstep = sp.seg_rows + 2;   // multiple of 3 (seg_rows = 1 mod 3)
+        for (int s = 0; s < 3; ++s) GA[s] = GB[s] = GD[s] = GE[s] = z;
+        t0 = g.r_lo - 2;
+        nstep = sp.seg_rows + 2;   // multiple of 3 (seg_rows = 1 mod 3)
+        if (!BORDER) {
+            const size_t o = (size_t)(t0 - sp.store_lo) * sp.pitch + g.cbase;
+            ix = X0 + o + 2 * (size_t)sp.pitch;
+            ip = P0 + o + 2 * (size_t)sp.pitch;
+            iy = b.Y + o + (size_t)sp.pitch;
+            ir = Rold + o;
+        }
+        if (g.lane == 0)
+            for (int k = 0; k < NST && k < nstep; ++k) issue(t0 + k);
+        // rows t0, t0+1 of x' (the window before the first step) by direct loads
+        set_x(0, ld4<BORDER>(rowp(X0, sp, t0), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0), g.col0, sp.W));
+        set_x(1, ld4<BORDER>(rowp(X0, sp, t0 + 1), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0 + 1), g.col0, sp.W));
         for (int t = t0; t < t0 + nstep; t += 3) {
             step<0>(t);
             step<1>(t + 1);
@@ -312,11 +479,14 @@ struct VG {
 
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, 2) k_vg_stream(StencilParams sp, Buffers b, int phase) {
+    extern __shared__ __align__(128) unsigned char smem[];
     ScgState* st = b.st;
     if (phase != PH_DEBUG && st->done) return;
     const int xcur = st->xcur, rcur = st->rcur;
     const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
     const Geo g = geometry(sp);
+    Ring ring;
+    ring.init(smem, threadIdx.x >> 5, g.lane);
     double acc[NSLOT];
     {
         const float* X = pick(b.X, xcur);
@@ -326,13 +496,15 @@ __global__ void __launch_bounds__(SWPB * 32, 2) k_vg_stream(StencilParams sp, Bu
         float ad = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, a_rr = 0.f, a_rro = 0.f;
         if (!g.live) {
         } else if (g.border) {
-            VG<BW, PN, true> v(sp, b, g, X, P, Ro, Rn, alpha);
+            VG<BW, PN, true> v(sp, b, g, ring, X, P, Ro, Rn, alpha);
             v.run();
-            ad = v.acc_d; v0 = v.vb[0]; v1 = v.vb[1]; v2 = v.vb[2]; v3 = v.vb[3]; a_rr = v.rr; a_rro = v.rro;
+            ad = msum(v.accd, g); v0 = msum(v.vb[0], g); v1 = msum(v.vb[1], g); v2 = msum(v.vb[2], g);
+            v3 = msum(v.vb[3], g); a_rr = msum(v.rr, g); a_rro = msum(v.rro, g);
         } else {
-            VG<BW, PN, false> v(sp, b, g, X, P, Ro, Rn, alpha);
+            VG<BW, PN, false> v(sp, b, g, ring, X, P, Ro, Rn, alpha);
             v.run();
-            ad = v.acc_d; v0 = v.vb[0]; v1 = v.vb[1]; v2 = v.vb[2]; v3 = v.vb[3]; a_rr = v.rr; a_rro = v.rro;
+            ad = msum(v.accd, g); v0 = msum(v.vb[0], g); v1 = msum(v.vb[1], g); v2 = msum(v.vb[2], g);
+            v3 = msum(v.vb[3], g); a_rr = msum(v.rr, g); a_rro = msum(v.rro, g);
         }
         acc[0] = ad;
         acc[1] = sp.gcls[0] * v0 + sp.gcls[1] * v1 + sp.gcls[2] * v2 + sp.gcls[3] * v3;
@@ -346,97 +518,102 @@ __global__ void __launch_bounds__(SWPB * 32, 2) k_vg_stream(StencilParams sp, Bu
 // ------------------------------------------------------------------------------------------------
 // update x <- x + alpha_upd p, p <- r + beta p (Alg. 1 lines 14, 20), then the exact curvature
 // p^T Hess J p, <p,p>, <p,r> at the new (x, p) (lines 6-12; reading 16), streaming.
+//   ring stage of step t: x, p, r at row t+2, Y at row t+1.
 // ------------------------------------------------------------------------------------------------
 template <int BW, int PN, bool BORDER>
 struct UC {
-    float XN[3][6], PN_[3][6];
-    float HX[3][4], HP[3][4];
-    float4 fx, fp, fr, fy;   // prefetched: x/p/r rows (t+2), Y (t+1)
-    float cd, cb[4], pp, mu;
+    float2 XA[3], XB[3], PA[3], PB[3];   // new x / p pairs (c0,c2), (c1,c3)
+    float X4[3], X5[3], P4[3], P5[3];    // new x / p at c4, c5
+    float2 HXA[3], HXB[3], HPA[3], HPB[3];
+    float2 cd, cb[4], pp, mu;            // .x: columns c0+c1, .y: columns c2+c3
+    const float *ix, *ip, *ir, *iy;      // interior warps: next rows to stage (strip start column)
+    int t0, nstep;
     const StencilParams& sp;
     const Buffers& b;
     const Geo& g;
+    const Ring& ring;
     const float *X0, *P0, *R0;
     float *Xn, *Pn;
     float au, be;
 
-    __device__ __forceinline__ UC(const StencilParams& sp_, const Buffers& b_, const Geo& g_, const float* x,
-                                  const float* p, const float* r, float* xn, float* pn, float a, float bb)
-        : sp(sp_), b(b_), g(g_), X0(x), P0(p), R0(r), Xn(xn), Pn(pn), au(a), be(bb) {}
+    __device__ __forceinline__ UC(const StencilParams& sp_, const Buffers& b_, const Geo& g_, const Ring& ring_,
+                                  const float* x, const float* p, const float* r, float* xn, float* pn, float a,
+                                  float bb)
+        : sp(sp_), b(b_), g(g_), ring(ring_), X0(x), P0(p), R0(r), Xn(xn), Pn(pn), au(a), be(bb) {}
 
-    __device__ __forceinline__ void load(int row, float4& xv, float4& pv, float4& rv) {
-        xv = ld4<BORDER>(rowp(X0, sp, row), g.col0, sp.W);
-        pv = ld4<BORDER>(rowp(P0, sp, row), g.col0, sp.W);
-        rv = ld4<BORDER>(rrowp(b, R0, sp, row), g.col0, sp.W);
+    __device__ __forceinline__ void issue(int tt) {
+        const int s = (tt - t0) % NST;
+        if (BORDER) {
+            ring.issue(s, rowp(X0, sp, tt + 2) + g.cbase, rowp(P0, sp, tt + 2) + g.cbase,
+                       rrowp(b, R0, sp, tt + 2) + g.cbase, rowp(b.Y, sp, tt + 1) + g.cbase);
+        } else {
+            ring.issue(s, ix, ip, ir, iy);
+            ix += sp.pitch; ip += sp.pitch; ir += sp.pitch; iy += sp.pitch;
+        }
     }
 
     __device__ __forceinline__ void set_row(int s, int row, const float4& xv, const float4& pv, const float4& rv) {
-        const float xo[4] = {xv.x, xv.y, xv.z, xv.w}, po[4] = {pv.x, pv.y, pv.z, pv.w};
-        const float ro[4] = {rv.x, rv.y, rv.z, rv.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            XN[s][j] = fmaf(au, po[j], xo[j]);
-            PN_[s][j] = fmaf(be, po[j], ro[j]);
-        }
+        XA[s] = fma2s(au, lo2(pv), lo2(xv));
+        XB[s] = fma2s(au, hi2(pv), hi2(xv));
+        PA[s] = fma2s(be, lo2(pv), lo2(rv));
+        PB[s] = fma2s(be, hi2(pv), hi2(rv));
         if (row >= g.w_lo && row < g.w_hi) {
-            const size_t off = (size_t)(row - sp.store_lo) * sp.pitch;
-            st4(Xn + off, g.col0, XN[s][0], XN[s][1], XN[s][2], XN[s][3], g.full, g.outc);
-            st4(Pn + off, g.col0, PN_[s][0], PN_[s][1], PN_[s][2], PN_[s][3], g.full, g.outc);
+            const size_t off = (size_t)(row - sp.store_lo) * sp.pitch + g.col0;
+            stp(Xn + off, XA[s], XB[s], g.olo, g.ohi);
+            stp(Pn + off, PA[s], PB[s], g.olo, g.ohi);
             if (row >= g.r_lo && row < g.r_hi) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (g.outc[j]) {
-                        pp = fmaf(PN_[s][j], PN_[s][j], pp);
-                        mu = fmaf(PN_[s][j], ro[j], mu);
-                    }
-                }
+                pp = fma2(PA[s], PA[s], pp);
+                pp = fma2(PB[s], PB[s], pp);
+                mu = fma2(PA[s], lo2(rv), mu);
+                mu = fma2(PB[s], hi2(rv), mu);
             }
         }
-        float xm1 = shup(XN[s][3]), pm1 = shup(PN_[s][3]);
-        XN[s][4] = shdn(XN[s][0]);
-        XN[s][5] = shdn(XN[s][1]);
-        PN_[s][4] = shdn(PN_[s][0]);
-        PN_[s][5] = shdn(PN_[s][1]);
+        float xm1 = shup(XB[s].y), pm1 = shup(PB[s].y);
+        X4[s] = shdn(XA[s].x);
+        X5[s] = shdn(XB[s].x);
+        P4[s] = shdn(PA[s].x);
+        P5[s] = shdn(PB[s].x);
         if (BORDER) {
-            if (g.strip0 && g.lane == 0) { xm1 = XN[s][0]; pm1 = PN_[s][0]; }
-            if (!g.cv[4]) { XN[s][4] = XN[s][5] = XN[s][3]; PN_[s][4] = PN_[s][5] = PN_[s][3]; }
+            if (g.strip0 && g.lane == 0) { xm1 = XA[s].x; pm1 = PA[s].x; }
+            if (!g.cv4) { X4[s] = X5[s] = XB[s].y; P4[s] = P5[s] = PB[s].y; }
         }
-        HX[s][0] = fmaf(sp.kb[0], xm1, fmaf(sp.kb[1], XN[s][0], sp.kb[2] * XN[s][1]));
-        HP[s][0] = fmaf(sp.kb[0], pm1, fmaf(sp.kb[1], PN_[s][0], sp.kb[2] * PN_[s][1]));
-#pragma unroll
-        for (int j = 1; j < 4; ++j) {
-            HX[s][j] = fmaf(sp.kb[0], XN[s][j - 1], fmaf(sp.kb[1], XN[s][j], sp.kb[2] * XN[s][j + 1]));
-            HP[s][j] = fmaf(sp.kb[0], PN_[s][j - 1], fmaf(sp.kb[1], PN_[s][j], sp.kb[2] * PN_[s][j + 1]));
-        }
+        HXA[s] = fma2s(sp.kb[0], F2(xm1, XB[s].x), fma2s(sp.kb[1], XA[s], mul2s(sp.kb[2], XB[s])));
+        HXB[s] = fma2s(sp.kb[0], XA[s], fma2s(sp.kb[1], XB[s], mul2s(sp.kb[2], F2(XA[s].y, X4[s]))));
+        HPA[s] = fma2s(sp.kb[0], F2(pm1, PB[s].x), fma2s(sp.kb[1], PA[s], mul2s(sp.kb[2], PB[s])));
+        HPB[s] = fma2s(sp.kb[0], PA[s], fma2s(sp.kb[1], PB[s], mul2s(sp.kb[2], F2(PA[s].y, P4[s]))));
     }
 
     template <int PH>
     __device__ __forceinline__ void step(int t) {
         constexpr int s0 = PH % 3, s1 = (PH + 1) % 3, sa = (PH + 2) % 3;
-        const float eps2 = sp.eps2;
-        set_row(sa, t + 2, fx, fp, fr);
-        load(t + 3, fx, fp, fr);
+        const float2 e2 = F2(sp.eps2, sp.eps2);
+        const int rs_ = (t - t0) % NST;
+        ring.wait(rs_, ((t - t0) / NST) & 1);
+        set_row(sa, t + 2, fixr<BORDER>(ring.get(rs_, 0, g.lane), g), fixr<BORDER>(ring.get(rs_, 1, g.lane), g),
+                fixr<BORDER>(ring.get(rs_, 2, g.lane), g));
+        const float4 fy = fixr<BORDER>(ring.get(rs_, 3, g.lane), g);
         // data curvature at row t+1: rho''(e) (A p)^2 = eps^2 rs^3 (A p)^2 (eps^2 in the affine term)
         {
             const int tz = t + 1;
-            const float yv[4] = {fy.x, fy.y, fy.z, fy.w};
-            fy = ld4<BORDER>(rowp(b.Y, sp, t + 2), g.col0, sp.W);
             if (tz >= g.r_lo && tz < g.r_hi) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float ap = fmaf(sp.ka[0], HP[s0][j], fmaf(sp.ka[1], HP[s1][j], sp.ka[2] * HP[sa][j]));
-                    if (PN == 2) {
-                        if (g.outc[j]) cd = fmaf(ap, ap, cd);
-                    } else {
-                        float z = fmaf(sp.ka[0], HX[s0][j], fmaf(sp.ka[1], HX[s1][j], sp.ka[2] * HX[sa][j]));
-                        float e = z - yv[j];
-                        float rs = rsqrtf(fmaf(e, e, eps2));
-                        float u = rs * ap;
-                        if (g.outc[j]) cd = fmaf(u * u, rs, cd);
-                    }
+                const float2 apA = fma2s(sp.ka[0], HPA[s0], fma2s(sp.ka[1], HPA[s1], mul2s(sp.ka[2], HPA[sa])));
+                const float2 apB = fma2s(sp.ka[0], HPB[s0], fma2s(sp.ka[1], HPB[s1], mul2s(sp.ka[2], HPB[sa])));
+                if (PN == 2) {
+                    cd = fma2(apA, apA, cd);
+                    cd = fma2(apB, apB, cd);
+                } else {
+                    const float2 zA = fma2s(sp.ka[0], HXA[s0], fma2s(sp.ka[1], HXA[s1], mul2s(sp.ka[2], HXA[sa])));
+                    const float2 zB = fma2s(sp.ka[0], HXB[s0], fma2s(sp.ka[1], HXB[s1], mul2s(sp.ka[2], HXB[sa])));
+                    const float2 eA = sub2(zA, lo2(fy)), eB = sub2(zB, hi2(fy));
+                    const float2 rA = rsq2(fma2(eA, eA, e2)), rB = rsq2(fma2(eB, eB, e2));
+                    const float2 uA = mul2(rA, apA), uB = mul2(rB, apB);
+                    cd = fma2(mul2(uA, uA), rA, cd);
+                    cd = fma2(mul2(uB, uB), rB, cd);
                 }
             }
         }
+        ring.release();
+        if (g.lane == 0 && t + NST < t0 + nstep) issue(t + NST);
         // BTV curvature of the pairs (t, t+d): psi''(D x) (D p)^2 = eps^2 rs^3 (D p)^2
         if (BW > 1 && t >= g.r_lo && t < g.r_hi) {
 #pragma unroll
@@ -447,32 +624,50 @@ struct UC {
                 for (int dx = 0; dx < BW; ++dx) {
                     if (dy == 0 && dx == 0) continue;
                     const int cls = dx + dy - 1;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        float dxv = XN[s0][j] - XN[sq][j + dx];
-                        float dpv = PN_[s0][j] - PN_[sq][j + dx];
-                        float rs = rsqrtf(fmaf(dxv, dxv, eps2));
-                        float u = rs * dpv;
-                        if (g.outc[j] && (!BORDER || g.cv[j + dx])) cb[cls] = fmaf(u * u, rs, cb[cls]);
+                    const float2 XD = F2(XA[sq].y, X4[sq]), XE = F2(XB[sq].y, X5[sq]);
+                    const float2 PD = F2(PA[sq].y, P4[sq]), PE = F2(PB[sq].y, P5[sq]);
+                    const float2 xA = dx == 0 ? XA[sq] : (dx == 1 ? XB[sq] : XD);
+                    const float2 xB = dx == 0 ? XB[sq] : (dx == 1 ? XD : XE);
+                    const float2 qpA = dx == 0 ? PA[sq] : (dx == 1 ? PB[sq] : PD);
+                    const float2 qpB = dx == 0 ? PB[sq] : (dx == 1 ? PD : PE);
+                    const float2 dxA = sub2(XA[s0], xA), dxB = sub2(XB[s0], xB);
+                    const float2 dpA = sub2(PA[s0], qpA), dpB = sub2(PB[s0], qpB);
+                    const float2 rA = rsq2(fma2(dxA, dxA, e2)), rB = rsq2(fma2(dxB, dxB, e2));
+                    float2 uA = mul2(rA, dpA), uB = mul2(rB, dpB);
+                    if (BORDER) {
+                        if (!g.cv0) { uA = F2(0.f, 0.f); uB = uA; }
+                        if (!g.cv4) {
+                            if (dx >= 2) uA.y = 0.f;
+                            if (dx >= 1) uB.y = 0.f;
+                        }
                     }
+                    cb[cls] = fma2(mul2(uA, uA), rA, cb[cls]);
+                    cb[cls] = fma2(mul2(uB, uB), rB, cb[cls]);
                 }
             }
         }
     }
 
     __device__ __forceinline__ void run() {
-        cd = 0.f; pp = 0.f; mu = 0.f;
+        const float2 z = F2(0.f, 0.f);
+        cd = pp = mu = z;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) cb[c] = 0.f;
-        const int t0 = g.r_lo - 2;
-        float4 xv, pv, rv;
-        load(t0, xv, pv, rv);
-        set_row(0, t0, xv, pv, rv);
-        load(t0 + 1, xv, pv, rv);
-        set_row(1, t0 + 1, xv, pv, rv);
-        load(t0 + 2, fx, fp, fr);
-        fy = ld4<BORDER>(rowp(b.Y, sp, t0 + 1), g.col0, sp.W);
-        const int nstep = sp.seg_rows + 2;
+        for (int c = 0; c < 4; ++c) cb[c] = z;
+        t0 = g.r_lo - 2;
+        nstep = sp.seg_rows + 2;
+        if (!BORDER) {
+            const size_t o = (size_t)(t0 - sp.store_lo) * sp.pitch + g.cbase;
+            ix = X0 + o + 2 * (size_t)sp.pitch;
+            ip = P0 + o + 2 * (size_t)sp.pitch;
+            ir = R0 + o + 2 * (size_t)sp.pitch;
+            iy = b.Y + o + (size_t)sp.pitch;
+        }
+        if (g.lane == 0)
+            for (int k = 0; k < NST && k < nstep; ++k) issue(t0 + k);
+        set_row(0, t0, ld4<BORDER>(rowp(X0, sp, t0), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0), g.col0, sp.W),
+                ld4<BORDER>(rrowp(b, R0, sp, t0), g.col0, sp.W));
+        set_row(1, t0 + 1, ld4<BORDER>(rowp(X0, sp, t0 + 1), g.col0, sp.W),
+                ld4<BORDER>(rowp(P0, sp, t0 + 1), g.col0, sp.W), ld4<BORDER>(rrowp(b, R0, sp, t0 + 1), g.col0, sp.W));
         for (int t = t0; t < t0 + nstep; t += 3) {
             step<0>(t);
             step<1>(t + 1);
@@ -483,6 +678,7 @@ struct UC {
 
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, 2) k_uc_stream(StencilParams sp, Buffers b, int phase) {
+    extern __shared__ __align__(128) unsigned char smem[];
     ScgState* st = b.st;
     if (phase != PH_DEBUG) {
         if (st->done) return;
@@ -495,18 +691,27 @@ __global__ void __launch_bounds__(SWPB * 32, 2) k_uc_stream(StencilParams sp, Bu
     const float au = (phase == PH_DEBUG) ? 0.0f : st->alpha_upd_f;
     const float be = (phase == PH_DEBUG) ? 0.0f : st->beta_f;
     const Geo g = geometry(sp);
+    Ring ring;
+    ring.init(smem, threadIdx.x >> 5, g.lane);
     double acc[NSLOT];
     {
         float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, c4 = 0.f, a_pp = 0.f, a_mu = 0.f;
+        const float* X = pick(b.X, xcur);
+        const float* P = pick(b.P, xcur);
+        const float* R = pick(b.R, rcur);
+        float* Xn = pick(b.X, xcur ^ 1);
+        float* Pn = pick(b.P, xcur ^ 1);
         if (!g.live) {
         } else if (g.border) {
-            UC<BW, PN, true> u(sp, b, g, pick(b.X, xcur), pick(b.P, xcur), pick(b.R, rcur), pick(b.X, xcur ^ 1), pick(b.P, xcur ^ 1), au, be);
+            UC<BW, PN, true> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
             u.run();
-            c0 = u.cd; c1 = u.cb[0]; c2 = u.cb[1]; c3 = u.cb[2]; c4 = u.cb[3]; a_pp = u.pp; a_mu = u.mu;
+            c0 = msum(u.cd, g); c1 = msum(u.cb[0], g); c2 = msum(u.cb[1], g); c3 = msum(u.cb[2], g);
+            c4 = msum(u.cb[3], g); a_pp = msum(u.pp, g); a_mu = msum(u.mu, g);
         } else {
-            UC<BW, PN, false> u(sp, b, g, pick(b.X, xcur), pick(b.P, xcur), pick(b.R, rcur), pick(b.X, xcur ^ 1), pick(b.P, xcur ^ 1), au, be);
+            UC<BW, PN, false> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
             u.run();
-            c0 = u.cd; c1 = u.cb[0]; c2 = u.cb[1]; c3 = u.cb[2]; c4 = u.cb[3]; a_pp = u.pp; a_mu = u.mu;
+            c0 = msum(u.cd, g); c1 = msum(u.cb[0], g); c2 = msum(u.cb[1], g); c3 = msum(u.cb[2], g);
+            c4 = msum(u.cb[3], g); a_pp = msum(u.pp, g); a_mu = msum(u.mu, g);
         }
         acc[0] = c0;
         acc[1] = sp.gcls[0] * c1 + sp.gcls[1] * c2 + sp.gcls[2] * c3 + sp.gcls[3] * c4;
@@ -520,33 +725,46 @@ __global__ void __launch_bounds__(SWPB * 32, 2) k_uc_stream(StencilParams sp, Bu
     }
 }
 
+template <typename K>
+cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers& b, int phase, cudaStream_t s) {
+    // opt in to > 48 KB of dynamic shared memory once per kernel instantiation (per device)
+    static const void* done[64];
+    static int ndone = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(kernel) ^ (uintptr_t)dev);
+    bool configured = false;
+    for (int i = 0; i < ndone; ++i) configured = configured || done[i] == key;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
+        if (e != cudaSuccess) return e;
+        if (ndone < 64) done[ndone++] = key;
+    }
+    kernel<<<(nw + SWPB - 1) / SWPB, SWPB * 32, RING_SMEM, s>>>(sp, b, phase);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 #define FL_SCASE(K, BW_, PN_) \
-    case BW_ * 10 + PN_: K<BW_, PN_><<<grid, SWPB * 32, 0, s>>>(sp, b, phase); break;
+    case BW_ * 10 + PN_: return launch_ring(K<BW_, PN_>, sp.nstrips * sp.nsegs, sp, b, phase, s);
 
 cudaError_t launch_value_grad_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
                                      cudaStream_t s) {
-    const int nw = sp.nstrips * sp.nsegs;
-    dim3 grid((nw + SWPB - 1) / SWPB);
     switch (bw * 10 + pn) {
         FL_SCASE(k_vg_stream, 1, 1) FL_SCASE(k_vg_stream, 1, 2) FL_SCASE(k_vg_stream, 2, 1)
         FL_SCASE(k_vg_stream, 2, 2) FL_SCASE(k_vg_stream, 3, 1) FL_SCASE(k_vg_stream, 3, 2)
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
                                       cudaStream_t s) {
-    const int nw = sp.nstrips * sp.nsegs;
-    dim3 grid((nw + SWPB - 1) / SWPB);
     switch (bw * 10 + pn) {
         FL_SCASE(k_uc_stream, 1, 1) FL_SCASE(k_uc_stream, 1, 2) FL_SCASE(k_uc_stream, 2, 1)
         FL_SCASE(k_uc_stream, 2, 2) FL_SCASE(k_uc_stream, 3, 1) FL_SCASE(k_uc_stream, 3, 2)
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 }  // namespace flmisr
