@@ -69,10 +69,12 @@ __device__ __forceinline__ float2 lo2(const float4& v) { return F2(v.x, v.y); } 
 __device__ __forceinline__ float2 hi2(const float4& v) { return F2(v.z, v.w); }   // (c1, c3)
 
 // ---- per-warp TMA ring: cp.async.bulk (1D bulk copy engine) row segments -> shared memory ----
-constexpr int NST = 4;            // stages per warp
+constexpr int NST = 3;            // stages per warp (== the row-loop unroll)
 constexpr int NARR = 4;           // rows per stage (4 arrays)
 constexpr int RING_FLOATS = NST * NARR * SCOLS;
-constexpr size_t RING_BYTES_PER_WARP = (size_t)RING_FLOATS * 4 + NST * 8;
+// ring data + mbarriers, rounded to 128 B so every warp's ring (bulk-copy destination, 16-byte
+// shared-memory vector reads) stays aligned
+constexpr size_t RING_BYTES_PER_WARP = ((size_t)RING_FLOATS * 4 + NST * 8 + 127) / 128 * 128;
 constexpr size_t RING_SMEM = SWPB * RING_BYTES_PER_WARP;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -243,6 +245,7 @@ struct VG {
     float2 GA[3], GB[3], GD[3], GE[3];   // pending r at (c0,c2), (c1,c3), (c2,c4), (c3,c5)
     float2 accd, vb[4], rr, rro;    // .x: columns c0+c1, .y: columns c2+c3
     const float *ix, *ip, *iy, *ir; // interior warps: next rows to stage (strip start column)
+    float* qw;                      // interior warps: r_new row of the current step (lane column)
     int t0, nstep;
 
     const StencilParams& sp;
@@ -260,8 +263,7 @@ struct VG {
         : sp(sp_), b(b_), g(g_), ring(ring_), X0(x), P0(p), Rold(ro), Rnew(rn), alpha(al) {}
 
     // lane 0: stage the rows of step tt (x, p at tt+2; Y at tt+1; r_old at tt)
-    __device__ __forceinline__ void issue(int tt) {
-        const int s = (tt - t0) % NST;
+    __device__ __forceinline__ void issue(int s, int tt) {
         if (BORDER) {
             ring.issue(s, rowp(X0, sp, tt + 2) + g.cbase, rowp(P0, sp, tt + 2) + g.cbase,
                        rowp(b.Y, sp, tt + 1) + g.cbase, rowp(Rold, sp, tt) + g.cbase);
@@ -288,11 +290,11 @@ struct VG {
     }
 
     template <int PH>
-    __device__ __forceinline__ void step(int t) {
+    __device__ __forceinline__ void step(int t, uint32_t par) {
         constexpr int s0 = PH % 3, s1 = (PH + 1) % 3, sa = (PH + 2) % 3;
         const float2 e2 = F2(sp.eps2, sp.eps2);
-        const int rs_ = (t - t0) % NST;
-        ring.wait(rs_, ((t - t0) / NST) & 1);
+        constexpr int rs_ = PH;   // NST == 3 == the unroll: stage index is a compile-time constant
+        ring.wait(rs_, par);
         const float4 fx = fixr<BORDER>(ring.get(rs_, 0, g.lane), g);
         const float4 fp = fixr<BORDER>(ring.get(rs_, 1, g.lane), g);
         const float4 fy = fixr<BORDER>(ring.get(rs_, 2, g.lane), g);
@@ -427,8 +429,10 @@ struct VG {
                 GA[s0].x += c4;
                 GB[s0].x += c5;
             }
+            float* rp = BORDER ? Rnew + (size_t)(t - sp.store_lo) * sp.pitch + g.col0 : qw;
+            if (!BORDER) qw += sp.pitch;
             if (orow) {
-                stp(Rnew + (size_t)(t - sp.store_lo) * sp.pitch + g.col0, GA[s0], GB[s0], g.olo, g.ohi);
+                stp(rp, GA[s0], GB[s0], g.olo, g.ohi);
                 rr = fma2(GA[s0], GA[s0], rr);
                 rr = fma2(GB[s0], GB[s0], rr);
                 rro = fma2(GA[s0], lo2(fr), rro);
@@ -445,7 +449,7 @@ struct VG {
 
         // the stage is consumed: refill it with the rows of step t + NST
         ring.release();
-        if (g.lane == 0 && t + NST < t0 + nstep) issue(t + NST);
+        if (g.lane == 0 && t + NST < t0 + nstep) issue(rs_, t + NST);
     }
 
     __device__ __forceinline__ void run() {
@@ -463,16 +467,19 @@ struct VG {
             ip = P0 + o + 2 * (size_t)sp.pitch;
             iy = b.Y + o + (size_t)sp.pitch;
             ir = Rold + o;
+            qw = Rnew + o + 4 * g.lane;
         }
         if (g.lane == 0)
-            for (int k = 0; k < NST && k < nstep; ++k) issue(t0 + k);
+            for (int k = 0; k < NST && k < nstep; ++k) issue(k, t0 + k);
         // rows t0, t0+1 of x' (the window before the first step) by direct loads
         set_x(0, ld4<BORDER>(rowp(X0, sp, t0), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0), g.col0, sp.W));
         set_x(1, ld4<BORDER>(rowp(X0, sp, t0 + 1), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0 + 1), g.col0, sp.W));
+        uint32_t par = 0;
         for (int t = t0; t < t0 + nstep; t += 3) {
-            step<0>(t);
-            step<1>(t + 1);
-            step<2>(t + 2);
+            step<0>(t, par);
+            step<1>(t + 1, par);
+            step<2>(t + 2, par);
+            par ^= 1u;
         }
     }
 };
@@ -541,8 +548,7 @@ struct UC {
                                   float bb)
         : sp(sp_), b(b_), g(g_), ring(ring_), X0(x), P0(p), R0(r), Xn(xn), Pn(pn), au(a), be(bb) {}
 
-    __device__ __forceinline__ void issue(int tt) {
-        const int s = (tt - t0) % NST;
+    __device__ __forceinline__ void issue(int s, int tt) {
         if (BORDER) {
             ring.issue(s, rowp(X0, sp, tt + 2) + g.cbase, rowp(P0, sp, tt + 2) + g.cbase,
                        rrowp(b, R0, sp, tt + 2) + g.cbase, rowp(b.Y, sp, tt + 1) + g.cbase);
@@ -584,11 +590,11 @@ struct UC {
     }
 
     template <int PH>
-    __device__ __forceinline__ void step(int t) {
+    __device__ __forceinline__ void step(int t, uint32_t par) {
         constexpr int s0 = PH % 3, s1 = (PH + 1) % 3, sa = (PH + 2) % 3;
         const float2 e2 = F2(sp.eps2, sp.eps2);
-        const int rs_ = (t - t0) % NST;
-        ring.wait(rs_, ((t - t0) / NST) & 1);
+        constexpr int rs_ = PH;   // NST == 3 == the unroll: stage index is a compile-time constant
+        ring.wait(rs_, par);
         set_row(sa, t + 2, fixr<BORDER>(ring.get(rs_, 0, g.lane), g), fixr<BORDER>(ring.get(rs_, 1, g.lane), g),
                 fixr<BORDER>(ring.get(rs_, 2, g.lane), g));
         const float4 fy = fixr<BORDER>(ring.get(rs_, 3, g.lane), g);
@@ -613,7 +619,7 @@ struct UC {
             }
         }
         ring.release();
-        if (g.lane == 0 && t + NST < t0 + nstep) issue(t + NST);
+        if (g.lane == 0 && t + NST < t0 + nstep) issue(rs_, t + NST);
         // BTV curvature of the pairs (t, t+d): psi''(D x) (D p)^2 = eps^2 rs^3 (D p)^2
         if (BW > 1 && t >= g.r_lo && t < g.r_hi) {
 #pragma unroll
@@ -663,15 +669,17 @@ struct UC {
             iy = b.Y + o + (size_t)sp.pitch;
         }
         if (g.lane == 0)
-            for (int k = 0; k < NST && k < nstep; ++k) issue(t0 + k);
+            for (int k = 0; k < NST && k < nstep; ++k) issue(k, t0 + k);
         set_row(0, t0, ld4<BORDER>(rowp(X0, sp, t0), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0), g.col0, sp.W),
                 ld4<BORDER>(rrowp(b, R0, sp, t0), g.col0, sp.W));
         set_row(1, t0 + 1, ld4<BORDER>(rowp(X0, sp, t0 + 1), g.col0, sp.W),
                 ld4<BORDER>(rowp(P0, sp, t0 + 1), g.col0, sp.W), ld4<BORDER>(rrowp(b, R0, sp, t0 + 1), g.col0, sp.W));
+        uint32_t par = 0;
         for (int t = t0; t < t0 + nstep; t += 3) {
-            step<0>(t);
-            step<1>(t + 1);
-            step<2>(t + 2);
+            step<0>(t, par);
+            step<1>(t + 1, par);
+            step<2>(t + 2, par);
+            par ^= 1u;
         }
     }
 };
