@@ -135,6 +135,23 @@ flmisr_status flmisr_destroy(flmisr_plan_t plan);
 /* Thread-local message describing the last error returned on this thread ("" if none). */
 const char* flmisr_last_error(void);
 
+/* Row band of `rank` among `world` (Eq. subfunction): rows [row_lo, row_hi) of an H-row HR
+ * image, boundaries rounded down to multiples of mag, remainder to the last band.  Host only. */
+flmisr_status flmisr_band(int32_t H, int32_t world, int32_t rank, int32_t mag, int32_t* row_lo, int32_t* row_hi);
+
+/*
+ * Single-device band emulation (tests, no NCCL): flmisr_plan_virtual builds the plan of band
+ * cfg->rank of cfg->world exactly like flmisr_plan but without a communicator (nccl_unique_id is
+ * ignored); flmisr_reconstruct_virtual runs the `g` bands plans[0..g-1] (ranks 0..g-1 of one
+ * configuration, same device) on plans[0]'s stream in Algorithm 1's order, with device-to-device
+ * copies in place of the allgather and the halo send/recv, and writes the fused image to hr_out
+ * (device, H x W).  lr_stack / x0 as in flmisr_reconstruct.  report: band 0's (all bands must agree;
+ * FLMISR_ERR_NUMERIC otherwise).
+ */
+flmisr_status flmisr_plan_virtual(const flmisr_config* cfg, flmisr_plan_t* out);
+flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const float* lr_stack, const float* x0,
+                                         float* hr_out, flmisr_report* report);
+
 /* Fill out128 (128 bytes, host) with a fresh ncclUniqueId (rank 0 calls this and broadcasts the
  * bytes to the other ranks, e.g. over the torch process group; S:288 coordinator role). */
 flmisr_status flmisr_nccl_unique_id(void* out128);

@@ -101,6 +101,8 @@ struct flmisr_plan_s {
     int row_lo = 0, row_hi = 0, store_lo = 0, store_hi = 0;
     int fast = 0;
     int stream_path = 0;   // 1: register-streaming kernels (flmisr_stream.cu), 0: tiled kernels
+    int virt = 0;          // 1: band of an in-process virtual group (flmisr_reconstruct_virtual), no NCCL
+    float* halo_mem = nullptr;   // send/recv halo rows (world > 1)
     StencilParams sp{};
     IngestParams ip{};
     Buffers b{};
@@ -149,7 +151,7 @@ void composed_taps(const flmisr_config& c, int i, std::vector<double>& kap, int&
         }
 }
 
-flmisr_status validate(const flmisr_config* c) {
+flmisr_status validate(const flmisr_config* c, bool virt) {
     if (!c) return fail(FLMISR_ERR_CONFIG, "config is NULL");
     if (c->k < 1) return fail(FLMISR_ERR_CONFIG, "k must be >= 1 (S:96)");
     if (c->lr_h < 1 || c->lr_w < 1) return fail(FLMISR_ERR_CONFIG, "lr_h and lr_w must be >= 1");
@@ -176,7 +178,8 @@ flmisr_status validate(const flmisr_config* c) {
     if (!(c->scg_lambda0 > 0.0) || !std::isfinite(c->scg_lambda0))
         return fail(FLMISR_ERR_CONFIG, "scg_lambda0 must be > 0 (S:362)");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(FLMISR_ERR_CONFIG, "need 0 <= rank < world");
-    if (c->world > 1 && !c->nccl_unique_id) return fail(FLMISR_ERR_CONFIG, "world > 1 needs nccl_unique_id");
+    if (c->world > 1 && !virt && !c->nccl_unique_id)
+        return fail(FLMISR_ERR_CONFIG, "world > 1 needs nccl_unique_id");
     return FLMISR_OK;
 }
 
@@ -186,10 +189,10 @@ extern "C" {
 
 const char* flmisr_last_error(void) { return g_last_error.c_str(); }
 
-flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
+static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, bool virt) {
     if (!out) return fail(FLMISR_ERR_CONFIG, "out is NULL");
     *out = nullptr;
-    flmisr_status vs = validate(cfg);
+    flmisr_status vs = validate(cfg, virt);
     if (vs != FLMISR_OK) return vs;
     const flmisr_config& c = *cfg;
 
@@ -222,7 +225,7 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
     const bool frac = (fy0 != 0.0 || fx0 != 0.0);
     const int kr = frac ? R + 1 : R;
     if (kr > MAXKR) return fail(FLMISR_ERR_CONFIG, "kappa radius exceeds 3");
-    if (c.world > 1 && !nccl().ok) return fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    if (c.world > 1 && !virt && !nccl().ok) return fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded");
 
     auto* p = new flmisr_plan_s();
     p->cfg = c;
@@ -232,6 +235,7 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
     p->cfg.psf = p->psf.data();
     p->cfg.nccl_unique_id = nullptr;
     p->fast = 1;
+    p->virt = virt ? 1 : 0;
     p->H = mag * c.lr_h;
     p->W = mag * c.lr_w;
     p->pitch = (p->W + 31) / 32 * 32;
@@ -401,30 +405,47 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) {
     b.halo_top = b.halo_bot = nullptr;
     b.send_top = b.send_bot = nullptr;
 
-    // ---- NCCL (world > 1): communicator + halo buffers (inner-outer border exchange) ----
+    // ---- world > 1: halo buffers (inner-outer border exchange) and the NCCL communicator ----
     if (world > 1) {
-        NcclApi& api = nccl();
-        if (!api.ok) return cleanup_fail(fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded"));
-        ncclUniqueId id;
-        std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
-        ncclResult_t r = api.CommInitRank(&p->comm, world, id, rank);
-        if (r != ncclSuccess) return cleanup_fail(fail(FLMISR_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)));
+        if (!p->stream_path)
+            return cleanup_fail(fail(FLMISR_ERR_CONFIG, "row-band partitioning (world > 1) needs the streaming path: "
+                                                        "separable PSF up to 3x3 with integer HR phases and W % 4 == 0"));
         const size_t hb = (size_t)p->eta * p->pitch * sizeof(float);
         float* hm = nullptr;
         // + 1 row: the bulk copies of a right-border strip read up to 512 B past a row's end
         e = cudaMalloc(&hm, 4 * hb + (size_t)p->pitch * sizeof(float));
         if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc halo buffers"));
-        cudaMemset(hm, 0, 4 * hb);
+        cudaMemset(hm, 0, 4 * hb + (size_t)p->pitch * sizeof(float));
+        p->halo_mem = hm;
         const size_t hf = hb / sizeof(float);
         if (rank > 0) { b.send_top = hm; p->recv_top = hm + 2 * hf; b.halo_top = p->recv_top; }
         if (rank < world - 1) { b.send_bot = hm + hf; p->recv_bot = hm + 3 * hf; b.halo_bot = p->recv_bot; }
-        if (!b.send_top && !b.send_bot) cudaFree(hm);
-        else if (!b.send_top) { /* keep allocation referenced through send_bot base */ }
+        if (!virt) {
+            NcclApi& api = nccl();
+            if (!api.ok) return cleanup_fail(fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded"));
+            ncclUniqueId id;
+            std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+            ncclResult_t r = api.CommInitRank(&p->comm, world, id, rank);
+            if (r != ncclSuccess)
+                return cleanup_fail(fail(FLMISR_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)));
+        }
     }
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("plan sync: ") + cudaGetErrorString(e)));
     *out = p;
     g_last_error.clear();
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out) { return make_plan(cfg, out, false); }
+
+flmisr_status flmisr_plan_virtual(const flmisr_config* cfg, flmisr_plan_t* out) { return make_plan(cfg, out, true); }
+
+flmisr_status flmisr_band(int32_t H, int32_t world, int32_t rank, int32_t mag, int32_t* row_lo, int32_t* row_hi) {
+    if (H < 1 || world < 1 || rank < 0 || rank >= world || mag < 1 || !row_lo || !row_hi)
+        return fail(FLMISR_ERR_CONFIG, "flmisr_band: invalid arguments");
+    *row_lo = (int32_t)(((long long)rank * H / world) / mag * mag);
+    *row_hi = (rank == world - 1) ? H : (int32_t)(((long long)(rank + 1) * H / world) / mag * mag);
     return FLMISR_OK;
 }
 
@@ -453,8 +474,7 @@ flmisr_status flmisr_destroy(flmisr_plan_t p) {
     if (!p) return FLMISR_OK;
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->comm && nccl().ok) nccl().CommDestroy(p->comm);
-    if (p->b.send_top) cudaFree(p->b.send_top);
-    else if (p->b.send_bot) cudaFree(p->b.send_bot);
+    if (p->halo_mem) cudaFree(p->halo_mem);
     if (p->mem) cudaFree(p->mem);
     if (p->dmem) cudaFree(p->dmem);
     if (p->st) cudaFree(p->st);
@@ -475,12 +495,28 @@ flmisr_status flmisr_destroy(flmisr_plan_t p) {
 
 namespace {
 
+// a1 polyphase ingest, a2 initial estimate (or the caller's x0), p0 = 0, r_old = 0, SCG state.
+flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float* x0, cudaStream_t s) {
+    const Buffers& b = p->b;
+    const int srows = p->store_hi - p->store_lo;
+    CUDA_TRY(launch_ingest(p->ip, lr_stack, const_cast<float*>(b.Y), s));
+    if (x0) {
+        CUDA_TRY(launch_hr_copy(x0 + (size_t)p->store_lo * p->W, p->W, 0, b.X[0], p->pitch, p->sp.perm, srows, p->W, s));
+    } else {
+        CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s));
+    }
+    CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
+    CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
+    CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
+    return FLMISR_OK;
+}
+
 // Enqueue one value+gradient pass and, for world > 1, the consensus allgather + scalar kernel and
 // the inner-outer border exchange of the r candidate.
 flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
     CUDA_TRY(p->stream_path ? launch_value_grad_stream(p->bw, p->pn, p->sp, p->b, phase, s)
                             : launch_value_grad(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
-    if (p->cfg.world > 1) {
+    if (p->cfg.world > 1 && !p->virt) {
         NcclApi& api = nccl();
         const int rank = p->cfg.rank, world = p->cfg.world;
         const size_t hcount = (size_t)p->eta * p->pitch;
@@ -495,8 +531,7 @@ flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
             NCCL_TRY(api.Recv(p->recv_bot, hcount, ncclFloat32, rank + 1, p->comm, s));
         }
         NCCL_TRY(api.GroupEnd());
-        (void)phase;
-        CUDA_TRY(launch_scalar_after_value(p->b, world, s));
+        CUDA_TRY(launch_scalar_after_value(p->b, world, phase, s));
     }
     return FLMISR_OK;
 }
@@ -504,7 +539,7 @@ flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
 flmisr_status enqueue_update_curv(flmisr_plan_s* p, int phase, cudaStream_t s) {
     CUDA_TRY(p->stream_path ? launch_update_curv_stream(p->bw, p->pn, p->sp, p->b, phase, s)
                             : launch_update_curv(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
-    if (p->cfg.world > 1) {
+    if (p->cfg.world > 1 && !p->virt) {
         NCCL_TRY(nccl().AllGather(p->b.rank_sums, p->b.part, NSLOT, ncclFloat64, p->comm, s));
         CUDA_TRY(launch_scalar_after_curv(p->b, p->cfg.world, s));
     }
@@ -533,16 +568,12 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
 
     // a1: polyphase ingest; a2: initial estimate, p0 = 0, r_old = 0, state
     CUDA_TRY(mark());
-    CUDA_TRY(launch_ingest(p->ip, lr_stack, const_cast<float*>(b.Y), s));
-    if (x0) {
-        CUDA_TRY(launch_hr_copy(x0 + (size_t)p->store_lo * p->W, p->W, 0, b.X[0], p->pitch, p->sp.perm, (int)srows,
-                                p->W, s));
-    } else {
-        CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s));
+    {
+        flmisr_status st0 = enqueue_setup(p, lr_stack, x0, s);
+        if (st0 != FLMISR_OK) return st0;
     }
-    CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
-    CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
-    CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
+    (void)srows;
+    (void)b;
     CUDA_TRY(mark());  // ev1: end of setup
 
     // init: f0 = J(x0), r0 = -grad J(x0) (Moller step 1), then n_iter SCG passes (Alg. 1 while-loop)
@@ -643,6 +674,90 @@ flmisr_status flmisr_profile(flmisr_plan_t p, int32_t enable, double* out8) {
         }
         pr.enabled = enable != 0;
     }
+    return FLMISR_OK;
+}
+
+// In-process virtual group: the g row bands of one reconstruction, each with its own plan (own
+// buffers, halos, state), run on ONE device and stream in Algorithm 1's order; the NCCL collectives
+// are replaced by device-to-device copies (allgather of the rank sums, halo rows to the neighbours).
+// Exercises every band-mode kernel path on a single GPU (the multi-GPU run differs only in transport).
+flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const float* lr_stack, const float* x0,
+                                         float* hr_out, flmisr_report* report) {
+    if (!plans || g < 2) return fail(FLMISR_ERR_SHAPE, "virtual group needs g >= 2 plans");
+    if (!lr_stack || !hr_out) return fail(FLMISR_ERR_SHAPE, "lr_stack and hr_out are required");
+    for (int h = 0; h < g; ++h) {
+        flmisr_plan_s* q = plans[h];
+        if (!q || !q->virt || q->cfg.world != g || q->cfg.rank != h || q->H != plans[0]->H || q->W != plans[0]->W ||
+            q->cfg.n_iter != plans[0]->cfg.n_iter || q->cfg.device != plans[0]->cfg.device)
+            return fail(FLMISR_ERR_SHAPE, "plans must be flmisr_plan_virtual bands 0..g-1 of one configuration");
+    }
+    CUDA_TRY(cudaSetDevice(plans[0]->cfg.device));
+    cudaStream_t s = plans[0]->stream;
+    const size_t hb = (size_t)plans[0]->eta * plans[0]->pitch * sizeof(float);
+    auto gather = [&]() -> flmisr_status {
+        for (int h = 0; h < g; ++h)
+            for (int r = 0; r < g; ++r)
+                CUDA_TRY(cudaMemcpyAsync(plans[h]->b.part + (size_t)r * NSLOT, plans[r]->b.rank_sums,
+                                         NSLOT * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        return FLMISR_OK;
+    };
+    auto exchange = [&]() -> flmisr_status {
+        for (int h = 0; h < g; ++h) {
+            if (h > 0)
+                CUDA_TRY(cudaMemcpyAsync(plans[h]->recv_top, plans[h - 1]->b.send_bot, hb, cudaMemcpyDeviceToDevice, s));
+            if (h < g - 1)
+                CUDA_TRY(cudaMemcpyAsync(plans[h]->recv_bot, plans[h + 1]->b.send_top, hb, cudaMemcpyDeviceToDevice, s));
+        }
+        return FLMISR_OK;
+    };
+    flmisr_status st;
+    for (int h = 0; h < g; ++h)
+        if ((st = enqueue_setup(plans[h], lr_stack, x0, s)) != FLMISR_OK) return st;
+    auto value_grad = [&](int phase) -> flmisr_status {
+        flmisr_status r;
+        for (int h = 0; h < g; ++h)
+            if ((r = enqueue_value_grad(plans[h], phase, s)) != FLMISR_OK) return r;
+        if ((r = gather()) != FLMISR_OK || (r = exchange()) != FLMISR_OK) return r;
+        for (int h = 0; h < g; ++h) CUDA_TRY(launch_scalar_after_value(plans[h]->b, g, phase, s));
+        return FLMISR_OK;
+    };
+    auto update_curv = [&]() -> flmisr_status {
+        flmisr_status r;
+        for (int h = 0; h < g; ++h)
+            if ((r = enqueue_update_curv(plans[h], PH_ITER, s)) != FLMISR_OK) return r;
+        if ((r = gather()) != FLMISR_OK) return r;
+        for (int h = 0; h < g; ++h) CUDA_TRY(launch_scalar_after_curv(plans[h]->b, g, s));
+        return FLMISR_OK;
+    };
+    if ((st = value_grad(PH_INIT)) != FLMISR_OK) return st;
+    for (int it = 0; it < plans[0]->cfg.n_iter; ++it) {
+        if ((st = update_curv()) != FLMISR_OK) return st;
+        if ((st = value_grad(PH_ITER)) != FLMISR_OK) return st;
+    }
+    for (int h = 0; h < g; ++h)
+        CUDA_TRY(launch_finalize(plans[h]->sp, plans[h]->b, hr_out, plans[h]->W, plans[h]->row_lo, plans[h]->row_hi, s));
+    // every band holds the same consensus scalars; report band 0 and check the others agree
+    const size_t ntrace = (size_t)(plans[0]->cfg.n_iter + 1) * 6;
+    for (int h = 0; h < g; ++h) {
+        CUDA_TRY(cudaMemcpyAsync(plans[h]->st_host, plans[h]->st, sizeof(ScgState), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(plans[h]->trace_host, plans[h]->b.trace, ntrace * sizeof(double), cudaMemcpyDeviceToHost,
+                                 s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int h = 1; h < g; ++h)
+        if (std::memcmp(plans[h]->trace_host, plans[0]->trace_host, ntrace * sizeof(double)) != 0 ||
+            plans[h]->st_host->k != plans[0]->st_host->k)
+            return fail(FLMISR_ERR_NUMERIC, "virtual group: bands disagree on the consensus trace");
+    const ScgState& hs = *plans[0]->st_host;
+    if (report) {
+        report->iters_run = hs.k;
+        report->accepted = hs.accepted;
+        report->converged_at = hs.converged_at;
+        report->failed_stage = hs.failed_stage;
+        report->failed_iter = hs.failed_iter;
+        if (report->f_trace) std::memcpy(report->f_trace, plans[0]->trace_host, ntrace * sizeof(double));
+    }
+    if (hs.failed_stage) return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar");
     return FLMISR_OK;
 }
 

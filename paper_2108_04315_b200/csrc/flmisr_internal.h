@@ -85,7 +85,7 @@ cudaError_t launch_value_grad_stream(int bw, int pn, const StencilParams& sp, co
                                      cudaStream_t s);
 cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
                                       cudaStream_t s);
-cudaError_t launch_scalar_after_value(const Buffers& b, int world, cudaStream_t s);  // world > 1
+cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s);  // world > 1
 cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s);   // world > 1
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,
                               cudaStream_t s);

@@ -301,13 +301,13 @@ __global__ void __launch_bounds__(NTHREADS) k_update_curv(StencilParams sp, Buff
 // Multi-GPU scalar kernels: the rank sums were allgathered into b.part[0 .. world*NSLOT); sum them
 // in rank order (identical on every rank) and run the scalar logic (Alg. 1 "Central" lines).
 // ------------------------------------------------------------------------------------------------
-__global__ void k_scalar_after_value(Buffers b, int world) {
+__global__ void k_scalar_after_value(Buffers b, int world, int phase) {
     ScgState* s = b.st;
     if (s->done) return;
     double t[NSLOT] = {0, 0, 0, 0};
     for (int r = 0; r < world; ++r)
         for (int k = 0; k < NSLOT; ++k) t[k] += b.part[r * NSLOT + k];
-    scg_after_value(s, t, b.trace, PH_ITER);
+    scg_after_value(s, t, b.trace, phase);
 }
 
 __global__ void k_scalar_after_curv(Buffers b, int world) {
@@ -465,8 +465,8 @@ cudaError_t launch_update_curv(int kr, int bw, int pn, const StencilParams& sp, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_scalar_after_value(const Buffers& b, int world, cudaStream_t s) {
-    k_scalar_after_value<<<1, 1, 0, s>>>(b, world);
+cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s) {
+    k_scalar_after_value<<<1, 1, 0, s>>>(b, world, phase);
     return cudaGetLastError();
 }
 cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s) {

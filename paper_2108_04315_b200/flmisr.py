@@ -48,7 +48,8 @@ class Report(C.Structure):
 
 EXPORTS = ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_async", "flmisr_finish",
            "flmisr_profile", "flmisr_reconstruct_host", "flmisr_destroy", "flmisr_last_error",
-           "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply")
+           "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply", "flmisr_band",
+           "flmisr_plan_virtual", "flmisr_reconstruct_virtual")
 
 
 def _load():
@@ -68,6 +69,9 @@ def _load():
     lib.flmisr_nccl_unique_id.argtypes = [vp]
     lib.flmisr_plan_info.argtypes = [vp] + [C.POINTER(C.c_int32)] * 5
     lib.flmisr_debug_apply.argtypes = [vp, C.c_int32, vp, vp, vp, vp, C.POINTER(C.c_double)]
+    lib.flmisr_band.argtypes = [C.c_int32] * 4 + [C.POINTER(C.c_int32)] * 2
+    lib.flmisr_plan_virtual.argtypes = [C.POINTER(Config), C.POINTER(vp)]
+    lib.flmisr_reconstruct_virtual.argtypes = [C.POINTER(vp), C.c_int32, vp, vp, vp, C.POINTER(Report)]
     for f in EXPORTS:
         if f == "flmisr_last_error":
             continue
@@ -91,6 +95,25 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.flmisr_nccl_unique_id(C.cast(buf, C.c_void_p)))
     return buf.raw
+
+
+def band(H: int, world: int, rank: int, mag: int):
+    """flmisr_band: owned HR rows [lo, hi) of `rank` (Eq. subfunction)."""
+    lo, hi = C.c_int32(), C.c_int32()
+    _check(_lib.flmisr_band(H, world, rank, mag, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0 draws an ncclUniqueId and broadcasts its 128 bytes over the torch process group
+    (any backend, e.g. gloo); every rank returns the same bytes."""
+    import torch
+    import torch.distributed as dist
+    buf = torch.zeros(128, dtype=torch.uint8)
+    if dist.get_rank(group) == 0:
+        buf = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
+    dist.broadcast(buf, src=0, group=group)
+    return bytes(buf.tolist())
 
 
 def _stream_handle(stream, device):
@@ -118,7 +141,7 @@ class Plan:
 
     def __init__(self, k, lr_h, lr_w, shifts, psf, mag=2, p_norm=1, l1_eps=1e-3, lam=0.05,
                  btv_alpha=0.4, btv_window=3, n_iter=20, scg_sigma0=1e-4, scg_lambda0=1e-6,
-                 rank=0, world=1, nccl_id: bytes | None = None, device=0):
+                 rank=0, world=1, nccl_id: bytes | None = None, device=0, virtual=False):
         self.shifts = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(k, 2))
         self.psf = np.ascontiguousarray(np.asarray(psf, dtype=np.float64))
         self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
@@ -129,7 +152,7 @@ class Plan:
         self.k, self.lr_h, self.lr_w, self.mag, self.n_iter = k, lr_h, lr_w, mag, n_iter
         self.rank, self.world, self.device = rank, world, device
         self._h = C.c_void_p()
-        _check(_lib.flmisr_plan(C.byref(cfg), C.byref(self._h)))
+        _check((_lib.flmisr_plan_virtual if virtual else _lib.flmisr_plan)(C.byref(cfg), C.byref(self._h)))
         vals = [C.c_int32() for _ in range(5)]
         _check(_lib.flmisr_plan_info(self._h, *[C.byref(v) for v in vals]))
         self.H, self.W, self.row_lo, self.row_hi, self.fast_path = [v.value for v in vals]
@@ -203,6 +226,21 @@ class Plan:
         sc = (C.c_double * 4)()
         _check(_lib.flmisr_debug_apply(self._h, op, _ptr(lr), _ptr(in0), _ptr(in1), _ptr(out), sc))
         return list(sc)
+
+
+def reconstruct_virtual(plans, lr_stack, x0=None, out=None):
+    """flmisr_reconstruct_virtual: the g bands of one reconstruction (plans from Plan(..., virtual=True,
+    rank=h, world=g)) on one device with copies in place of NCCL; returns (hr, report)."""
+    import torch
+    p0 = plans[0]
+    if out is None:
+        out = torch.empty((p0.H, p0.W), dtype=torch.float32, device=lr_stack.device)
+    arr = (C.c_void_p * len(plans))(*[p._h.value for p in plans])
+    trace = np.zeros((p0.n_iter + 1, 6))
+    rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
+    torch.cuda.current_stream(lr_stack.device).synchronize()
+    _check(_lib.flmisr_reconstruct_virtual(arr, len(plans), _ptr(lr_stack), _ptr(x0), _ptr(out), C.byref(rep)))
+    return out, p0._report(rep, trace)
 
 
 # ---- functional names mirroring the C ABI ----
