@@ -200,8 +200,15 @@ def run_flmisr(args):
     k, lr, mag, n_iter = len(sh), c["lr"], c["mag"], c["n_iter"]
     H = W = lr * mag
     npx = H * W
-    pl = flmisr.Plan(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, p_norm=1,
-                     l1_eps=1e-3, lam=0.05, btv_alpha=0.4, btv_window=3, n_iter=n_iter, device=local)
+    partitioned = world > 1 and args.mode == "partitioned"
+    if partitioned:   # row bands of ONE projection, NCCL halo exchange + consensus allgather
+        nid = flmisr.broadcast_unique_id()
+        pl = flmisr.Plan(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, p_norm=1,
+                         l1_eps=1e-3, lam=0.05, btv_alpha=0.4, btv_window=3, n_iter=n_iter, device=local,
+                         rank=rank, world=world, nccl_id=nid)
+    else:             # replicas: every rank reconstructs its own projection
+        pl = flmisr.Plan(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, p_norm=1,
+                         l1_eps=1e-3, lam=0.05, btv_alpha=0.4, btv_window=3, n_iter=n_iter, device=local)
     dev = torch.device("cuda", local)
     y_d = torch.from_numpy(y).to(dev)
     out_d = torch.empty((H, W), dtype=torch.float32, device=dev)
@@ -240,7 +247,8 @@ def run_flmisr(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     ms_per_step = tot_ms / args.steps
-    value = world * args.steps / (tot_ms / 1000.0)   # replicas: every rank finished `steps` projections
+    # replicas: every rank finished `steps` projections; partitioned: the ranks shared each projection
+    value = (1 if partitioned else world) * args.steps / (tot_ms / 1000.0)
 
     # e2e through the public host API: pinned host LR stack in, pinned host HR image out
     y_h = torch.from_numpy(y).pin_memory()
@@ -258,7 +266,8 @@ def run_flmisr(args):
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    e2e = {"value": world * e2e_steps / e2e_s, "unit": "proj/s", "h2d_bytes_per_step": int(y.nbytes),
+    e2e = {"value": (1 if partitioned else world) * e2e_steps / e2e_s, "unit": "proj/s",
+           "h2d_bytes_per_step": int(y.nbytes),
            "d2h_bytes_per_step": int(npx * 4)}
 
     peak, peak_src = load_peaks()
@@ -275,12 +284,14 @@ def run_flmisr(args):
     launches_per_step = 5 + 2 * n_iter
     line = {
         "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if partitioned else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOADS[cfg], "n_iter": n_iter, "hr": [H, W], "p_norm": 1, "lambda": 0.05,
                    "btv_alpha": 0.4, "btv_window": 3, "psf": "3x3 Gaussian sigma 0.5",
                    "l2": "flushed before every timed step (512 MiB device write)",
-                   "parallelism": "single GPU" if world == 1 else f"replicas x{world}"},
+                   "parallelism": "single GPU" if world == 1 else
+                   (f"row bands x{world} (NCCL halo + allgather)" if partitioned else f"replicas x{world}")},
         "scg_iters_per_s": value * n_iter,
         "accepted_fraction": float(np.mean(accepted)) / n_iter if n_iter else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -316,6 +327,8 @@ def main():
     ap.add_argument("--impl", default="flmisr", choices=["flmisr", "reference"])
     ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned"],
+                    help="N > 1: independent projections per rank (default) or row bands of one projection")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "flmisr" else args.warmup
     if args.impl == "reference":

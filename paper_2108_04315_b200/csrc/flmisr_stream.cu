@@ -110,16 +110,22 @@ struct Ring {
         }
         __syncwarp();
     }
-    // lane 0: stage s <- four 512-byte row segments
+    // whole (converged) warp: one elected lane arms stage s and issues its four 512-byte row copies;
+    // the addresses are warp-uniform, so no per-lane branch or register-to-uniform waterfall
     __device__ __forceinline__ void issue(int s, const float* a0, const float* a1, const float* a2,
                                           const float* a3) const {
         const uint32_t bar = bars + 8 * s;
-        mbar_expect_tx(bar, NARR * SCOLS * 4);
         const uint32_t d = data + (uint32_t)(s * NARR * SCOLS * 4);
-        bulk_g2s(d, a0, SCOLS * 4, bar);
-        bulk_g2s(d + SCOLS * 4, a1, SCOLS * 4, bar);
-        bulk_g2s(d + 2 * SCOLS * 4, a2, SCOLS * 4, bar);
-        bulk_g2s(d + 3 * SCOLS * 4, a3, SCOLS * 4, bar);
+        asm volatile(
+            "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\t"
+            "@P mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+            "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], 512, [%0];\n\t"
+            "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%5], 512, [%0];\n\t"
+            "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%6], [%7], 512, [%0];\n\t"
+            "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%8], [%9], 512, [%0];\n\t}"
+            ::"r"(bar), "r"(NARR * SCOLS * 4), "r"(d), "l"(a0), "r"(d + SCOLS * 4), "l"(a1), "r"(d + 2 * SCOLS * 4),
+              "l"(a2), "r"(d + 3 * SCOLS * 4), "l"(a3)
+            : "memory");
     }
     __device__ __forceinline__ void wait(int s, uint32_t parity) const {
         while (!mbar_try(bars + 8 * s, parity)) {
@@ -184,7 +190,10 @@ struct Geo {
 
 __device__ __forceinline__ Geo geometry(const StencilParams& sp) {
     Geo g;
-    const int warp = threadIdx.x >> 5;
+    // warp index through a lane-0 shuffle so the compiler sees it (and every row pointer and the
+    // ring addresses derived from it) as warp-uniform: the bulk copies then take uniform-register
+    // operands directly instead of a per-copy R2UR waterfall
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     g.lane = threadIdx.x & 31;
     const int gw = blockIdx.x * SWPB + warp;
     g.live = gw < sp.nstrips * sp.nsegs;
@@ -437,10 +446,11 @@ struct VG {
                 rr = fma2(GB[s0], GB[s0], rr);
                 rro = fma2(GA[s0], lo2(fr), rro);
                 rro = fma2(GB[s0], hi2(fr), rro);
-                // band mode: owned boundary rows of the candidate go to the neighbours
-                if (b.send_top && t - sp.row_lo < b.eta)
+                // band mode: owned boundary rows of the candidate go to the neighbours; those
+                // rows lie in the first / last segment of the band, which are border warps
+                if (BORDER && b.send_top && t - sp.row_lo < b.eta)
                     stp(b.send_top + (size_t)(t - sp.row_lo) * sp.pitch + g.col0, GA[s0], GB[s0], g.olo, g.ohi);
-                if (b.send_bot && sp.row_hi - 1 - t < b.eta)
+                if (BORDER && b.send_bot && sp.row_hi - 1 - t < b.eta)
                     stp(b.send_bot + (size_t)(t - (sp.row_hi - b.eta)) * sp.pitch + g.col0, GA[s0], GB[s0], g.olo,
                         g.ohi);
             }
@@ -449,7 +459,7 @@ struct VG {
 
         // the stage is consumed: refill it with the rows of step t + NST
         ring.release();
-        if (g.lane == 0 && t + NST < t0 + nstep) issue(rs_, t + NST);
+        if (t + NST < t0 + nstep) issue(rs_, t + NST);
     }
 
     __device__ __forceinline__ void run() {
@@ -469,8 +479,7 @@ struct VG {
             ir = Rold + o;
             qw = Rnew + o + 4 * g.lane;
         }
-        if (g.lane == 0)
-            for (int k = 0; k < NST && k < nstep; ++k) issue(k, t0 + k);
+        for (int k = 0; k < NST && k < nstep; ++k) issue(k, t0 + k);
         // rows t0, t0+1 of x' (the window before the first step) by direct loads
         set_x(0, ld4<BORDER>(rowp(X0, sp, t0), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0), g.col0, sp.W));
         set_x(1, ld4<BORDER>(rowp(X0, sp, t0 + 1), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0 + 1), g.col0, sp.W));
@@ -493,7 +502,7 @@ __global__ void __launch_bounds__(SWPB * 32, 2) k_vg_stream(StencilParams sp, Bu
     const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
     const Geo g = geometry(sp);
     Ring ring;
-    ring.init(smem, threadIdx.x >> 5, g.lane);
+    ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
     {
         const float* X = pick(b.X, xcur);
@@ -619,7 +628,7 @@ struct UC {
             }
         }
         ring.release();
-        if (g.lane == 0 && t + NST < t0 + nstep) issue(rs_, t + NST);
+        if (t + NST < t0 + nstep) issue(rs_, t + NST);
         // BTV curvature of the pairs (t, t+d): psi''(D x) (D p)^2 = eps^2 rs^3 (D p)^2
         if (BW > 1 && t >= g.r_lo && t < g.r_hi) {
 #pragma unroll
@@ -668,8 +677,7 @@ struct UC {
             ir = R0 + o + 2 * (size_t)sp.pitch;
             iy = b.Y + o + (size_t)sp.pitch;
         }
-        if (g.lane == 0)
-            for (int k = 0; k < NST && k < nstep; ++k) issue(k, t0 + k);
+        for (int k = 0; k < NST && k < nstep; ++k) issue(k, t0 + k);
         set_row(0, t0, ld4<BORDER>(rowp(X0, sp, t0), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0), g.col0, sp.W),
                 ld4<BORDER>(rrowp(b, R0, sp, t0), g.col0, sp.W));
         set_row(1, t0 + 1, ld4<BORDER>(rowp(X0, sp, t0 + 1), g.col0, sp.W),
@@ -700,7 +708,7 @@ __global__ void __launch_bounds__(SWPB * 32, 2) k_uc_stream(StencilParams sp, Bu
     const float be = (phase == PH_DEBUG) ? 0.0f : st->beta_f;
     const Geo g = geometry(sp);
     Ring ring;
-    ring.init(smem, threadIdx.x >> 5, g.lane);
+    ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
     {
         float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, c4 = 0.f, a_pp = 0.f, a_mu = 0.f;

@@ -109,11 +109,12 @@ def broadcast_unique_id(group=None) -> bytes:
     (any backend, e.g. gloo); every rank returns the same bytes."""
     import torch
     import torch.distributed as dist
-    buf = torch.zeros(128, dtype=torch.uint8)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    buf = torch.zeros(128, dtype=torch.uint8, device=dev)
     if dist.get_rank(group) == 0:
-        buf = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone()
+        buf = torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8).clone().to(dev)
     dist.broadcast(buf, src=0, group=group)
-    return bytes(buf.tolist())
+    return bytes(buf.cpu().tolist())
 
 
 def _stream_handle(stream, device):
