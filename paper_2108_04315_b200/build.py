@@ -11,7 +11,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libflmisr.so")
+LIB = os.environ.get("FLMISR_LIB", os.path.join(HERE, "libflmisr.so"))
+DEFS = os.environ.get("FLMISR_DEFS", "").split()   # e.g. "-DFLMISR_SWPB=4 -DFLMISR_SMINB=4" (tuning builds)
 SOURCES = [os.path.join(CSRC, f) for f in ("flmisr_kernels.cu", "flmisr_stream.cu", "flmisr_api.cpp")]
 HEADERS = [os.path.join(CSRC, "flmisr_internal.h"), os.path.join(CSRC, "flmisr_common.cuh"), os.path.join(ROOT, "include", "flmisr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -30,8 +31,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+        obj = os.path.join(CSRC, os.path.basename(src) + "." + os.path.basename(LIB) + ".o")
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", *DEFS,
                "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []

@@ -322,11 +322,11 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
                          std::getenv("FLMISR_FORCE_TILED") == nullptr;
         if (p->stream_path) {
             for (int i = 0; i < 3; ++i) { sp.ka[i] = (float)a3[i]; sp.kb[i] = (float)b3[i]; }
-            sp.wpb = 8;
+            sp.wpb = SWPB;
             sp.nstrips = 1 + (p->W > SCOLS - SHALO ? (p->W - (SCOLS - SHALO) + SSTEP - 1) / SSTEP : 0);
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
-            const long long cap = (long long)nsm * 2 * sp.wpb;   // 2 CTAs of 8 warps per SM
+            const long long cap = (long long)nsm * SMINB * sp.wpb;   // one wave of resident warps
             const int rows = p->row_hi - p->row_lo;
             int S = 16;
             while (S < rows && (long long)sp.nstrips * ((rows + S - 1) / S) > cap) S += 3;

@@ -54,6 +54,14 @@ struct StencilParams {
 };
 
 // Streaming kernels (flmisr_stream.cu): strips of SCOLS columns per warp, stepping by SSTEP.
+#ifndef FLMISR_SWPB
+#define FLMISR_SWPB 8
+#endif
+#ifndef FLMISR_SMINB
+#define FLMISR_SMINB 2
+#endif
+constexpr int SWPB = FLMISR_SWPB;    // warps per CTA of the streaming kernels
+constexpr int SMINB = FLMISR_SMINB;  // resident CTAs per SM they are compiled for (register budget)
 constexpr int SCOLS = 128;
 constexpr int SHALO = 2;
 constexpr int SSTEP = SCOLS - 2 * SHALO;

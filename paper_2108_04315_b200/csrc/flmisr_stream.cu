@@ -34,7 +34,6 @@
 namespace flmisr {
 namespace {
 
-constexpr int SWPB = 8;   // warps per CTA
 
 // ---- packed fp32x2 helpers (PTX f32x2 -> SASS FFMA2 / FADD2 / FMUL2 on sm_100a) ----
 __device__ __forceinline__ float2 F2(float a, float b) { return make_float2(a, b); }
@@ -494,7 +493,7 @@ struct VG {
 };
 
 template <int BW, int PN>
-__global__ void __launch_bounds__(SWPB * 32, 2) k_vg_stream(StencilParams sp, Buffers b, int phase) {
+__global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
     ScgState* st = b.st;
     if (phase != PH_DEBUG && st->done) return;
@@ -693,7 +692,7 @@ struct UC {
 };
 
 template <int BW, int PN>
-__global__ void __launch_bounds__(SWPB * 32, 2) k_uc_stream(StencilParams sp, Buffers b, int phase) {
+__global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
     ScgState* st = b.st;
     if (phase != PH_DEBUG) {

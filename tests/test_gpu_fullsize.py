@@ -1,0 +1,60 @@
+"""Parity at BASELINE.json's full size (C3: K=4 LR 2048^2 -> 4096^2) in the launch configuration
+bench.py times (streaming path, one wave of 128-column warp strips), against the fp64 oracle on the
+full image (per-operator: value, gradient, curvature), and properties of a full reconstruction."""
+import numpy as np
+import pytest
+
+from paper_2108_04315_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2108_04315_b200 import flmisr  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def c3(orc):
+    c = synth.CONFIGS["C3"]
+    y, sh, _ = synth.make_stack(c["lr"], c["mag"], seed=c["seed"])
+    pl = flmisr.Plan(k=4, lr_h=c["lr"], lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=2, n_iter=c["n_iter"])
+    pb = orc.Problem(k=4, lr_h=c["lr"], lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=2)
+    assert pl.fast_path == 2   # the streaming kernels bench.py times
+    return y, pl, pb
+
+
+def test_c3_gradient_value_curvature(orc, c3):
+    y, pl, pb = c3
+    yd = torch.from_numpy(y).cuda()
+    x0 = torch.zeros((pl.H, pl.W), device="cuda")
+    pl.debug(flmisr.OP_X0, lr=yd, out=x0)
+    x = x0.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(x, orc.init_x0(pb, y.astype(np.float64)), rtol=0, atol=1e-6)
+    r = torch.zeros_like(x0)
+    D, R, rr, _ = pl.debug(flmisr.OP_GRAD, lr=yd, in0=x0, out=r)
+    g = orc.grad(pb, x, y.astype(np.float64))
+    rn = r.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(rn + g) <= 1e-5 * np.linalg.norm(g)
+    Do, Ro = orc.value(pb, x, y.astype(np.float64))
+    assert abs(D - Do) <= 1e-5 * Do and abs(R - Ro) <= 1e-5 * Ro
+    p = synth.random_fields((pl.H, pl.W), 71, -1, 1)
+    delta, pp, mu, _ = pl.debug(flmisr.OP_CURV, lr=yd, in0=x0, in1=torch.from_numpy(p).cuda())
+    dref = orc.curv(pb, x, y.astype(np.float64), p.astype(np.float64))
+    assert abs(delta - dref) <= 1e-5 * abs(dref)
+
+
+def test_c3_reconstruction_properties(orc, c3):
+    """Full 20-pass reconstruction: objective non-increasing over accepted steps, the reported f
+    equals the oracle's J at the returned image (to fp32 summation accuracy), finite output."""
+    y, pl, pb = c3
+    hr, rep = pl.reconstruct(torch.from_numpy(y).cuda())
+    f = rep["trace"][:, 1]
+    acc = rep["trace"][:, 5] > 0
+    assert np.all(np.diff(f[acc]) <= 0)
+    assert rep["iters_run"] == 20 and rep["accepted"] >= 15
+    h = hr.cpu().numpy().astype(np.float64)
+    assert np.isfinite(h).all()
+    J = orc.objective(pb, h, y.astype(np.float64))
+    assert abs(J - f[-1]) <= 1e-5 * J
