@@ -126,6 +126,9 @@ struct flmisr_plan_s {
     int pending = 0;
     int prof_marks = 0;
     Prof prof;
+    cudaGraphExec_t graph_exec = nullptr;   // the captured SCG loop (world == 1)
+    cudaGraphExec_t graph_exec_prof = nullptr;   // the same with per-kernel event records
+    int no_graph = 0;                       // FLMISR_NO_GRAPH=1: always launch eagerly
 };
 
 namespace {
@@ -236,6 +239,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     p->cfg.nccl_unique_id = nullptr;
     p->fast = 1;
     p->virt = virt ? 1 : 0;
+    p->no_graph = std::getenv("FLMISR_NO_GRAPH") != nullptr;
     p->H = mag * c.lr_h;
     p->W = mag * c.lr_w;
     p->pitch = (p->W + 31) / 32 * 32;
@@ -486,6 +490,8 @@ flmisr_status flmisr_destroy(flmisr_plan_t p) {
     if (p->d_out) cudaFree(p->d_out);
     for (auto e : p->prof.ev) cudaEventDestroy(e);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
+    if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
+    if (p->graph_exec_prof) cudaGraphExecDestroy(p->graph_exec_prof);
     if (p->stream) cudaStreamDestroy(p->stream);
     delete p;
     return FLMISR_OK;
@@ -576,18 +582,52 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
     (void)b;
     CUDA_TRY(mark());  // ev1: end of setup
 
-    // init: f0 = J(x0), r0 = -grad J(x0) (Moller step 1), then n_iter SCG passes (Alg. 1 while-loop)
-    flmisr_status st = enqueue_value_grad(p, PH_INIT, s);
-    if (st != FLMISR_OK) return st;
-    CUDA_TRY(mark());  // ev2
-    for (int it = 0; it < p->cfg.n_iter; ++it) {
-        st = enqueue_update_curv(p, PH_ITER, s);
+    // init: f0 = J(x0), r0 = -grad J(x0) (Moller step 1), then n_iter SCG passes (Alg. 1 while-loop).
+    // Single GPU without per-kernel profiling: the whole loop (plan-owned buffers only, all control on
+    // the device) is one CUDA graph, captured on the first call and replayed into the caller's stream.
+    flmisr_status st = FLMISR_OK;
+    // the loop body; with profiling, event records between the kernels (captured as graph nodes)
+    auto loop = [&](cudaStream_t ls, int ev0) -> flmisr_status {
+        int e = ev0;
+        // external event nodes: inside a captured graph a plain record is only an internal dependency
+        auto m = [&]() -> cudaError_t {
+            return prof ? cudaEventRecordWithFlags(pr.ev[e++], ls, cudaEventRecordExternal) : cudaSuccess;
+        };
+        flmisr_status r = enqueue_value_grad(p, PH_INIT, ls);
+        if (r != FLMISR_OK) return r;
+        CUDA_TRY(m());  // ev2
+        for (int it = 0; it < p->cfg.n_iter; ++it) {
+            if ((r = enqueue_update_curv(p, PH_ITER, ls)) != FLMISR_OK) return r;
+            CUDA_TRY(m());
+            if ((r = enqueue_value_grad(p, PH_ITER, ls)) != FLMISR_OK) return r;
+            CUDA_TRY(m());
+        }
+        return FLMISR_OK;
+    };
+    const bool use_graph = p->cfg.world == 1 && !p->no_graph;
+    if (use_graph) {
+        cudaGraphExec_t& ge = prof ? p->graph_exec_prof : p->graph_exec;
+        if (!ge) {
+            cudaStream_t cs = p->stream;   // capture needs a non-legacy stream
+            CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            st = loop(cs, ev);
+            cudaGraph_t graph = nullptr;
+            cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+            if (st != FLMISR_OK) {
+                if (graph) cudaGraphDestroy(graph);
+                return st;
+            }
+            if (ce != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+            ce = cudaGraphInstantiate(&ge, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ce != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+        }
+        CUDA_TRY(cudaGraphLaunch(ge, s));
+    } else {
+        st = loop(s, ev);
         if (st != FLMISR_OK) return st;
-        CUDA_TRY(mark());
-        st = enqueue_value_grad(p, PH_ITER, s);
-        if (st != FLMISR_OK) return st;
-        CUDA_TRY(mark());
     }
+    if (prof) ev += 1 + 2 * p->cfg.n_iter;
     // a12: fuse (owned rows; rank 0 gathers the bands for world > 1)
     if (hr_out) CUDA_TRY(launch_finalize(p->sp, b, hr_out, p->W, p->row_lo, p->row_hi, s));
     if (p->cfg.world > 1) {
@@ -646,6 +686,8 @@ flmisr_status flmisr_finish(flmisr_plan_t p, flmisr_report* rep) {
         cudaEventElapsedTime(&ms, pr.ev[m], pr.ev[m + 1]); pr.ms[2] += ms;
         cudaEventElapsedTime(&ms, pr.ev[0], pr.ev[m + 1]); pr.ms[3] += ms; pr.n[3] += 1;
         pr.n[2] += 1;
+        cudaError_t pe = cudaGetLastError();   // do not leave a timing error sticky for the next launch
+        if (pe != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("profiling events: ") + cudaGetErrorString(pe));
     }
     if (h.failed_stage)
         return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar at SCG pass " + std::to_string(h.failed_iter) +

@@ -482,8 +482,65 @@ cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, 
 
 static dim3 rowgrid(int W, int rows) { return dim3((W + 255) / 256, rows); }
 
+// Vectorised setup/output kernels for the streaming path's permuted layout (W % 4 == 0): one thread
+// per group of four HR columns, 16-byte stores.
+// mag = 2: the group (c0, c2 | c1, c3) of HR row u holds LR columns (2q, 2q+1) of the frames with
+// phases (u & 1, 0) and (u & 1, 1) -- two 8-byte loads, one 16-byte store.
+__global__ void k_ingest_m2(IngestParams ip, const float* __restrict__ lr, float* __restrict__ Y) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = ip.store_lo + blockIdx.y;
+    if (4 * q >= ip.W || gy >= ip.store_hi) return;
+    const int py = gy & 1;
+    const int f0 = ip.frame_of_phase[py * 2], f1 = ip.frame_of_phase[py * 2 + 1];
+    const int a0 = (gy - ip.sy[f0]) >> 1, a1 = (gy - ip.sy[f1]) >> 1;
+    const float2 v0 = __ldg(reinterpret_cast<const float2*>(lr + ((size_t)f0 * ip.lr_h + a0) * ip.lr_w + 2 * q));
+    const float2 v1 = __ldg(reinterpret_cast<const float2*>(lr + ((size_t)f1 * ip.lr_h + a1) * ip.lr_w + 2 * q));
+    *reinterpret_cast<float4*>(Y + (size_t)(gy - ip.store_lo) * ip.pitch + 4 * q) = make_float4(v0.x, v0.y, v1.x, v1.y);
+}
+
+__device__ __forceinline__ float bilerp_x0(const IngestParams& ip, const float* __restrict__ y, int gy, int gx) {
+    float a = ((float)gy - ip.t0y) / (float)ip.mag, c = ((float)gx - ip.t0x) / (float)ip.mag;
+    float a0 = floorf(a), c0 = floorf(c);
+    float fa = a - a0, fc = c - c0;
+    int ia0 = clampi((int)a0, 0, ip.lr_h - 1), ia1 = clampi((int)a0 + 1, 0, ip.lr_h - 1);
+    int ic0 = clampi((int)c0, 0, ip.lr_w - 1), ic1 = clampi((int)c0 + 1, 0, ip.lr_w - 1);
+    return (1.f - fa) * (1.f - fc) * __ldg(y + (size_t)ia0 * ip.lr_w + ic0) +
+           (1.f - fa) * fc * __ldg(y + (size_t)ia0 * ip.lr_w + ic1) +
+           fa * (1.f - fc) * __ldg(y + (size_t)ia1 * ip.lr_w + ic0) + fa * fc * __ldg(y + (size_t)ia1 * ip.lr_w + ic1);
+}
+
+__global__ void k_init_x0_perm(IngestParams ip, const float* __restrict__ lr, float* __restrict__ X) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = ip.store_lo + blockIdx.y;
+    if (4 * q >= ip.W || gy >= ip.store_hi) return;
+    const int c = 4 * q;
+    *reinterpret_cast<float4*>(X + (size_t)(gy - ip.store_lo) * ip.pitch + c) =
+        make_float4(bilerp_x0(ip, lr, gy, c), bilerp_x0(ip, lr, gy, c + 2), bilerp_x0(ip, lr, gy, c + 1),
+                    bilerp_x0(ip, lr, gy, c + 3));
+}
+
+__global__ void k_finalize_perm(StencilParams sp, Buffers b, float* __restrict__ out, int out_pitch, int row_lo,
+                                int row_hi) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = row_lo + blockIdx.y;
+    if (4 * q >= sp.W || gy >= row_hi) return;
+    const ScgState* s = b.st;
+    const float a = s->success ? s->alpha_upd_f : 0.0f;
+    const size_t off = (size_t)(gy - sp.store_lo) * sp.pitch + 4 * q;
+    const float4 x = *reinterpret_cast<const float4*>(pick(b.X, s->xcur) + off);
+    const float4 p = *reinterpret_cast<const float4*>(pick(b.P, s->xcur) + off);
+    // stored (c0, c2, c1, c3) -> natural (c0, c1, c2, c3)
+    *reinterpret_cast<float4*>(out + (size_t)gy * out_pitch + 4 * q) =
+        make_float4(fmaf(a, p.x, x.x), fmaf(a, p.z, x.z), fmaf(a, p.y, x.y), fmaf(a, p.w, x.w));
+}
+
+static bool vec4_ok(int perm, int W, int pitch) { return perm && W % 4 == 0 && pitch % 4 == 0; }
+
 cudaError_t launch_ingest(const IngestParams& ip, const float* lr, float* Y, cudaStream_t s) {
-    k_ingest<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, Y);
+    if (vec4_ok(ip.perm, ip.W, ip.pitch) && ip.mag == 2 && ip.lr_w % 2 == 0)
+        k_ingest_m2<<<rowgrid(ip.W / 4, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, Y);
+    else
+        k_ingest<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, Y);
     return cudaGetLastError();
 }
 cudaError_t launch_egest(const IngestParams& ip, const float* Yhr, float* lr, cudaStream_t s) {
@@ -497,12 +554,18 @@ cudaError_t launch_hr_copy(const float* src, int src_pitch, int src_perm, float*
     return cudaGetLastError();
 }
 cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s) {
-    k_init_x0<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X);
+    if (vec4_ok(ip.perm, ip.W, ip.pitch))
+        k_init_x0_perm<<<rowgrid(ip.W / 4, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X);
+    else
+        k_init_x0<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X);
     return cudaGetLastError();
 }
 cudaError_t launch_finalize(const StencilParams& sp, const Buffers& b, float* out, int out_pitch, int row_lo,
                             int row_hi, cudaStream_t s) {
-    k_finalize<<<rowgrid(sp.W, row_hi - row_lo), 256, 0, s>>>(sp, b, out, out_pitch, row_lo, row_hi);
+    if (vec4_ok(sp.perm, sp.W, sp.pitch) && out_pitch % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+        k_finalize_perm<<<rowgrid(sp.W / 4, row_hi - row_lo), 256, 0, s>>>(sp, b, out, out_pitch, row_lo, row_hi);
+    else
+        k_finalize<<<rowgrid(sp.W, row_hi - row_lo), 256, 0, s>>>(sp, b, out, out_pitch, row_lo, row_hi);
     return cudaGetLastError();
 }
 cudaError_t launch_forward_debug(int kr, const StencilParams& sp, const float* x, float* z, cudaStream_t s) {
