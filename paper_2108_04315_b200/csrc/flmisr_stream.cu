@@ -222,6 +222,9 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp) {
     // interior warps: no image border, every row they touch (r_lo - 2 .. r_hi + 2) is an owned row of
     // the band, so they need no clamps, no halo buffers and no masks beyond the strip's output columns
     g.border = g.strip0 || g.rstrip || g.r_lo < sp.row_lo + 3 || g.r_hi > sp.row_hi - 3;
+#ifdef FLMISR_ALL_BORDER   // tuning build: every warp takes the border instantiation
+    g.border = true;
+#endif
     return g;
 }
 
