@@ -171,7 +171,10 @@ typedef enum {
     FLMISR_OP_GRAD = 2,    /* in0 = x, lr = y            -> out = -grad J(x) (H x W); s[0..1] = D, R      */
     FLMISR_OP_CURV = 3,    /* in0 = x, in1 = p, lr = y   -> s[0] = p^T Hess J(x) p, s[1] = <p,p>          */
     FLMISR_OP_VALUE = 4,   /* in0 = x, lr = y            -> s[0] = D(x), s[1] = R(x)  (J = D + lambda R)  */
-    FLMISR_OP_X0 = 5       /* lr = y                     -> out = bilinear initial estimate (H x W)       */
+    FLMISR_OP_X0 = 5,      /* lr = y                     -> out = bilinear initial estimate (H x W)       */
+    FLMISR_OP_INTERP = 6   /* lr = y -> out = multi-image interpolation fusion: every LR pixel at
+                              its integer HR site (the polyphase interleave; all sites are covered on
+                              the fast path)                                                             */
 } flmisr_op;
 
 flmisr_status flmisr_debug_apply(flmisr_plan_t plan, int32_t op, const float* lr_stack, const float* in0,

@@ -560,3 +560,27 @@ double orc_value_rows(const orc_problem* pb, const double* x, const double* y, i
 }
 
 void orc_band_bounds(int H, int g, int mag, int h, int* lo, int* hi) { band_bounds(H, g, mag, h, lo, hi); }
+
+/* Multi-image interpolation fusion (tab:runtime "interpolation" row P:432): every
+ * LR pixel is inserted at its integer HR location r*(a,b) + s_i (frames with a fractional phase are
+ * not inserted); HR sites no frame covers take the bilinear upsample of frame 0 (orc_init_x0).
+ * The first frame (in index order) that covers a site wins. */
+void orc_interp_fuse(const orc_problem* pb, const double* y, double* out)
+{
+    int H = H_of(pb), W = W_of(pb);
+    orc_init_x0(pb, y, out);
+    unsigned char* done = (unsigned char*)calloc((size_t)H * W, 1);
+    for (int i = 0; i < pb->k; ++i) {
+        double ty = pb->mag * pb->shifts[2 * i], tx = pb->mag * pb->shifts[2 * i + 1];
+        if (ty != floor(ty) || tx != floor(tx)) continue;
+        int sy = (int)ty, sx = (int)tx;
+        for (int a = 0; a < pb->lr_h; ++a)
+            for (int b = 0; b < pb->lr_w; ++b) {
+                int u = pb->mag * a + sy, v = pb->mag * b + sx;
+                if (u < 0 || u >= H || v < 0 || v >= W || (done && done[(size_t)u * W + v])) continue;
+                out[(size_t)u * W + v] = y[((size_t)i * pb->lr_h + a) * pb->lr_w + b];
+                if (done) done[(size_t)u * W + v] = 1;
+            }
+    }
+    free(done);
+}

@@ -61,6 +61,7 @@ def lib():
         _lib.orc_curv.argtypes = [pp, dp, dp, dp]
         _lib.orc_curv.restype = C.c_double
         _lib.orc_init_x0.argtypes = [pp, dp, dp]
+        _lib.orc_interp_fuse.argtypes = [pp, dp, dp]
         _lib.orc_scg.argtypes = [pp, dp, dp, C.c_int, C.c_int, C.c_double, C.c_double,
                                  C.c_int, C.c_int, dp, dp, C.POINTER(_Stats)]
         _lib.orc_value_rows.argtypes = [pp, dp, dp, C.c_int, C.c_int]
@@ -178,6 +179,15 @@ def init_x0(pb: Problem, y) -> np.ndarray:
     c = pb.c()
     lib().orc_init_x0(C.byref(c), _dp(y), _dp(x0))
     return x0
+
+
+def interp_fuse(pb: Problem, y) -> np.ndarray:
+    """Multi-image interpolation fusion: LR pixels at their integer HR sites, bilinear elsewhere."""
+    y = _f64(y).reshape(pb.k, pb.lr_h, pb.lr_w)
+    out = np.zeros((pb.H, pb.W))
+    c = pb.c()
+    lib().orc_interp_fuse(C.byref(c), _dp(y), _dp(out))
+    return out
 
 
 def band_bounds(H: int, g: int, mag: int, h: int):

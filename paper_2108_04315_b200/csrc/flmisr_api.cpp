@@ -106,6 +106,9 @@ struct flmisr_plan_s {
     StencilParams sp{};
     IngestParams ip{};
     Buffers b{};
+    GenParams gp{};          // general-geometry path (fast == 0)
+    float* gmem = nullptr;   // general path: taps, LR copy, rho' weights
+    double* gpart = nullptr; // general path: first-pass partials
     size_t hr_bytes = 0;     // bytes of one stored HR buffer
     float* mem = nullptr;    // one allocation for all HR buffers
     double* dmem = nullptr;  // partials + rank sums + trace + gathered
@@ -220,14 +223,16 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         if (frame_of_phase[ph] >= 0) fast = false;
         else frame_of_phase[ph] = i;
     }
-    if (!fast)
+    if (std::getenv("FLMISR_FORCE_GENERAL")) fast = false;
+    if (!fast && c.world > 1)
         return fail(FLMISR_ERR_CONFIG,
-                    "unsupported geometry: this build implements the polyphase-complete fast path (K = mag^2 "
-                    "frames with distinct integer HR phases in [0,mag)^2 and one common sub-pixel remainder); "
-                    "general shifts are SURVEY 8(f) NEXT-2");
+                    "row-band partitioning (world > 1) needs the polyphase fast path (K = mag^2 frames with distinct "
+                    "integer HR phases in [0,mag)^2 and one common sub-pixel remainder); general geometries run on "
+                    "one GPU per projection");
+    if (!fast && K > GMAXK) return fail(FLMISR_ERR_CONFIG, "the general-geometry path supports k <= 64 frames");
     const bool frac = (fy0 != 0.0 || fx0 != 0.0);
-    const int kr = frac ? R + 1 : R;
-    if (kr > MAXKR) return fail(FLMISR_ERR_CONFIG, "kappa radius exceeds 3");
+    const int kr = fast ? (frac ? R + 1 : R) : R + 1;
+    if (fast && kr > MAXKR) return fail(FLMISR_ERR_CONFIG, "kappa radius exceeds 3");
     if (c.world > 1 && !virt && !nccl().ok) return fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded");
 
     auto* p = new flmisr_plan_s();
@@ -237,7 +242,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     p->cfg.shifts = p->shifts.data();
     p->cfg.psf = p->psf.data();
     p->cfg.nccl_unique_id = nullptr;
-    p->fast = 1;
+    p->fast = fast ? 1 : 0;
     p->virt = virt ? 1 : 0;
     p->no_graph = std::getenv("FLMISR_NO_GRAPH") != nullptr;
     p->H = mag * c.lr_h;
@@ -254,7 +259,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         lo = (int)(((long long)h * p->H / world) / mag * mag);
         hi = (h == world - 1) ? p->H : (int)(((long long)(h + 1) * p->H / world) / mag * mag);
     };
-    for (int h = 0; h < world; ++h) {
+    for (int h = 0; h < world && world > 1; ++h) {
         int lo, hi;
         band(h, lo, hi);
         if (hi - lo < std::max(p->eta, 1)) {
@@ -322,7 +327,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 3; ++j) err = std::max(err, std::fabs(K3[i * 3 + j] - a3[i] * b3[j]));
         const bool separable = kr <= 1 && err <= 1e-12 * std::fabs(K3[pm]);
-        p->stream_path = separable && (p->W % 4 == 0) && p->W >= 8 && p->H >= 4 &&
+        p->stream_path = fast && separable && (p->W % 4 == 0) && p->W >= 8 && p->H >= 4 &&
                          std::getenv("FLMISR_FORCE_TILED") == nullptr;
         if (p->stream_path) {
             for (int i = 0; i < 3; ++i) { sp.ka[i] = (float)a3[i]; sp.kb[i] = (float)b3[i]; }
@@ -357,8 +362,10 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     ip.H = p->H; ip.W = p->W; ip.pitch = p->pitch; ip.k = K; ip.lr_h = c.lr_h; ip.lr_w = c.lr_w; ip.mag = mag;
     ip.store_lo = p->store_lo; ip.store_hi = p->store_hi;
     for (int i = 0; i < 16; ++i) { ip.frame_of_phase[i] = 0; ip.sy[i] = 0; ip.sx[i] = 0; }
-    for (int ph = 0; ph < mag * mag; ++ph) ip.frame_of_phase[ph] = frame_of_phase[ph];
-    for (int i = 0; i < K; ++i) { ip.sy[i] = sy[i]; ip.sx[i] = sx[i]; }
+    if (fast) {
+        for (int ph = 0; ph < mag * mag; ++ph) ip.frame_of_phase[ph] = frame_of_phase[ph];
+        for (int i = 0; i < K; ++i) { ip.sy[i] = sy[i]; ip.sx[i] = sx[i]; }
+    }
     ip.t0y = (float)(mag * c.shifts[0]);
     ip.t0x = (float)(mag * c.shifts[1]);
     ip.perm = sp.perm = p->stream_path;
@@ -384,7 +391,9 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     b.P[0] = p->mem + 3 * fl; b.P[1] = p->mem + 4 * fl;
     b.R[0] = p->mem + 5 * fl; b.R[1] = p->mem + 6 * fl;
     const size_t nsblk = p->stream_path ? ((size_t)sp.nstrips * sp.nsegs + sp.wpb - 1) / sp.wpb : 0;
-    const size_t ntiles = std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk);
+    const long long nlr_px = (long long)K * c.lr_h * c.lr_w, nhr_px = (long long)p->H * p->W;
+    const size_t ngblk = fast ? 0 : std::max<size_t>(gen_blocks(nlr_px), gen_blocks(nhr_px));
+    const size_t ntiles = std::max<size_t>(std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk), ngblk);
     const size_t npart = std::max<size_t>(NSLOT * ntiles, (size_t)NSLOT * world);
     const size_t ntrace = (size_t)(c.n_iter + 1) * 6;
     const size_t nd = npart + NSLOT + ntrace + (size_t)NSLOT * world;
@@ -408,6 +417,41 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     b.eta = p->eta;
     b.halo_top = b.halo_bot = nullptr;
     b.send_top = b.send_bot = nullptr;
+
+    // ---- general-geometry path: per-frame taps and phases, LR copy, rho' weights (flmisr_general.cu) ----
+    if (!fast) {
+        GenParams& gp = p->gp;
+        gp.k = K; gp.lr_h = c.lr_h; gp.lr_w = c.lr_w; gp.mag = mag;
+        gp.R = R; gp.kd = 2 * R + 2;
+        gp.nblk_lr = (int)gen_blocks(nlr_px);
+        gp.nblk_hr = (int)gen_blocks(nhr_px);
+        gp.fy_lo = 0; gp.fx_lo = 0; gp.fy_hi = p->H - 1; gp.fx_hi = p->W - 1;
+        const size_t ntap = (size_t)K * gp.kd * gp.kd;
+        std::vector<float> taps(ntap);
+        for (int i = 0; i < K; ++i) {
+            std::vector<double> kap;
+            double fy, fx;
+            int syi, sxi;
+            composed_taps(c, i, kap, syi, sxi, fy, fx);
+            for (size_t j = 0; j < kap.size(); ++j) taps[(size_t)i * gp.kd * gp.kd + j] = (float)kap[j];
+            gp.sy[i] = syi; gp.sx[i] = sxi;
+            gp.integer_phase[i] = (fy == 0.0 && fx == 0.0);
+            gp.fy_lo = std::min(gp.fy_lo, syi - R);
+            gp.fx_lo = std::min(gp.fx_lo, sxi - R);
+            gp.fy_hi = std::max(gp.fy_hi, mag * (c.lr_h - 1) + syi + R + 1);
+            gp.fx_hi = std::max(gp.fx_hi, mag * (c.lr_w - 1) + sxi + R + 1);
+        }
+        const size_t gbytes = ntap * sizeof(float) + 2 * (size_t)nlr_px * sizeof(float);
+        e = cudaMalloc(&p->gmem, gbytes);
+        if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc general-path buffers"));
+        e = cudaMalloc(&p->gpart, (size_t)NSLOT * ngblk * sizeof(double));
+        if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc general-path partials"));
+        cudaMemcpy(p->gmem, taps.data(), ntap * sizeof(float), cudaMemcpyHostToDevice);
+        gp.taps = p->gmem;
+        gp.lr = p->gmem + ntap;
+        gp.w = p->gmem + ntap + nlr_px;
+        gp.part_a = p->gpart;
+    }
 
     // ---- world > 1: halo buffers (inner-outer border exchange) and the NCCL communicator ----
     if (world > 1) {
@@ -479,6 +523,8 @@ flmisr_status flmisr_destroy(flmisr_plan_t p) {
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->comm && nccl().ok) nccl().CommDestroy(p->comm);
     if (p->halo_mem) cudaFree(p->halo_mem);
+    if (p->gmem) cudaFree(p->gmem);
+    if (p->gpart) cudaFree(p->gpart);
     if (p->mem) cudaFree(p->mem);
     if (p->dmem) cudaFree(p->dmem);
     if (p->st) cudaFree(p->st);
@@ -505,7 +551,13 @@ namespace {
 flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float* x0, cudaStream_t s) {
     const Buffers& b = p->b;
     const int srows = p->store_hi - p->store_lo;
-    CUDA_TRY(launch_ingest(p->ip, lr_stack, const_cast<float*>(b.Y), s));
+    if (p->fast) {
+        CUDA_TRY(launch_ingest(p->ip, lr_stack, const_cast<float*>(b.Y), s));
+    } else {   // general path: the kernels read the frames in their own layout from a plan-owned copy
+        CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(p->gp.lr), lr_stack,
+                                 (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
+    }
     if (x0) {
         CUDA_TRY(launch_hr_copy(x0 + (size_t)p->store_lo * p->W, p->W, 0, b.X[0], p->pitch, p->sp.perm, srows, p->W, s));
     } else {
@@ -519,9 +571,20 @@ flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float
 
 // Enqueue one value+gradient pass and, for world > 1, the consensus allgather + scalar kernel and
 // the inner-outer border exchange of the r candidate.
+cudaError_t launch_vg(flmisr_plan_s* p, int phase, cudaStream_t s) {
+    if (!p->fast) return launch_gen_value_grad(p->bw, p->pn, p->sp, p->gp, p->b, phase, s);
+    return p->stream_path ? launch_value_grad_stream(p->bw, p->pn, p->sp, p->b, phase, s)
+                          : launch_value_grad(p->kr, p->bw, p->pn, p->sp, p->b, phase, s);
+}
+
+cudaError_t launch_uc(flmisr_plan_s* p, int phase, cudaStream_t s) {
+    if (!p->fast) return launch_gen_update_curv(p->bw, p->pn, p->sp, p->gp, p->b, phase, s);
+    return p->stream_path ? launch_update_curv_stream(p->bw, p->pn, p->sp, p->b, phase, s)
+                          : launch_update_curv(p->kr, p->bw, p->pn, p->sp, p->b, phase, s);
+}
+
 flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
-    CUDA_TRY(p->stream_path ? launch_value_grad_stream(p->bw, p->pn, p->sp, p->b, phase, s)
-                            : launch_value_grad(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
+    CUDA_TRY(launch_vg(p, phase, s));
     if (p->cfg.world > 1 && !p->virt) {
         NcclApi& api = nccl();
         const int rank = p->cfg.rank, world = p->cfg.world;
@@ -543,8 +606,7 @@ flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
 }
 
 flmisr_status enqueue_update_curv(flmisr_plan_s* p, int phase, cudaStream_t s) {
-    CUDA_TRY(p->stream_path ? launch_update_curv_stream(p->bw, p->pn, p->sp, p->b, phase, s)
-                            : launch_update_curv(p->kr, p->bw, p->pn, p->sp, p->b, phase, s));
+    CUDA_TRY(launch_uc(p, phase, s));
     if (p->cfg.world > 1 && !p->virt) {
         NCCL_TRY(nccl().AllGather(p->b.rank_sums, p->b.part, NSLOT, ncclFloat64, p->comm, s));
         CUDA_TRY(launch_scalar_after_curv(p->b, p->cfg.world, s));
@@ -863,38 +925,64 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
     StencilParams sp0 = p->sp;
     sp0.perm = 0;
     CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
+    const bool gen = !p->fast;
+    const size_t lr_bytes = (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w * sizeof(float);
+    // the LR stack in the layout the data-term kernels read (polyphase Y, or the general path's copy)
+    auto put_lr = [&](const float* src) -> cudaError_t {
+        return gen ? cudaMemcpyAsync(const_cast<float*>(p->gp.lr), src, lr_bytes, cudaMemcpyDeviceToDevice, s)
+                   : launch_ingest(p->ip, src, const_cast<float*>(b.Y), s);
+    };
     switch (op) {
         case FLMISR_OP_FORWARD:
             if (!in0 || !out) return fail(FLMISR_ERR_SHAPE, "FORWARD needs in0 and out");
             CUDA_TRY(launch_hr_copy(in0, p->W, 0, b.X[0], p->pitch, 0, H, p->W, s));
-            CUDA_TRY(launch_forward_debug(p->kr, sp0, b.X[0], b.R[0], s));
-            CUDA_TRY(launch_egest(ip0, b.R[0], out, s));
+            if (gen) {
+                CUDA_TRY(launch_gen_forward(sp0, p->gp, b.X[0], out, s));
+            } else {
+                CUDA_TRY(launch_forward_debug(p->kr, sp0, b.X[0], b.R[0], s));
+                CUDA_TRY(launch_egest(ip0, b.R[0], out, s));
+            }
             break;
         case FLMISR_OP_ADJOINT:
             if (!in0 || !out) return fail(FLMISR_ERR_SHAPE, "ADJOINT needs in0 and out");
-            CUDA_TRY(launch_ingest(ip0, in0, b.R[0], s));
-            CUDA_TRY(launch_adjoint_debug(p->kr, sp0, b.R[0], b.R[1], s));
+            if (gen) {
+                CUDA_TRY(cudaMemcpyAsync(p->gp.w, in0, lr_bytes, cudaMemcpyDeviceToDevice, s));
+                CUDA_TRY(launch_gen_adjoint(sp0, p->gp, p->gp.w, b.R[1], s));
+            } else {
+                CUDA_TRY(launch_ingest(ip0, in0, b.R[0], s));
+                CUDA_TRY(launch_adjoint_debug(p->kr, sp0, b.R[0], b.R[1], s));
+            }
             CUDA_TRY(launch_hr_copy(b.R[1], p->pitch, 0, out, p->W, 0, H, p->W, s));
             break;
         case FLMISR_OP_GRAD:
         case FLMISR_OP_VALUE:
             if (!lr || !in0) return fail(FLMISR_ERR_SHAPE, "GRAD/VALUE need lr and in0");
-            CUDA_TRY(launch_ingest(p->ip, lr, const_cast<float*>(b.Y), s));
+            CUDA_TRY(put_lr(lr));
             CUDA_TRY(put_hr(b.X[0], in0));
             CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
             CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
-            CUDA_TRY(p->stream_path ? launch_value_grad_stream(p->bw, p->pn, p->sp, b, PH_DEBUG, s)
-                                    : launch_value_grad(p->kr, p->bw, p->pn, p->sp, b, PH_DEBUG, s));
+            CUDA_TRY(launch_vg(p, PH_DEBUG, s));
             if (op == FLMISR_OP_GRAD && out) CUDA_TRY(get_hr(out, b.R[1]));
             break;
         case FLMISR_OP_CURV:
             if (!lr || !in0 || !in1) return fail(FLMISR_ERR_SHAPE, "CURV needs lr, in0 and in1");
-            CUDA_TRY(launch_ingest(p->ip, lr, const_cast<float*>(b.Y), s));
+            CUDA_TRY(put_lr(lr));
             CUDA_TRY(put_hr(b.X[0], in0));
             CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
             CUDA_TRY(put_hr(b.R[0], in1));
-            CUDA_TRY(p->stream_path ? launch_update_curv_stream(p->bw, p->pn, p->sp, b, PH_DEBUG, s)
-                                    : launch_update_curv(p->kr, p->bw, p->pn, p->sp, b, PH_DEBUG, s));
+            CUDA_TRY(launch_uc(p, PH_DEBUG, s));
+            break;
+        case FLMISR_OP_INTERP:
+            if (!lr || !out) return fail(FLMISR_ERR_SHAPE, "INTERP needs lr and out");
+            if (gen) {   // bilinear estimate everywhere, then the integer-phase frames' pixels on their sites
+                CUDA_TRY(put_lr(lr));
+                CUDA_TRY(launch_init_x0(ip0, lr, b.R[0], s));
+                CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, H, p->W, s));
+                CUDA_TRY(launch_gen_interp(sp0, p->gp, out, p->W, s));
+            } else {     // polyphase-complete stack: every HR site holds exactly one LR pixel
+                CUDA_TRY(launch_ingest(ip0, lr, b.R[0], s));
+                CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, H, p->W, s));
+            }
             break;
         case FLMISR_OP_X0:
             if (!lr || !out) return fail(FLMISR_ERR_SHAPE, "X0 needs lr and out");

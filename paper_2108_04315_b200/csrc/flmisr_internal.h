@@ -107,6 +107,29 @@ struct IngestParams {
     int perm;                    // 1: HR buffers use the streaming path's permuted column layout
 };
 
+// General-geometry path (flmisr_general.cu): per-frame integer phase and composed kernel.
+constexpr int GMAXK = 64;                                // frames supported by the general path
+struct GenParams {
+    int k, lr_h, lr_w, mag;
+    int R, kd;                   // kappa offsets [-R, R+1] per axis, kd = 2R + 2
+    int fy_lo, fy_hi, fx_lo, fx_hi;   // virtual HR rows/cols any forward sample reads (clamp folding)
+    int nblk_lr, nblk_hr;        // CTAs of the LR-pixel and HR-pixel passes
+    const float* taps;           // k x kd x kd, kappa_i(P, Q) at [i][P + R][Q + R] (correlation orientation)
+    const float* lr;             // plan-owned copy of the LR stack (k x lr_h x lr_w)
+    float* w;                    // rho'(e) per LR pixel (k x lr_h x lr_w)
+    double* part_a;              // NSLOT x max(nblk) partials of the first pass of each pair
+    int sy[GMAXK], sx[GMAXK];    // integer HR phase floor(mag * shift_i)
+    int integer_phase[GMAXK];    // 1: mag * shift_i is integral (interpolation fusion inserts the frame)
+};
+cudaError_t launch_gen_value_grad(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
+                                  int phase, cudaStream_t s);
+cudaError_t launch_gen_update_curv(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
+                                   int phase, cudaStream_t s);
+cudaError_t launch_gen_forward(const StencilParams& sp, const GenParams& gp, const float* x, float* y, cudaStream_t s);
+cudaError_t launch_gen_adjoint(const StencilParams& sp, const GenParams& gp, const float* w, float* g, cudaStream_t s);
+cudaError_t launch_gen_interp(const StencilParams& sp, const GenParams& gp, float* out, int out_pitch, cudaStream_t s);
+unsigned gen_blocks(long long n);
+
 // Streaming-path column layout: each aligned group of 4 columns is stored as (c0, c2, c1, c3).
 __host__ __device__ __forceinline__ int phys_col(int c, int perm) {
     return perm ? ((c & ~3) | ((c & 1) << 1) | ((c >> 1) & 1)) : c;

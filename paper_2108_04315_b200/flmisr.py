@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FLMISR_LIB", os.path.join(_HERE, "libflmisr.so"))
 
 OK, ERR_CONFIG, ERR_SHAPE, ERR_CUDA, ERR_NCCL, ERR_NUMERIC = 0, -1, -2, -3, -4, -5
-OP_FORWARD, OP_ADJOINT, OP_GRAD, OP_CURV, OP_VALUE, OP_X0 = range(6)
+OP_FORWARD, OP_ADJOINT, OP_GRAD, OP_CURV, OP_VALUE, OP_X0, OP_INTERP = range(7)
 
 
 class FlmisrError(RuntimeError):

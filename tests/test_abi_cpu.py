@@ -46,9 +46,11 @@ def cfg(**kw):
     (dict(btv_window=4), "btv_window"),
     (dict(lam=-1.0), "lambda"),
     (dict(mag=5), "mag"),
-    (dict(k=3, shifts=synth.shift_pattern(2)[:3]), "unsupported geometry"),
-    (dict(shifts=np.array([[0, 0], [0, .5], [.5, .5], [.5, .5]])), "unsupported geometry"),
-    (dict(shifts=np.array([[0, 0], [0, .5], [.5, .5], [.5, .25]])), "unsupported geometry"),
+    # general geometries run on one GPU; bands need the polyphase fast path
+    (dict(k=3, shifts=synth.shift_pattern(2)[:3], world=2, rank=0, nccl_id=b"\0" * 128), "row-band partitioning"),
+    (dict(shifts=np.array([[0, 0], [0, .5], [.5, .5], [.5, .5]]), world=2, rank=1, nccl_id=b"\0" * 128),
+     "row-band partitioning"),
+    (dict(k=65, shifts=np.zeros((65, 2))), "k <= 64"),
 ])
 def test_config_errors_raised_before_gpu_work(fl, kw, msg):
     c = cfg(**kw)

@@ -320,3 +320,34 @@ def test_fd_curvature_mode_agrees_with_exact(orc):
     xe, tre, _ = orc.scg(pb, y, 10, curv_mode=orc.CURV_EXACT)
     xf, trf, _ = orc.scg(pb, y, 10, curv_mode=orc.CURV_FD)
     assert np.linalg.norm(xf - xe) <= 1e-3 * np.linalg.norm(xe)
+
+
+# ----------------------------------------------------------------------------- interpolation fusion
+def test_interp_fuse_single_frame_is_bilinear(orc):
+    """k = 1, zero shift -> plain bilinear upsampling except at the frame's own sites."""
+    pb = problem(orc, lr=9, mag=2, shifts=[[0.0, 0.0]])
+    y = np.random.default_rng(30).uniform(size=(1, 9, 9))
+    out = orc.interp_fuse(pb, y)
+    np.testing.assert_allclose(out, orc.init_x0(pb, y), atol=1e-15)
+    np.testing.assert_array_equal(out[0::2, 0::2], y[0])
+
+
+def test_interp_fuse_complete_phases_is_exact_inverse(orc):
+    """K = r^2 distinct integer phases of a sliced image reassemble it exactly."""
+    for mag in (2, 3):
+        pb = problem(orc, lr=7, mag=mag, psf=synth.delta_psf())
+        x = np.random.default_rng(31).uniform(size=(pb.H, pb.W))
+        y = orc.forward(pb, x)
+        np.testing.assert_array_equal(orc.interp_fuse(pb, y), x)
+
+
+def test_interp_fuse_partial_coverage(orc):
+    """Two of four phases: their sites are exact, the others bilinear from frame 0."""
+    pb = problem(orc, lr=8, mag=2, psf=synth.delta_psf(), shifts=[[0, 0], [0.5, 0.5]])
+    x = np.random.default_rng(32).uniform(size=(pb.H, pb.W))
+    y = orc.forward(pb, x)
+    out = orc.interp_fuse(pb, y)
+    np.testing.assert_array_equal(out[0::2, 0::2], x[0::2, 0::2])
+    np.testing.assert_array_equal(out[1::2, 1::2], x[1::2, 1::2])
+    x0 = orc.init_x0(pb, y)
+    np.testing.assert_array_equal(out[0::2, 1::2], x0[0::2, 1::2])
