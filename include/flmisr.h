@@ -76,8 +76,10 @@ typedef struct {
 /*
  * flmisr_plan: validate `cfg`, derive the per-frame taps kappa_i = PSF (*) bilinear(frac(mag*shift_i))
  * and integer phases, choose the polyphase fast path (K = mag^2 distinct phases in [0,mag)^2 with one
- * common kappa), compute the row band and halo, allocate all device scratch on
- * cfg->device and (world > 1) initialise the NCCL communicator from cfg->nccl_unique_id.
+ * common kappa) or the general-geometry path (any k <= 64, missing, repeated or
+ * fractional phases, per-frame kappa_i; world == 1 only), compute the row band and halo, allocate all
+ * device scratch on cfg->device and (world > 1) initialise the NCCL communicator from
+ * cfg->nccl_unique_id.
  * Ownership: the plan copies everything it needs from cfg (shifts/psf may be freed afterwards).
  * Errors: FLMISR_ERR_CONFIG for invalid parameters or an unsupported geometry (message names the
  * violated rule, e.g. the minimum band height); FLMISR_ERR_CUDA / _NCCL for runtime failures.
@@ -161,6 +163,38 @@ flmisr_status flmisr_plan_info(flmisr_plan_t plan, int32_t* H, int32_t* W, int32
                                int32_t* fast_path);
 
 /* ------------------------------------------------------------------------------------------
+ * Streaming capture-reconstruct pipeline (fig:capture: each view is
+ * super-resolved while the next one is acquired).  A pipeline owns `depth` device input and output
+ * slots and two copy streams beside the plan's compute stream; for every submitted view it enqueues
+ *   H2D of the LR stack (upload stream) -> [uint16 -> fp32 on the device] -> the plan's whole SCG
+ *   reconstruction (compute stream) -> D2H of the HR image (download stream),
+ * so view j+1's upload and view j-1's download overlap view j's reconstruction.
+ *
+ * flmisr_pipeline_create: plan = a world-1 plan or one band of a partitioned group (every rank of
+ *   the group creates its pipeline and submits the same views in the same order); the pipeline uses
+ *   the plan's buffers exclusively (no flmisr_reconstruct* on that plan until it is destroyed).
+ *   depth >= 2 slots (views in flight).  input_u16: 0 = fp32 frames; 1 = uint16 frames, value =
+ *   u16_scale * code, converted on the device (halves the H2D bytes; 16-bit detector data).
+ *   Errors: FLMISR_ERR_SHAPE (bad arguments), FLMISR_ERR_CUDA (allocation).
+ * flmisr_pipeline_submit: lr_host = host k x lr_h x lr_w frames (fp32 or uint16); hr_host = host
+ *   H x W fp32 destination (world 1 / rank 0; may be NULL on other ranks).  Page-locked buffers are
+ *   DMA'd in place and must stay valid until the view completes; pageable buffers are staged through
+ *   per-slot pinned memory (the output is copied out when the slot is next reused or at _wait).
+ *   Returns once the view is enqueued; blocks only while the slot it reuses is still in flight.
+ * flmisr_pipeline_wait: drain every submitted view.  n_done (nullable) = views completed since
+ *   create; report (nullable; f_trace is not filled) = the most recent view's.  Returns the first
+ *   error any view hit since the last _wait (FLMISR_ERR_NUMERIC if a view's loop froze).
+ * flmisr_pipeline_destroy: drain and free (NULL accepted); the plan stays valid.  A plan drives at
+ *   most one pipeline; flmisr_destroy(plan) drains and frees it too (its handle is then invalid).
+ * ------------------------------------------------------------------------------------------ */
+typedef struct flmisr_pipeline_s* flmisr_pipeline_t;
+flmisr_status flmisr_pipeline_create(flmisr_plan_t plan, int32_t depth, int32_t input_u16, float u16_scale,
+                                     flmisr_pipeline_t* out);
+flmisr_status flmisr_pipeline_submit(flmisr_pipeline_t pipe, const void* lr_host, float* hr_host);
+flmisr_status flmisr_pipeline_wait(flmisr_pipeline_t pipe, int64_t* n_done, flmisr_report* report);
+flmisr_status flmisr_pipeline_destroy(flmisr_pipeline_t pipe);
+
+/* ------------------------------------------------------------------------------------------
  * Debug entry points (parity tests).  Each runs the SAME kernels as the SCG loop (for VALUE,
  * GRAD and CURV) or shares their device stencil code (FORWARD, ADJOINT) on the plan's stream,
  * synchronises, and returns.  All array arguments are device pointers (fp32), scalars host.
@@ -172,9 +206,9 @@ typedef enum {
     FLMISR_OP_CURV = 3,    /* in0 = x, in1 = p, lr = y   -> s[0] = p^T Hess J(x) p, s[1] = <p,p>          */
     FLMISR_OP_VALUE = 4,   /* in0 = x, lr = y            -> s[0] = D(x), s[1] = R(x)  (J = D + lambda R)  */
     FLMISR_OP_X0 = 5,      /* lr = y                     -> out = bilinear initial estimate (H x W)       */
-    FLMISR_OP_INTERP = 6   /* lr = y -> out = multi-image interpolation fusion: every LR pixel at
-                              its integer HR site (the polyphase interleave; all sites are covered on
-                              the fast path)                                                             */
+    FLMISR_OP_INTERP = 6   /* lr = y -> out = multi-image interpolation fusion: every LR pixel of an
+                              integer-phase frame at its HR site (first frame wins), the bilinear initial
+                              estimate on sites no frame covers (none on the fast path)                  */
 } flmisr_op;
 
 flmisr_status flmisr_debug_apply(flmisr_plan_t plan, int32_t op, const float* lr_stack, const float* in0,

@@ -132,6 +132,7 @@ struct flmisr_plan_s {
     cudaGraphExec_t graph_exec = nullptr;   // the captured SCG loop (world == 1)
     cudaGraphExec_t graph_exec_prof = nullptr;   // the same with per-kernel event records
     int no_graph = 0;                       // FLMISR_NO_GRAPH=1: always launch eagerly
+    flmisr_pipeline_s* pipe = nullptr;      // the pipeline driving this plan, if any
 };
 
 namespace {
@@ -520,6 +521,7 @@ flmisr_status flmisr_plan_info(flmisr_plan_t p, int32_t* H, int32_t* W, int32_t*
 
 flmisr_status flmisr_destroy(flmisr_plan_t p) {
     if (!p) return FLMISR_OK;
+    if (p->pipe) flmisr_pipeline_destroy(p->pipe);   // drains it; the pipeline cannot outlive its plan
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->comm && nccl().ok) nccl().CommDestroy(p->comm);
     if (p->halo_mem) cudaFree(p->halo_mem);
@@ -999,6 +1001,192 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
         if (op == FLMISR_OP_GRAD || op == FLMISR_OP_VALUE) { sc[0] = d[0]; sc[1] = d[1]; sc[2] = d[2]; }
         if (op == FLMISR_OP_CURV) { sc[0] = d[0] + p->cfg.lambda * d[1]; sc[1] = d[2]; sc[2] = d[3]; }
     }
+    return FLMISR_OK;
+}
+
+}  // extern "C"
+
+// ---- streaming capture-reconstruct pipeline ----
+struct flmisr_pipeline_s {
+    flmisr_plan_s* p = nullptr;
+    int depth = 0, u16 = 0;
+    float scale = 1.0f;
+    size_t nlr = 0, nhr = 0, in_bytes = 0, out_bytes = 0;
+    bool root = true;
+    cudaStream_t up = nullptr, dn = nullptr;   // copy streams; compute runs on the plan's stream
+    std::vector<void*> d_in, pin_in;
+    std::vector<float*> d_out, pin_out, user_out;
+    float* d_lr = nullptr;                     // fp32 frames converted from uint16 (compute stream)
+    std::vector<cudaEvent_t> ev_up, ev_dn;
+    ScgState* slot_state = nullptr;            // pinned, one per slot: the view's final SCG state
+    std::vector<int> busy;
+    long long submitted = 0, done = 0;
+    flmisr_status first_err = FLMISR_OK;
+    std::string err_msg;
+    ScgState last{};
+};
+
+namespace {
+
+bool host_pinned(const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// wait for slot `i`'s view (its download, hence its compute), record its status, copy staged output
+flmisr_status pipe_complete(flmisr_pipeline_s* q, int i) {
+    if (!q->busy[i]) return FLMISR_OK;
+    q->busy[i] = 0;
+    CUDA_TRY(cudaEventSynchronize(q->ev_dn[i]));
+    if (q->user_out[i]) std::memcpy(q->user_out[i], q->pin_out[i], q->out_bytes);
+    q->user_out[i] = nullptr;
+    q->last = q->slot_state[i];
+    q->done += 1;
+    if (q->last.failed_stage && q->first_err == FLMISR_OK) {
+        q->first_err = FLMISR_ERR_NUMERIC;
+        q->err_msg = "pipeline view " + std::to_string(q->done - 1) + ": non-finite consensus scalar at SCG pass " +
+                     std::to_string(q->last.failed_iter);
+    }
+    return FLMISR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+flmisr_status flmisr_pipeline_destroy(flmisr_pipeline_t q) {
+    if (!q) return FLMISR_OK;
+    if (q->p && q->p->pipe == q) q->p->pipe = nullptr;
+    for (int i = 0; i < q->depth; ++i)
+        if (q->busy[i]) cudaEventSynchronize(q->ev_dn[i]);
+    if (q->p && q->p->stream) cudaStreamSynchronize(q->p->stream);
+    for (auto v : q->d_in) if (v) cudaFree(v);
+    for (auto v : q->d_out) if (v) cudaFree(v);
+    for (auto v : q->pin_in) if (v) cudaFreeHost(v);
+    for (auto v : q->pin_out) if (v) cudaFreeHost(v);
+    for (auto e : q->ev_up) if (e) cudaEventDestroy(e);
+    for (auto e : q->ev_dn) if (e) cudaEventDestroy(e);
+    if (q->d_lr) cudaFree(q->d_lr);
+    if (q->slot_state) cudaFreeHost(q->slot_state);
+    if (q->up) cudaStreamDestroy(q->up);
+    if (q->dn) cudaStreamDestroy(q->dn);
+    delete q;
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_pipeline_create(flmisr_plan_t p, int32_t depth, int32_t input_u16, float u16_scale,
+                                     flmisr_pipeline_t* out) {
+    if (!out) return fail(FLMISR_ERR_SHAPE, "out is NULL");
+    *out = nullptr;
+    if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    if (depth < 2 || depth > 64) return fail(FLMISR_ERR_SHAPE, "pipeline depth must be in [2, 64]");
+    if (input_u16 != 0 && input_u16 != 1) return fail(FLMISR_ERR_SHAPE, "input_u16 must be 0 or 1");
+    if (input_u16 && !(u16_scale > 0.0f) ) return fail(FLMISR_ERR_SHAPE, "u16_scale must be > 0");
+    if (p->virt) return fail(FLMISR_ERR_SHAPE, "virtual band plans cannot drive a pipeline");
+    if (p->pipe) return fail(FLMISR_ERR_SHAPE, "the plan already drives a pipeline");
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    auto* q = new flmisr_pipeline_s();
+    q->p = p;
+    q->depth = depth;
+    q->u16 = input_u16;
+    q->scale = u16_scale;
+    q->nlr = (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w;
+    q->nhr = (size_t)p->H * p->W;
+    q->in_bytes = q->nlr * (input_u16 ? sizeof(uint16_t) : sizeof(float));
+    q->out_bytes = q->nhr * sizeof(float);
+    q->root = p->cfg.world == 1 || p->cfg.rank == 0;
+    q->d_in.assign(depth, nullptr); q->pin_in.assign(depth, nullptr);
+    q->d_out.assign(depth, nullptr); q->pin_out.assign(depth, nullptr); q->user_out.assign(depth, nullptr);
+    q->ev_up.assign(depth, nullptr); q->ev_dn.assign(depth, nullptr);
+    q->busy.assign(depth, 0);
+    auto bad = [&](const char* what, cudaError_t e) {
+        flmisr_pipeline_destroy(q);
+        return fail(FLMISR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&q->up, cudaStreamNonBlocking)) != cudaSuccess) return bad("upload stream", e);
+    if ((e = cudaStreamCreateWithFlags(&q->dn, cudaStreamNonBlocking)) != cudaSuccess) return bad("download stream", e);
+    for (int i = 0; i < depth; ++i) {
+        // input slots padded to 16 B (the uint16 conversion reads 8 codes per thread)
+        if ((e = cudaMalloc(&q->d_in[i], (q->in_bytes + 15) / 16 * 16)) != cudaSuccess) return bad("cudaMalloc input slot", e);
+        if ((e = cudaMalloc(&q->d_out[i], q->out_bytes)) != cudaSuccess) return bad("cudaMalloc output slot", e);
+        if ((e = cudaEventCreateWithFlags(&q->ev_up[i], cudaEventDisableTiming)) != cudaSuccess) return bad("event", e);
+        if ((e = cudaEventCreateWithFlags(&q->ev_dn[i], cudaEventDisableTiming)) != cudaSuccess) return bad("event", e);
+    }
+    if (input_u16 && (e = cudaMalloc(&q->d_lr, q->nlr * sizeof(float))) != cudaSuccess) return bad("cudaMalloc frames", e);
+    if ((e = cudaMallocHost(&q->slot_state, (size_t)depth * sizeof(ScgState))) != cudaSuccess) return bad("pinned state", e);
+    p->pipe = q;
+    *out = q;
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_pipeline_submit(flmisr_pipeline_t q, const void* lr_host, float* hr_host) {
+    if (!q) return fail(FLMISR_ERR_SHAPE, "pipeline is NULL");
+    if (!lr_host) return fail(FLMISR_ERR_SHAPE, "lr_host is NULL");
+    if (q->root && !hr_host) return fail(FLMISR_ERR_SHAPE, "hr_host is NULL (world 1 / rank 0)");
+    flmisr_plan_s* p = q->p;
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    const int i = (int)(q->submitted % q->depth);
+    flmisr_status st = pipe_complete(q, i);   // the slot's previous view must be out of the device buffers
+    if (st != FLMISR_OK) return st;
+    cudaStream_t cs = p->stream;
+    // 1. upload (pageable sources are staged through the slot's pinned buffer)
+    const void* src = lr_host;
+    if (!host_pinned(lr_host)) {
+        if (!q->pin_in[i]) CUDA_TRY(cudaMallocHost(&q->pin_in[i], q->in_bytes));
+        std::memcpy(q->pin_in[i], lr_host, q->in_bytes);
+        src = q->pin_in[i];
+    }
+    CUDA_TRY(cudaMemcpyAsync(q->d_in[i], src, q->in_bytes, cudaMemcpyHostToDevice, q->up));
+    CUDA_TRY(cudaEventRecord(q->ev_up[i], q->up));
+    // 2. reconstruct on the compute stream once the frames are in
+    CUDA_TRY(cudaStreamWaitEvent(cs, q->ev_up[i], 0));
+    const float* lr_dev = (const float*)q->d_in[i];
+    if (q->u16) {
+        CUDA_TRY(launch_u16_to_f32((const uint16_t*)q->d_in[i], q->d_lr, (long long)q->nlr, q->scale, cs));
+        lr_dev = q->d_lr;
+    }
+    st = flmisr_reconstruct_async(p, lr_dev, nullptr, q->d_out[i], cs);
+    p->pending = 0;   // the pipeline tracks completion per slot
+    if (st != FLMISR_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(&q->slot_state[i], p->st, sizeof(ScgState), cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(cudaEventRecord(p->done_ev, cs));
+    // 3. download after the reconstruction (ev_dn marks the whole view complete on every rank)
+    CUDA_TRY(cudaStreamWaitEvent(q->dn, p->done_ev, 0));
+    if (q->root && hr_host) {
+        float* dst = hr_host;
+        if (!host_pinned(hr_host)) {
+            if (!q->pin_out[i]) CUDA_TRY(cudaMallocHost(&q->pin_out[i], q->out_bytes));
+            dst = q->pin_out[i];
+            q->user_out[i] = hr_host;
+        }
+        CUDA_TRY(cudaMemcpyAsync(dst, q->d_out[i], q->out_bytes, cudaMemcpyDeviceToHost, q->dn));
+    }
+    CUDA_TRY(cudaEventRecord(q->ev_dn[i], q->dn));
+    q->busy[i] = 1;
+    q->submitted += 1;
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_pipeline_wait(flmisr_pipeline_t q, int64_t* n_done, flmisr_report* rep) {
+    if (!q) return fail(FLMISR_ERR_SHAPE, "pipeline is NULL");
+    CUDA_TRY(cudaSetDevice(q->p->cfg.device));
+    for (long long v = std::max(0LL, q->submitted - q->depth); v < q->submitted; ++v) {
+        flmisr_status st = pipe_complete(q, (int)(v % q->depth));
+        if (st != FLMISR_OK) return st;
+    }
+    if (n_done) *n_done = q->done;
+    if (rep) {
+        rep->iters_run = q->last.k;
+        rep->accepted = q->last.accepted;
+        rep->converged_at = q->last.converged_at;
+        rep->failed_stage = q->last.failed_stage;
+        rep->failed_iter = q->last.failed_iter;
+    }
+    const flmisr_status e = q->first_err;
+    q->first_err = FLMISR_OK;
+    if (e != FLMISR_OK) return fail(e, q->err_msg);
     return FLMISR_OK;
 }
 

@@ -140,6 +140,8 @@ cudaError_t launch_hr_copy(const float* src, int src_pitch, int src_perm, float*
 cudaError_t launch_ingest(const IngestParams& ip, const float* lr, float* Y, cudaStream_t s);
 cudaError_t launch_egest(const IngestParams& ip, const float* Yhr, float* lr, cudaStream_t s);   // debug
 cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s);
+// uint16 detector frames -> fp32 (pipeline input; in and out 16-B aligned)
+cudaError_t launch_u16_to_f32(const uint16_t* in, float* out, long long n, float scale, cudaStream_t s);
 cudaError_t launch_finalize(const StencilParams& sp, const Buffers& b, float* out, int out_pitch, int row_lo,
                             int row_hi, cudaStream_t s);
 cudaError_t launch_forward_debug(int kr, const StencilParams& sp, const float* x, float* zhr, cudaStream_t s);

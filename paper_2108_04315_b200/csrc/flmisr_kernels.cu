@@ -591,4 +591,29 @@ cudaError_t launch_adjoint_debug(int kr, const StencilParams& sp, const float* w
     return cudaGetLastError();
 }
 
+// uint16 detector codes -> fp32 (value = scale * code): 8 codes (16 B) per thread, two 16-B stores
+__global__ void k_u16_to_f32(const uint16_t* __restrict__ in, float* __restrict__ out, long long n, float scale) {
+    const long long i8 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (i8 + 8 <= n) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in + i8));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            o[2 * j] = scale * (float)(w[j] & 0xffffu);
+            o[2 * j + 1] = scale * (float)(w[j] >> 16);
+        }
+        reinterpret_cast<float4*>(out + i8)[0] = make_float4(o[0], o[1], o[2], o[3]);
+        reinterpret_cast<float4*>(out + i8)[1] = make_float4(o[4], o[5], o[6], o[7]);
+    } else {
+        for (long long i = i8; i < n; ++i) out[i] = scale * (float)in[i];
+    }
+}
+cudaError_t launch_u16_to_f32(const uint16_t* in, float* out, long long n, float scale, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const long long nt = (n + 7) / 8;
+    k_u16_to_f32<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(in, out, n, scale);
+    return cudaGetLastError();
+}
+
 }  // namespace flmisr

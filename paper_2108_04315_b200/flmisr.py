@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -49,7 +50,8 @@ class Report(C.Structure):
 EXPORTS = ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_async", "flmisr_finish",
            "flmisr_profile", "flmisr_reconstruct_host", "flmisr_destroy", "flmisr_last_error",
            "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply", "flmisr_band",
-           "flmisr_plan_virtual", "flmisr_reconstruct_virtual")
+           "flmisr_plan_virtual", "flmisr_reconstruct_virtual", "flmisr_pipeline_create",
+           "flmisr_pipeline_submit", "flmisr_pipeline_wait", "flmisr_pipeline_destroy")
 
 
 def _load():
@@ -72,6 +74,10 @@ def _load():
     lib.flmisr_band.argtypes = [C.c_int32] * 4 + [C.POINTER(C.c_int32)] * 2
     lib.flmisr_plan_virtual.argtypes = [C.POINTER(Config), C.POINTER(vp)]
     lib.flmisr_reconstruct_virtual.argtypes = [C.POINTER(vp), C.c_int32, vp, vp, vp, C.POINTER(Report)]
+    lib.flmisr_pipeline_create.argtypes = [vp, C.c_int32, C.c_int32, C.c_float, C.POINTER(vp)]
+    lib.flmisr_pipeline_submit.argtypes = [vp, vp, vp]
+    lib.flmisr_pipeline_wait.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(Report)]
+    lib.flmisr_pipeline_destroy.argtypes = [vp]
     for f in EXPORTS:
         if f == "flmisr_last_error":
             continue
@@ -152,6 +158,7 @@ class Plan:
                      rank, world, C.cast(self._id, C.c_void_p) if self._id is not None else None, device)
         self.k, self.lr_h, self.lr_w, self.mag, self.n_iter = k, lr_h, lr_w, mag, n_iter
         self.rank, self.world, self.device = rank, world, device
+        self._pipes = weakref.WeakSet()   # pipelines driving this plan (destroyed first)
         self._h = C.c_void_p()
         _check((_lib.flmisr_plan_virtual if virtual else _lib.flmisr_plan)(C.byref(cfg), C.byref(self._h)))
         vals = [C.c_int32() for _ in range(5)]
@@ -159,6 +166,8 @@ class Plan:
         self.H, self.W, self.row_lo, self.row_hi, self.fast_path = [v.value for v in vals]
 
     def destroy(self):
+        for pipe in list(getattr(self, "_pipes", ())):
+            pipe.destroy()
         if self._h:
             _lib.flmisr_destroy(self._h)
             self._h = C.c_void_p()
@@ -242,6 +251,47 @@ def reconstruct_virtual(plans, lr_stack, x0=None, out=None):
     torch.cuda.current_stream(lr_stack.device).synchronize()
     _check(_lib.flmisr_reconstruct_virtual(arr, len(plans), _ptr(lr_stack), _ptr(x0), _ptr(out), C.byref(rep)))
     return out, p0._report(rep, trace)
+
+
+class Pipeline:
+    """flmisr_pipeline_*: streamed capture-reconstruct.  submit() enqueues
+    H2D -> SCG -> D2H of one view and returns; views overlap up to `depth` in flight.  Host buffers
+    (numpy arrays or pinned torch CPU tensors) are referenced until their view completes."""
+
+    def __init__(self, plan: Plan, depth: int = 2, input_u16: bool = False, u16_scale: float = 1.0 / 65535.0):
+        self.plan = plan
+        self.depth = depth
+        self._h = C.c_void_p()
+        _check(_lib.flmisr_pipeline_create(plan._h, depth, int(input_u16), u16_scale, C.byref(self._h)))
+        plan._pipes.add(self)
+        self._keep = [None] * depth
+        self._n = 0
+
+    def submit(self, lr_host, hr_host=None):
+        slot = self._n % self.depth
+        _check(_lib.flmisr_pipeline_submit(self._h, _ptr(lr_host), _ptr(hr_host)))
+        self._keep[slot] = (lr_host, hr_host)
+        self._n += 1
+
+    def wait(self) -> dict:
+        n = C.c_int64()
+        rep = Report(0, 0, 0, 0, 0, None)
+        _check(_lib.flmisr_pipeline_wait(self._h, C.byref(n), C.byref(rep)))
+        self._keep = [None] * self.depth
+        return dict(done=n.value, iters_run=rep.iters_run, accepted=rep.accepted,
+                    converged_at=rep.converged_at, failed_stage=rep.failed_stage)
+
+    def destroy(self):
+        if self._h:
+            if self.plan._h:   # flmisr_destroy(plan) already freed an attached pipeline
+                _lib.flmisr_pipeline_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
 
 
 # ---- functional names mirroring the C ABI ----
