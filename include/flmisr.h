@@ -61,6 +61,13 @@ typedef struct {
     int32_t rank, world; /* row band `rank` of `world` partitions; world = 1: no NCCL    */
     const void* nccl_unique_id; /* host, 128-byte ncclUniqueId (same on all ranks) or NULL if world == 1 */
     int32_t device;      /* CUDA device ordinal for this rank                                    */
+    /* Variants (0 = the readings of DESIGN.md section 3):                      */
+    int32_t btv_offsets; /* 0: the paper's quadrant dx, dy in [0, w-1] (reading 6);
+                            1: Farsiu's set dy = m in [0, w-1], dx = l in [-(w-1), w-1], l + m >= 0,
+                            gamma = alpha^(|l|+m) (the [BTV] citation); general path, world 1 */
+    int32_t scg_rules;   /* bit mask: 1 = PR+ restart (beta <- max(beta, 0)); 2 = Netlab scale
+                            rules (delta = curv + lam |p|^2 each pass; lam x4 at Delta < 0.25, x1/2 at
+                            Delta > 0.75, bounded to [1e-15, 1e100]); 0 = Moller literal (reading 11) */
 } flmisr_config;
 
 typedef struct {

@@ -32,11 +32,33 @@ typedef struct {
     double lambda;           /* regularisation weight (Eq. objective; 0.05 at P:271) */
     double btv_alpha;        /* gamma(d) = alpha^(dx+dy) (Eq. prior)                  */
     int32_t btv_window;      /* w: dx, dy in [0, w-1] (reading 6/7)                  */
+    int32_t btv_offsets;     /* 0: the paper's quadrant dx, dy in [0, w-1] (reading 6);
+                                1: Farsiu's set dy = m in [0, w-1], dx = l in [-(w-1), w-1], l + m >= 0
+                                (the [BTV] citation), gamma = alpha^(|l|+m) */
 } orc_problem;
 
 static int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 static int H_of(const orc_problem* pb) { return pb->mag * pb->lr_h; }
 static int W_of(const orc_problem* pb) { return pb->mag * pb->lr_w; }
+
+/* The BTV offset set Q of Eq. prior as an explicit list, (0,0) excluded:
+ * quadrant (reading 6): d = (dy, dx), dy, dx in [0, w-1], gamma(d) = alpha^(dx+dy);
+ * Farsiu (NEXT-4): d = (m, l), m in [0, w-1], l in [-(w-1), w-1], l + m >= 0, gamma = alpha^(|l|+m).
+ * Returns the number of offsets (<= 3w^2). */
+static int btv_offset_list(const orc_problem* pb, int* dys, int* dxs, double* gams)
+{
+    int w = pb->btv_window, n = 0;
+    for (int dy = 0; dy < w; ++dy)
+        for (int dx = pb->btv_offsets ? -(w - 1) : 0; dx < w; ++dx) {
+            if (dy == 0 && dx == 0) continue;
+            if (pb->btv_offsets && dx + dy < 0) continue;
+            dys[n] = dy; dxs[n] = dx;
+            gams[n] = pow(pb->btv_alpha, (dx < 0 ? -dx : dx) + dy);
+            ++n;
+        }
+    return n;
+}
+#define BTV_MAXOFF 64
 
 /* ---------------------------------------------------------------------------------
  * Per-frame operator A_i = D B M_i  (Eq. sisr; reading 1, 3, 4, 19).
@@ -171,20 +193,21 @@ static double data_value_rows(const orc_problem* pb, const double* x, const doub
  * (Eq. prior; valid pairs only, reading 5; quadrant offsets, reading 6). */
 static double btv_value_rows(const orc_problem* pb, const double* x, int lo, int hi)
 {
-    int H = H_of(pb), W = W_of(pb), w = pb->btv_window;
+    int H = H_of(pb), W = W_of(pb);
+    int dys[BTV_MAXOFF], dxs[BTV_MAXOFF];
+    double gams[BTV_MAXOFF];
+    int no = btv_offset_list(pb, dys, dxs, gams);
     double acc = 0.0;
-    for (int dy = 0; dy < w; ++dy)
-        for (int dx = 0; dx < w; ++dx) {
-            if (dy == 0 && dx == 0) continue;
-            double g = pow(pb->btv_alpha, dx + dy);
-            double s = 0.0;
-            for (int u = lo; u < hi; ++u)
-                for (int v = 0; v < W; ++v) {
-                    if (u + dy >= H || v + dx >= W) continue;
-                    s += psi(pb->eps, x[(size_t)u * W + v] - x[(size_t)(u + dy) * W + v + dx]);
-                }
-            acc += g * s;
-        }
+    for (int o = 0; o < no; ++o) {
+        int dy = dys[o], dx = dxs[o];
+        double s = 0.0;
+        for (int u = lo; u < hi; ++u)
+            for (int v = 0; v < W; ++v) {
+                if (u + dy >= H || v + dx < 0 || v + dx >= W) continue;
+                s += psi(pb->eps, x[(size_t)u * W + v] - x[(size_t)(u + dy) * W + v + dx]);
+            }
+        acc += gams[o] * s;
+    }
     return acc;
 }
 
@@ -206,7 +229,10 @@ double orc_objective(const orc_problem* pb, const double* x, const double* y)
  * A_i^T by the scatter of orc_adjoint; grad R by differentiating each pair term). */
 int orc_grad(const orc_problem* pb, const double* x, const double* y, double* g)
 {
-    int H = H_of(pb), W = W_of(pb), w = pb->btv_window;
+    int H = H_of(pb), W = W_of(pb);
+    int dys[BTV_MAXOFF], dxs[BTV_MAXOFF];
+    double gams[BTV_MAXOFF];
+    int no = btv_offset_list(pb, dys, dxs, gams);
     size_t M = (size_t)pb->k * pb->lr_h * pb->lr_w;
     double* res = (double*)malloc(sizeof(double) * M);
     if (!res) return -1;
@@ -214,18 +240,18 @@ int orc_grad(const orc_problem* pb, const double* x, const double* y, double* g)
     for (size_t m = 0; m < M; ++m) res[m] = drho(pb->p_norm, pb->eps, res[m] - y[m]);
     orc_adjoint(pb, res, g);
     free(res);
-    for (int dy = 0; dy < w; ++dy)
-        for (int dx = 0; dx < w; ++dx) {
-            if (dy == 0 && dx == 0) continue;
-            double gam = pb->lambda * pow(pb->btv_alpha, dx + dy);
-            for (int u = 0; u + dy < H; ++u)
-                for (int v = 0; v + dx < W; ++v) {
-                    size_t i0 = (size_t)u * W + v, i1 = (size_t)(u + dy) * W + v + dx;
-                    double d = gam * dpsi(pb->eps, x[i0] - x[i1]);
-                    g[i0] += d;
-                    g[i1] -= d;
-                }
-        }
+    for (int o = 0; o < no; ++o) {
+        int dy = dys[o], dx = dxs[o];
+        double gam = pb->lambda * gams[o];
+        for (int u = 0; u + dy < H; ++u)
+            for (int v = 0; v < W; ++v) {
+                if (v + dx < 0 || v + dx >= W) continue;
+                size_t i0 = (size_t)u * W + v, i1 = (size_t)(u + dy) * W + v + dx;
+                double d = gam * dpsi(pb->eps, x[i0] - x[i1]);
+                g[i0] += d;
+                g[i1] -= d;
+            }
+    }
     return 0;
 }
 
@@ -234,7 +260,10 @@ int orc_grad(const orc_problem* pb, const double* x, const double* y, double* g)
  *   sum_i sum rho''(A_i x - y_i) (A_i p)^2 + lambda sum_d gamma_d sum_valid psi''(x_u-x_{u+d}) (p_u-p_{u+d})^2. */
 static double curv_rows(const orc_problem* pb, const double* x, const double* y, const double* p, int lo, int hi)
 {
-    int H = H_of(pb), W = W_of(pb), w = pb->btv_window;
+    int H = H_of(pb), W = W_of(pb);
+    int dys[BTV_MAXOFF], dxs[BTV_MAXOFF];
+    double gams[BTV_MAXOFF];
+    int no = btv_offset_list(pb, dys, dxs, gams);
     orc_taps t;
     double acc = 0.0;
     for (int i = 0; i < pb->k; ++i) {
@@ -250,20 +279,18 @@ static double curv_rows(const orc_problem* pb, const double* x, const double* y,
         }
     }
     double reg = 0.0;
-    for (int dy = 0; dy < w; ++dy)
-        for (int dx = 0; dx < w; ++dx) {
-            if (dy == 0 && dx == 0) continue;
-            double gam = pow(pb->btv_alpha, dx + dy);
-            double s = 0.0;
-            for (int u = lo; u < hi; ++u)
-                for (int v = 0; v < W; ++v) {
-                    if (u + dy >= H || v + dx >= W) continue;
-                    size_t i0 = (size_t)u * W + v, i1 = (size_t)(u + dy) * W + v + dx;
-                    double dp = p[i0] - p[i1];
-                    s += d2psi(pb->eps, x[i0] - x[i1]) * dp * dp;
-                }
-            reg += gam * s;
-        }
+    for (int o = 0; o < no; ++o) {
+        int dy = dys[o], dx = dxs[o];
+        double s = 0.0;
+        for (int u = lo; u < hi; ++u)
+            for (int v = 0; v < W; ++v) {
+                if (u + dy >= H || v + dx < 0 || v + dx >= W) continue;
+                size_t i0 = (size_t)u * W + v, i1 = (size_t)(u + dy) * W + v + dx;
+                double dp = p[i0] - p[i1];
+                s += d2psi(pb->eps, x[i0] - x[i1]) * dp * dp;
+            }
+        reg += gams[o] * s;
+    }
     return acc + pb->lambda * reg;
 }
 
@@ -352,21 +379,23 @@ static int band_grad(const orc_problem* pb, const double* xfull, const double* y
             }
         }
     }
-    int w = pb->btv_window;
-    for (int dy = 0; dy < w; ++dy)
-        for (int dx = 0; dx < w; ++dx) {
-            if (dy == 0 && dx == 0) continue;
-            double gam = pb->lambda * pow(pb->btv_alpha, dx + dy);
-            for (int u = lo - dy; u < hi; ++u) {
-                if (u < 0 || u + dy >= H) continue;
-                for (int v = 0; v + dx < W; ++v) {
-                    size_t i0 = (size_t)u * W + v, i1 = (size_t)(u + dy) * W + v + dx;
-                    double d = gam * dpsi(pb->eps, scratch[i0] - scratch[i1]);
-                    g[i0] += d;
-                    g[i1] -= d;
-                }
+    int dys[BTV_MAXOFF], dxs[BTV_MAXOFF];
+    double gams[BTV_MAXOFF];
+    int no = btv_offset_list(pb, dys, dxs, gams);
+    for (int o = 0; o < no; ++o) {
+        int dy = dys[o], dx = dxs[o];
+        double gam = pb->lambda * gams[o];
+        for (int u = lo - dy; u < hi; ++u) {
+            if (u < 0 || u + dy >= H) continue;
+            for (int v = 0; v < W; ++v) {
+                if (v + dx < 0 || v + dx >= W) continue;
+                size_t i0 = (size_t)u * W + v, i1 = (size_t)(u + dy) * W + v + dx;
+                double d = gam * dpsi(pb->eps, scratch[i0] - scratch[i1]);
+                g[i0] += d;
+                g[i1] -= d;
             }
         }
+    }
     for (int u = lo; u < hi; ++u)
         memcpy(gfull_out + (size_t)u * W, g + (size_t)u * W, sizeof(double) * W);
     free(g);
@@ -455,12 +484,19 @@ static double curv_consensus(const orc_problem* pb, const double* x, const doubl
  *     if <r,r> == 0: break
  * trace (nullable): (n_iter+1) rows of 6 doubles (k, f, <r,r>, alpha, lam, accepted);
  * row 0 is the initial state (alpha = 0, accepted = 1).
+ * rules (SURVEY 8(f) NEXT-4 variants, bit mask; 0 = Moller literal as above):
+ *   1  PR+ restart: beta <- max(beta, 0), i.e. p <- r on non-positive beta
+ *   2  Netlab scale rules (Nabney's scg.m): every pass delta <- curv + lam pp with curv the last
+ *      CURV(x,p); if delta <= 0: delta <- lam pp, lam <- lam - curv/pp (no lamb); after the
+ *      comparison: Delta < 0.25 -> lam <- min(4 lam, 1e100); Delta > 0.75 -> lam <- max(lam/2, 1e-15)
  * x0 == NULL -> orc_init_x0 on frame 0.  g >= 1 bands, eta halo rows (band simulation above).
  * Returns 0, or -1 on allocation failure, -2 when a consensus scalar is non-finite.
  */
 int orc_scg(const orc_problem* pb, const double* y, const double* x0, int n_iter, int curv_mode,
-            double sigma0, double lambda0, int g, int eta, double* x_out, double* trace, orc_stats* st)
+            double sigma0, double lambda0, int g, int eta, double* x_out, double* trace, orc_stats* st, int rules)
 {
+    const int pr_plus = rules & 1, netlab = rules & 2;
+    double curv = 0.0;
     int H = H_of(pb), W = W_of(pb);
     size_t N = (size_t)H * W;
     double *x = x_out, *r = malloc(sizeof(double) * N), *p = malloc(sizeof(double) * N);
@@ -501,12 +537,21 @@ int orc_scg(const orc_problem* pb, const double* y, const double* x0, int n_iter
             } else {
                 delta = curv_consensus(pb, x, y, p, g);
             }
+            curv = delta;
         }
-        delta = delta + (lam - lamb) * pp;
-        if (delta <= 0.0) {
-            lamb = 2.0 * (lam - delta / pp);
-            delta = -delta + lam * pp;
-            lam = lamb;
+        if (netlab) {
+            delta = curv + lam * pp;
+            if (delta <= 0.0) {
+                delta = lam * pp;
+                lam = lam - curv / pp;
+            }
+        } else {
+            delta = delta + (lam - lamb) * pp;
+            if (delta <= 0.0) {
+                lamb = 2.0 * (lam - delta / pp);
+                delta = -delta + lam * pp;
+                lam = lamb;
+            }
         }
         double mu = dot_consensus(pb, p, r, g);
         double alpha = mu / delta;
@@ -531,15 +576,21 @@ int orc_scg(const orc_problem* pb, const double* y, const double* x0, int n_iter
                 memcpy(p, r, sizeof(double) * N);
             } else {
                 double beta = (rr - dot_consensus(pb, r, rold, g)) / mu;
+                if (pr_plus && beta < 0.0) beta = 0.0;
                 for (size_t n = 0; n < N; ++n) p[n] = r[n] + beta * p[n];
             }
-            if (Delta >= 0.75) lam = lam / 4.0;
+            if (!netlab && Delta >= 0.75) lam = lam / 4.0;
             if (st) st->accepted++;
         } else {
             lamb = lam;
             success = 0;
         }
-        if (Delta < 0.25) lam = lam + delta * (1.0 - Delta) / pp;
+        if (netlab) {
+            if (Delta < 0.25) lam = fmin(4.0 * lam, 1e100);
+            if (Delta > 0.75) lam = fmax(0.5 * lam, 1e-15);
+        } else if (Delta < 0.25) {
+            lam = lam + delta * (1.0 - Delta) / pp;
+        }
         k = k + 1;
         if (st) st->iters_run = k;
         if (trace) {

@@ -35,6 +35,7 @@ class _Problem(C.Structure):
         ("psf", C.POINTER(C.c_double)), ("psf_h", C.c_int32), ("psf_w", C.c_int32),
         ("mag", C.c_int32), ("p_norm", C.c_int32), ("eps", C.c_double),
         ("lam", C.c_double), ("btv_alpha", C.c_double), ("btv_window", C.c_int32),
+        ("btv_offsets", C.c_int32),
     ]
 
 
@@ -63,7 +64,7 @@ def lib():
         _lib.orc_init_x0.argtypes = [pp, dp, dp]
         _lib.orc_interp_fuse.argtypes = [pp, dp, dp]
         _lib.orc_scg.argtypes = [pp, dp, dp, C.c_int, C.c_int, C.c_double, C.c_double,
-                                 C.c_int, C.c_int, dp, dp, C.POINTER(_Stats)]
+                                 C.c_int, C.c_int, dp, dp, C.POINTER(_Stats), C.c_int]
         _lib.orc_value_rows.argtypes = [pp, dp, dp, C.c_int, C.c_int]
         _lib.orc_value_rows.restype = C.c_double
         _lib.orc_band_bounds.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int,
@@ -94,6 +95,7 @@ class Problem:
     lam: float = 0.05
     btv_alpha: float = 0.4
     btv_window: int = 3
+    btv_offsets: int = 0          # 0 quadrant, 1 Farsiu (NEXT-4)
     _keep: list = field(default_factory=list, repr=False)
 
     @property
@@ -109,7 +111,8 @@ class Problem:
         ps = _f64(self.psf)
         self._keep = [sh, ps]
         return _Problem(self.k, self.lr_h, self.lr_w, _dp(sh), _dp(ps), ps.shape[0], ps.shape[1],
-                        self.mag, self.p_norm, self.eps, self.lam, self.btv_alpha, self.btv_window)
+                        self.mag, self.p_norm, self.eps, self.lam, self.btv_alpha, self.btv_window,
+                        self.btv_offsets)
 
 
 def forward(pb: Problem, x) -> np.ndarray:
@@ -199,10 +202,14 @@ def band_bounds(H: int, g: int, mag: int, h: int):
 CURV_EXACT, CURV_FD = 0, 1
 
 
+RULE_PR_PLUS, RULE_NETLAB = 1, 2
+
+
 def scg(pb: Problem, y, n_iter: int, x0=None, curv_mode: int = CURV_EXACT, sigma0: float = 1e-4,
-        lambda0: float = 1e-6, g: int = 1, eta: int = 2):
+        lambda0: float = 1e-6, g: int = 1, eta: int = 2, rules: int = 0):
     """Moller SCG reconstruction (Alg. 1).  Returns (x, trace, stats) where trace is an
-    (n_iter+1) x 6 array of (k, f, <r,r>, alpha, lambda_scg, accepted) rows."""
+    (n_iter+1) x 6 array of (k, f, <r,r>, alpha, lambda_scg, accepted) rows.
+    rules: NEXT-4 variants (bit mask RULE_PR_PLUS | RULE_NETLAB; 0 = Moller literal)."""
     y = _f64(y).reshape(pb.k, pb.lr_h, pb.lr_w)
     x = np.zeros((pb.H, pb.W))
     tr = np.zeros((n_iter + 1, 6))
@@ -213,7 +220,7 @@ def scg(pb: Problem, y, n_iter: int, x0=None, curv_mode: int = CURV_EXACT, sigma
         x0p = _dp(x0a)
     c = pb.c()
     rc = lib().orc_scg(C.byref(c), _dp(y), x0p, n_iter, curv_mode, sigma0, lambda0, g, eta,
-                       _dp(x), _dp(tr), C.byref(st))
+                       _dp(x), _dp(tr), C.byref(st), rules)
     if rc == -1:
         raise MemoryError("oracle allocation failed")
     stats = dict(iters_run=st.iters_run, accepted=st.accepted, converged_at=st.converged_at,

@@ -187,6 +187,11 @@ flmisr_status validate(const flmisr_config* c, bool virt) {
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(FLMISR_ERR_CONFIG, "need 0 <= rank < world");
     if (c->world > 1 && !virt && !c->nccl_unique_id)
         return fail(FLMISR_ERR_CONFIG, "world > 1 needs nccl_unique_id");
+    if (c->btv_offsets != 0 && c->btv_offsets != 1)
+        return fail(FLMISR_ERR_CONFIG, "btv_offsets must be 0 (quadrant, P:136) or 1 (Farsiu)");
+    if (c->scg_rules < 0 || c->scg_rules > 3) return fail(FLMISR_ERR_CONFIG, "scg_rules must be in [0, 3]");
+    if (c->btv_offsets == 1 && c->world > 1)
+        return fail(FLMISR_ERR_CONFIG, "Farsiu BTV offsets (btv_offsets = 1) run on the general path: world must be 1");
     return FLMISR_OK;
 }
 
@@ -224,7 +229,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         if (frame_of_phase[ph] >= 0) fast = false;
         else frame_of_phase[ph] = i;
     }
-    if (std::getenv("FLMISR_FORCE_GENERAL")) fast = false;
+    if (std::getenv("FLMISR_FORCE_GENERAL") || c.btv_offsets == 1) fast = false;
     if (!fast && c.world > 1)
         return fail(FLMISR_ERR_CONFIG,
                     "row-band partitioning (world > 1) needs the polyphase fast path (K = mag^2 frames with distinct "
@@ -340,6 +345,10 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             const int rows = p->row_hi - p->row_lo;
             int S = 16;
             while (S < rows && (long long)sp.nstrips * ((rows + S - 1) / S) > cap) S += 3;
+            if (const char* ev = std::getenv("FLMISR_SEG_ROWS")) {   // tuning override (S = 1 mod 3)
+                const int v = std::atoi(ev);
+                if (v >= 4) S = v + ((1 - v % 3) + 3) % 3;
+            }
             if (S > rows) S = rows + ((1 - rows % 3) + 3) % 3;   // smallest >= rows with S = 1 mod 3
             sp.seg_rows = S;
             sp.nsegs = (rows + S - 1) / S;
@@ -442,6 +451,15 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             gp.fy_hi = std::max(gp.fy_hi, mag * (c.lr_h - 1) + syi + R + 1);
             gp.fx_hi = std::max(gp.fx_hi, mag * (c.lr_w - 1) + sxi + R + 1);
         }
+        gp.noff = 0;   // BTV offset list: quadrant or Farsiu's set (NEXT-4)
+        for (int dy = 0; dy < c.btv_window; ++dy)
+            for (int dx = c.btv_offsets ? -(c.btv_window - 1) : 0; dx < c.btv_window; ++dx) {
+                if ((dy == 0 && dx == 0) || (c.btv_offsets && dx + dy < 0)) continue;
+                gp.offy[gp.noff] = dy;
+                gp.offx[gp.noff] = dx;
+                gp.ogam[gp.noff] = (float)std::pow(c.btv_alpha, std::abs(dx) + dy);
+                ++gp.noff;
+            }
         const size_t gbytes = ntap * sizeof(float) + 2 * (size_t)nlr_px * sizeof(float);
         e = cudaMalloc(&p->gmem, gbytes);
         if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc general-path buffers"));
@@ -567,7 +585,8 @@ flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float
     }
     CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
     CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
-    CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
+    CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W,
+                               p->cfg.scg_rules, s));
     return FLMISR_OK;
 }
 
@@ -926,7 +945,8 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
     ip0.perm = 0;
     StencilParams sp0 = p->sp;
     sp0.perm = 0;
-    CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W, s));
+    CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W,
+                               p->cfg.scg_rules, s));
     const bool gen = !p->fast;
     const size_t lr_bytes = (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w * sizeof(float);
     // the LR stack in the layout the data-term kernels read (polyphase Y, or the general path's copy)

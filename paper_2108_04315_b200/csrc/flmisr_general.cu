@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(GT) k_gen_residual(StencilParams sp, GenParams
     block_partials(acc, gp.part_a, gridDim.x, blockIdx.x);
 }
 
-template <int PN, int BW>
+template <int PN>
 __global__ void __launch_bounds__(GT) k_gen_grad(StencilParams sp, GenParams gp, Buffers b, int phase) {
     ScgState* st = b.st;
     if (phase != PH_DEBUG && st->done) return;
@@ -143,21 +143,18 @@ __global__ void __launch_bounds__(GT) k_gen_grad(StencilParams sp, GenParams gp,
         float g = adj_gather(sp, gp, gp.w, vy, vx);
         float gb = 0.0f;
         const float xv = xval(sp, X, P, alpha, vy, vx);
-#pragma unroll
-        for (int dy = 0; dy < BW; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < BW; ++dx) {
-                if (dy == 0 && dx == 0) continue;
-                const float gm = sp.gam[dy * MAXBW + dx];
-                if (vy + dy < sp.H && vx + dx < sp.W) {
-                    float v, d1;
-                    charb_val_d1(xv - xval(sp, X, P, alpha, vy + dy, vx + dx), sp.eps, sp.eps2, v, d1);
-                    acc[1] = fmaf(gm, v, acc[1]);
-                    gb = fmaf(gm, d1, gb);
-                }
-                if (vy - dy >= 0 && vx - dx >= 0)
-                    gb = fmaf(-gm, charb_d1(xval(sp, X, P, alpha, vy - dy, vx - dx) - xv, sp.eps2), gb);
+        for (int o = 0; o < gp.noff; ++o) {   // BTV offset list (quadrant or Farsiu), valid pairs only
+            const int dy = gp.offy[o], dx = gp.offx[o];
+            const float gm = gp.ogam[o];
+            if (vy + dy < sp.H && vx + dx >= 0 && vx + dx < sp.W) {      // pair (v, v + d)
+                float v, d1;
+                charb_val_d1(xv - xval(sp, X, P, alpha, vy + dy, vx + dx), sp.eps, sp.eps2, v, d1);
+                acc[1] = fmaf(gm, v, acc[1]);
+                gb = fmaf(gm, d1, gb);
             }
+            if (vy - dy >= 0 && vx - dx >= 0 && vx - dx < sp.W)          // pair (v - d, v)
+                gb = fmaf(-gm, charb_d1(xval(sp, X, P, alpha, vy - dy, vx - dx) - xv, sp.eps2), gb);
+        }
         const float rn = -fmaf(sp.lam, gb, g);
         const size_t o = (size_t)(vy - sp.store_lo) * sp.pitch + vx;
         Rn[o] = rn;
@@ -173,7 +170,7 @@ __global__ void __launch_bounds__(GT) k_gen_grad(StencilParams sp, GenParams gp,
 }
 
 // ---- update + curvature -------------------------------------------------------------------------
-template <int PN, int BW>
+template <int PN>
 __global__ void __launch_bounds__(GT) k_gen_update(StencilParams sp, GenParams gp, Buffers b, int phase) {
     ScgState* st = b.st;
     if (phase != PH_DEBUG) {
@@ -209,16 +206,13 @@ __global__ void __launch_bounds__(GT) k_gen_update(StencilParams sp, GenParams g
         Pn[o] = pn;
         acc[2] = pn * pn;
         acc[3] = pn * __ldg(R + o);
-#pragma unroll
-        for (int dy = 0; dy < BW; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < BW; ++dx) {
-                if (dy == 0 && dx == 0) continue;
-                if (uy + dy < sp.H && ux + dx < sp.W) {
-                    const float t = xn - newx(uy + dy, ux + dx), dp = pn - newp(uy + dy, ux + dx);
-                    acc[1] = fmaf(sp.gam[dy * MAXBW + dx] * charb_d2(t, sp.eps2), dp * dp, acc[1]);
-                }
+        for (int o = 0; o < gp.noff; ++o) {
+            const int dy = gp.offy[o], dx = gp.offx[o];
+            if (uy + dy < sp.H && ux + dx >= 0 && ux + dx < sp.W) {
+                const float t = xn - newx(uy + dy, ux + dx), dp = pn - newp(uy + dy, ux + dx);
+                acc[1] = fmaf(gp.ogam[o] * charb_d2(t, sp.eps2), dp * dp, acc[1]);
             }
+        }
     }
     block_partials(acc, gp.part_a, gridDim.x, blockIdx.x);
 }
@@ -306,30 +300,18 @@ cudaError_t launch_gen_value_grad(int bw, int pn, const StencilParams& sp, const
     const long long nlr = (long long)gp.k * gp.lr_h * gp.lr_w, nhr = (long long)sp.H * sp.W;
     if (pn == 2) k_gen_residual<2><<<nblk(nlr), GT, 0, s>>>(sp, gp, b, phase);
     else k_gen_residual<1><<<nblk(nlr), GT, 0, s>>>(sp, gp, b, phase);
-    switch (pn * 10 + bw) {
-        case 11: k_gen_grad<1, 1><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 12: k_gen_grad<1, 2><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 13: k_gen_grad<1, 3><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 21: k_gen_grad<2, 1><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 22: k_gen_grad<2, 2><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 23: k_gen_grad<2, 3><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        default: return cudaErrorInvalidValue;
-    }
+    (void)bw;   // the general kernels walk the plan's BTV offset list (quadrant or Farsiu)
+    if (pn == 2) k_gen_grad<2><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase);
+    else k_gen_grad<1><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase);
     return cudaGetLastError();
 }
 
 cudaError_t launch_gen_update_curv(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
                                    int phase, cudaStream_t s) {
     const long long nlr = (long long)gp.k * gp.lr_h * gp.lr_w, nhr = (long long)sp.H * sp.W;
-    switch (pn * 10 + bw) {
-        case 11: k_gen_update<1, 1><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 12: k_gen_update<1, 2><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 13: k_gen_update<1, 3><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 21: k_gen_update<2, 1><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 22: k_gen_update<2, 2><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        case 23: k_gen_update<2, 3><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase); break;
-        default: return cudaErrorInvalidValue;
-    }
+    (void)bw;
+    if (pn == 2) k_gen_update<2><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase);
+    else k_gen_update<1><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase);
     if (pn == 2) k_gen_curv_data<2><<<nblk(nlr), GT, 0, s>>>(sp, gp, b, phase);
     else k_gen_curv_data<1><<<nblk(nlr), GT, 0, s>>>(sp, gp, b, phase);
     return cudaGetLastError();

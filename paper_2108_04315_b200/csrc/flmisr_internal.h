@@ -30,7 +30,8 @@ struct ScgState {
     int xcur, rcur;              // ping-pong indices of x/p and r buffers
     int accepted, converged_at, failed_stage, failed_iter;
     unsigned int counter;        // CTA arrival counter (last-CTA reduction), reset by the last CTA
-    int pad1;
+    int rules;                   // SCG variant bits (flmisr_config.scg_rules): 1 PR+ restart, 2 Netlab scale rules
+    double curv;                 // last exact curvature p^T Hess J p (Netlab rules recompute delta from it)
 };
 
 struct StencilParams {
@@ -96,7 +97,7 @@ cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, c
 cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s);  // world > 1
 cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s);   // world > 1
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,
-                              cudaStream_t s);
+                              int rules, cudaStream_t s);
 
 struct IngestParams {
     int H, W, pitch, k, lr_h, lr_w, mag;
@@ -109,6 +110,7 @@ struct IngestParams {
 
 // General-geometry path (flmisr_general.cu): per-frame integer phase and composed kernel.
 constexpr int GMAXK = 64;                                // frames supported by the general path
+constexpr int GMAXOFF = 16;                              // BTV offsets (w <= 3: quadrant 8, Farsiu 11)
 struct GenParams {
     int k, lr_h, lr_w, mag;
     int R, kd;                   // kappa offsets [-R, R+1] per axis, kd = 2R + 2
@@ -120,6 +122,9 @@ struct GenParams {
     double* part_a;              // NSLOT x max(nblk) partials of the first pass of each pair
     int sy[GMAXK], sx[GMAXK];    // integer HR phase floor(mag * shift_i)
     int integer_phase[GMAXK];    // 1: mag * shift_i is integral (interpolation fusion inserts the frame)
+    int noff;                    // BTV offsets d = (offy, offx), offy >= 0 (quadrant or Farsiu set)
+    int offy[GMAXOFF], offx[GMAXOFF];
+    float ogam[GMAXOFF];         // gamma(d)
 };
 cudaError_t launch_gen_value_grad(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
                                   int phase, cudaStream_t s);

@@ -320,7 +320,7 @@ __global__ void k_scalar_after_curv(Buffers b, int world) {
     scg_after_curv(s, t);
 }
 
-__global__ void k_state_init(ScgState* s, double lam0, double lambda_reg, int n_iter, long long npix) {
+__global__ void k_state_init(ScgState* s, double lam0, double lambda_reg, int n_iter, long long npix, int rules) {
     s->f = 0; s->f_new = 0; s->lam = lam0; s->lamb = 0; s->delta = 0; s->pp = 0; s->mu = 0;
     s->alpha = 0; s->beta = 0; s->rr = 0; s->lambda_reg = lambda_reg;
     for (int i = 0; i < 8; ++i) s->dbg[i] = 0;
@@ -328,6 +328,7 @@ __global__ void k_state_init(ScgState* s, double lam0, double lambda_reg, int n_
     s->npix = npix; s->k = 0; s->n_iter = n_iter; s->success = 1; s->done = 0;
     s->xcur = 0; s->rcur = 0; s->accepted = 0; s->converged_at = -1; s->failed_stage = 0; s->failed_iter = -1;
     s->counter = 0;
+    s->rules = rules; s->curv = 0;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -475,8 +476,8 @@ cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s
 }
 
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,
-                              cudaStream_t s) {
-    k_state_init<<<1, 1, 0, s>>>(b.st, lam0, lambda_reg, n_iter, npix);
+                              int rules, cudaStream_t s) {
+    k_state_init<<<1, 1, 0, s>>>(b.st, lam0, lambda_reg, n_iter, npix, rules);
     return cudaGetLastError();
 }
 

@@ -51,6 +51,9 @@ def cfg(**kw):
     (dict(shifts=np.array([[0, 0], [0, .5], [.5, .5], [.5, .5]]), world=2, rank=1, nccl_id=b"\0" * 128),
      "row-band partitioning"),
     (dict(k=65, shifts=np.zeros((65, 2))), "k <= 64"),
+    (dict(btv_offsets=2), "btv_offsets"),
+    (dict(scg_rules=4), "scg_rules"),
+    (dict(btv_offsets=1, world=2, rank=0, nccl_id=b"\0" * 128), "world must be 1"),
 ])
 def test_config_errors_raised_before_gpu_work(fl, kw, msg):
     c = cfg(**kw)

@@ -1,0 +1,92 @@
+"""NEXT-4 variants vs the fp64 oracle through the C ABI: Farsiu's BTV offset set
+(btv_offsets = 1, general path) and the SCG rule variants (scg_rules: 1 PR+ restart, 2 Netlab
+scale rules) on the fast streaming path and the general path.  Same bars as the default readings."""
+import numpy as np
+import pytest
+
+from paper_2108_04315_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2108_04315_b200 import flmisr  # noqa: E402
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+GEOM = {
+    "polyphase": (31, 40, synth.shift_pattern(2)),
+    "fractional": (26, 22, np.array([[0, 0], [0.2, 0.7], [0.55, 0.1]])),
+}
+
+
+def make(orc, geom, w=3, offsets=1, rules=0, p_norm=1, lam=0.05, n_iter=20):
+    lr_h, lr_w, sh = GEOM[geom]
+    kw = dict(k=len(sh), lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=synth.gaussian_psf(), mag=2, p_norm=p_norm,
+              lam=lam, btv_window=w)
+    pl = flmisr.Plan(**kw, n_iter=n_iter, btv_offsets=offsets, scg_rules=rules)
+    pb = orc.Problem(**kw, btv_offsets=offsets)
+    return pl, pb
+
+
+@pytest.mark.parametrize("geom", list(GEOM))
+@pytest.mark.parametrize("w", [2, 3])
+def test_farsiu_offsets_operators(orc, geom, w):
+    pl, pb = make(orc, geom, w=w)
+    assert pl.fast_path == 0
+    x = synth.random_fields((pb.H, pb.W), 3)
+    y = synth.random_fields((pb.k, pb.lr_h, pb.lr_w), 4)
+    out = torch.zeros((pb.H, pb.W), device="cuda")
+    D, R, rr, _ = pl.debug(flmisr.OP_GRAD, lr=dev(y), in0=dev(x), out=out)
+    g = orc.grad(pb, x.astype(np.float64), y.astype(np.float64))
+    assert rel(out.cpu().numpy(), -g) <= 1e-5
+    Dr, Rr = orc.value(pb, x.astype(np.float64), y.astype(np.float64))
+    assert abs(D - Dr) <= 1e-5 * abs(Dr) and abs(R - Rr) <= 1e-5 * abs(Rr)
+    p = synth.random_fields((pb.H, pb.W), 7, -1, 1)
+    # p_norm = 2 isolates the BTV curvature from the ill-conditioned Charbonnier data curvature
+    pl2, pb2 = make(orc, geom, w=w, p_norm=2, lam=0.5)
+    delta, pp, mu, _ = pl2.debug(flmisr.OP_CURV, lr=dev(y), in0=dev(x), in1=dev(p))
+    ref = orc.curv(pb2, x.astype(np.float64), y.astype(np.float64), p.astype(np.float64))
+    assert abs(delta - ref) <= 1e-5 * abs(ref)
+
+
+@pytest.mark.parametrize("geom", list(GEOM))
+def test_farsiu_offsets_reconstruct(orc, geom):
+    lr_h, lr_w, sh = GEOM[geom]
+    truth = synth.phantom(2 * lr_h, 2 * lr_w, seed=71)
+    y = synth.detector_stack(truth, 2, sh, 1 / 255, seed=71).astype(np.float32)
+    pl, pb = make(orc, geom)
+    hr, rep = pl.reconstruct(dev(y))
+    xo, tr, st = orc.scg(pb, y.astype(np.float64), 20)
+    assert rel(hr.cpu().numpy(), xo) <= 1e-3
+    np.testing.assert_allclose(rep["trace"][:, 1], tr[:, 1], rtol=1e-4)
+    np.testing.assert_array_equal(rep["trace"][:, 5], tr[:, 5])
+
+
+@pytest.mark.parametrize("geom", list(GEOM))
+@pytest.mark.parametrize("rules", [1, 2, 3])
+def test_scg_rules_reconstruct(orc, geom, rules):
+    """PR+ / Netlab variants: image, f trace, lambda_scg trace and accept flags follow the oracle.
+    The polyphase geometry runs on the streaming kernels, the fractional one on the general path."""
+    lr_h, lr_w, sh = GEOM[geom]
+    truth = synth.phantom(2 * lr_h, 2 * lr_w, seed=72)
+    y = synth.detector_stack(truth, 2, sh, 1 / 255, seed=72).astype(np.float32)
+    pl, pb = make(orc, geom, offsets=0, rules=rules)
+    assert pl.fast_path == (2 if geom == "polyphase" else 0)
+    hr, rep = pl.reconstruct(dev(y))
+    xo, tr, st = orc.scg(pb, y.astype(np.float64), 20, rules=rules)
+    assert rel(hr.cpu().numpy(), xo) <= 1e-3
+    np.testing.assert_allclose(rep["trace"][:, 1], tr[:, 1], rtol=1e-4)
+    np.testing.assert_allclose(rep["trace"][:, 4], tr[:, 4], rtol=1e-3)
+    np.testing.assert_array_equal(rep["trace"][:, 5], tr[:, 5])

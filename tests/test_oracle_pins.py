@@ -351,3 +351,116 @@ def test_interp_fuse_partial_coverage(orc):
     np.testing.assert_array_equal(out[1::2, 1::2], x[1::2, 1::2])
     x0 = orc.init_x0(pb, y)
     np.testing.assert_array_equal(out[0::2, 1::2], x0[0::2, 1::2])
+
+
+# ----------------------------------------------------------------------------- NEXT-4 variants
+def _psi(t, eps=1e-3):
+    return np.sqrt(t * t + eps * eps) - eps
+
+
+@pytest.mark.parametrize("offsets", [0, 1])
+def test_btv_offsets_2x2_closed_form(orc, offsets):
+    """w = 2 on [[a, b], [c, d]]: the quadrant has d = (0,1), (1,0), (1,1); Farsiu's set
+    (m in [0,1], l in [-1,1], l + m >= 0) adds the anti-diagonal (1,-1) with gamma = alpha^2:
+    R = alpha [psi(a-b) + psi(c-d) + psi(a-c) + psi(b-d)] + alpha^2 [psi(a-d) (+ psi(b-c))]."""
+    a, b, c, d = 0.9, 0.1, 0.35, 0.6
+    al = 0.4
+    pb = orc.Problem(k=1, lr_h=2, lr_w=2, shifts=np.zeros((1, 2)), psf=np.ones((1, 1)), mag=1,
+                     btv_alpha=al, btv_window=2, btv_offsets=offsets)
+    x = np.array([[a, b], [c, d]])
+    _, R = orc.value(pb, x, x[None])
+    ref = al * (_psi(a - b) + _psi(c - d) + _psi(a - c) + _psi(b - d)) + al ** 2 * _psi(a - d)
+    if offsets:
+        ref += al ** 2 * _psi(b - c)
+    assert abs(R - ref) <= 1e-15
+
+
+def test_btv_farsiu_w3_weights(orc):
+    """Farsiu w = 3 on a 3x3 image with a single bright centre pixel: every pair touching the centre
+    has |diff| = 1; the offsets reaching it are the 11 of the set, each counted from both sides when
+    valid.  Brute force from the set {(m, l): 0 <= m <= 2, -2 <= l <= 2, l + m >= 0} \\ {(0,0)}."""
+    al, eps = 0.4, 1e-3
+    pb = orc.Problem(k=1, lr_h=3, lr_w=3, shifts=np.zeros((1, 2)), psf=np.ones((1, 1)), mag=1,
+                     btv_alpha=al, btv_window=3, btv_offsets=1, eps=eps)
+    x = np.zeros((3, 3))
+    x[1, 1] = 1.0
+    _, R = orc.value(pb, x, x[None])
+    offs = [(m, l) for m in range(3) for l in range(-2, 3) if l + m >= 0 and (m, l) != (0, 0)]
+    assert len(offs) == 11
+    ref = 0.0
+    for m, l in offs:
+        for (u, v) in [(1 - m, 1 - l), (1, 1)]:          # centre as second or first endpoint
+            u2, v2 = u + m, v + l
+            if 0 <= u < 3 and 0 <= v < 3 and 0 <= u2 < 3 and 0 <= v2 < 3 and (u, v) != (u2, v2):
+                ref += al ** (abs(l) + m) * _psi(x[u, v] - x[u2, v2], eps)
+    assert abs(R - ref) <= 1e-15
+
+
+def test_gradient_and_curvature_fd_farsiu(orc):
+    """Farsiu offsets: central-FD gradient (<= 1e-6 rel L2) and curvature (<= 1e-6) on 16x16."""
+    pb = problem(orc, lr=8, mag=2, p_norm=1, lam=0.3, shifts=[[0, 0], [0, .5], [.5, .5], [.5, .1]])
+    pb.btv_offsets = 1
+    rng = np.random.default_rng(31)
+    x = rng.uniform(size=(pb.H, pb.W))
+    y = rng.uniform(size=(pb.k, pb.lr_h, pb.lr_w))
+    g = orc.grad(pb, x, y)
+    h = 1e-6
+    fd = np.zeros_like(x)
+    for n in range(x.size):
+        xp = x.copy().ravel(); xp[n] += h
+        xm = x.copy().ravel(); xm[n] -= h
+        fd.ravel()[n] = (orc.objective(pb, xp, y) - orc.objective(pb, xm, y)) / (2 * h)
+    assert np.linalg.norm(g - fd) <= 1e-6 * np.linalg.norm(fd)
+    p = rng.standard_normal((pb.H, pb.W))
+    cfd = (np.vdot(p, orc.grad(pb, x + h * p, y)) - np.vdot(p, orc.grad(pb, x - h * p, y))) / (2 * h)
+    assert abs(orc.curv(pb, x, y, p) - cfd) <= 1e-6 * abs(cfd)
+
+
+def test_band_simulation_farsiu_equals_centralised(orc):
+    """The anti-diagonal offsets keep the halo at w - 1 rows: g = 4 bands with eta = 2 == g = 1."""
+    y, sh, _ = synth.make_stack(32, 2, seed=32)
+    pb = problem(orc, lr=32, mag=2, shifts=sh)
+    pb.btv_offsets = 1
+    x1, tr1, _ = orc.scg(pb, y, 6, g=1)
+    xg, trg, _ = orc.scg(pb, y, 6, g=4, eta=2)
+    assert np.linalg.norm(xg - x1) <= 1e-10 * np.linalg.norm(x1)
+
+
+@pytest.mark.parametrize("rules", [1, 2, 3])
+def test_scg_rule_variants_equal_cg_on_quadratic(orc, rules):
+    """On a strictly convex quadratic PR+ never triggers (beta = <r,r>/mu > 0) and the Netlab scale
+    rules keep lambda negligible, so every variant reproduces textbook CG (scipy) like Moller's."""
+    pb = problem(orc, lr=6, mag=2, p_norm=2, lam=0.0)
+    rng = np.random.default_rng(12)
+    y = rng.uniform(size=(pb.k, pb.lr_h, pb.lr_w))
+    A, _ = _dense(orc, pb)
+    x0 = orc.init_x0(pb, y)
+    its = []
+    spla.cg(2 * A.T @ A, 2 * A.T @ y.ravel(), x0=x0.ravel(), rtol=1e-30, atol=0, maxiter=12,
+            callback=lambda xk: its.append(xk.copy()))
+    for n in (1, 3, 6, 12):
+        xs, _, _ = orc.scg(pb, y, n, x0=x0, rules=rules)
+        assert np.linalg.norm(xs.ravel() - its[n - 1]) <= 1e-4 * np.linalg.norm(its[n - 1]), n
+
+
+def test_netlab_lambda_rule_1d(orc):
+    """J(x) = (x - 3)^2 from x0 = 0, lambda_1 = 1e-6: the first step is accepted with Delta ~ 1 > 0.75,
+    so Moller divides lambda by 4 and Netlab halves it (exact fp64 scalings of 1e-6); x1 agrees."""
+    pb = orc.Problem(k=1, lr_h=1, lr_w=1, shifts=np.zeros((1, 2)), psf=np.ones((1, 1)), mag=1,
+                     p_norm=2, lam=0.0)
+    y = np.array([[[3.0]]])
+    xm, trm, _ = orc.scg(pb, y, 1, x0=np.zeros((1, 1)))
+    xn, trn, _ = orc.scg(pb, y, 1, x0=np.zeros((1, 1)), rules=orc.RULE_NETLAB)
+    assert trm[1, 4] == 1e-6 / 4 and trn[1, 4] == 1e-6 / 2
+    assert xm[0, 0] == xn[0, 0]
+
+
+def test_pr_plus_monotone_on_robust_problem(orc):
+    """PR+ and Netlab variants on the robust (Charbonnier) problem: f non-increasing over accepted
+    steps and a substantial decrease within 20 passes (same bar as Moller's)."""
+    y, sh, _ = synth.make_stack(24, 2, seed=21)
+    pb = problem(orc, lr=24, mag=2, shifts=sh)
+    for rules in (1, 2, 3):
+        x, tr, st = orc.scg(pb, y, 20, rules=rules)
+        assert np.all(np.diff(tr[:, 1]) <= 0)
+        assert tr[-1, 1] <= 0.6 * tr[0, 1]
