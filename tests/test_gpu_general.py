@@ -98,7 +98,7 @@ def test_curvature(orc, name):
 
 
 def curv_rounding_bound(orc, pb, x, y, p, u=2.0 ** -24, sigmas=6.0):
-    """Propagated fp32 rounding of the data curvature sum_i rho''(e_i) (A p)_i^2 (reading 22).
+    """Propagated fp32 rounding of the data curvature sum_i rho''(e_i) (A p)_i^2 (reading 23).
 
     For the Charbonnier penalty rho''(e) = eps^2 / (e^2 + eps^2)^(3/2) is ill-conditioned near e = 0:
     d rho''/de = -3 eps^2 e / (e^2 + eps^2)^(5/2), ~1/eps^2 at |e| ~ eps.  Each fp32 residual carries the
