@@ -343,15 +343,41 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
             const long long cap = (long long)nsm * SMINB * sp.wpb;   // one wave of resident warps
             const int rows = p->row_hi - p->row_lo;
+            // Work items, one warp each, one wave.  Warps touching an image or band edge run the border
+            // instantiation, ~1.4x slower per row (per-warp timing), so border pieces
+            // get seg_b ~ seg_rows / 1.4 rows: interior strips are split seg_b | seg_rows ... | seg_b,
+            // the two edge strips (column 0 / W-1) into pieces of seg_b.
+            double ratio = 1.4;
+            if (const char* ev = std::getenv("FLMISR_EDGE_RATIO")) ratio = std::max(1.0, std::atof(ev));
+            sp.ne = sp.nstrips >= 2 ? 2 : 1;
+            sp.ni = sp.nstrips - sp.ne;
+            auto to1mod3 = [](int v) { v = std::max(v, 4); return v + ((1 - v % 3) + 3) % 3; };
+            auto nseg_int = [&](int Si, int Sb) {   // pieces of one interior strip
+                return rows <= 2 * Sb ? (rows + Sb - 1) / Sb : 2 + (rows - 2 * Sb + Si - 1) / Si;
+            };
+            auto items = [&](int Si, int Sb) {
+                return (long long)sp.ni * nseg_int(Si, Sb) + (long long)sp.ne * ((rows + Sb - 1) / Sb);
+            };
             int S = 16;
-            while (S < rows && (long long)sp.nstrips * ((rows + S - 1) / S) > cap) S += 3;
+            int Sb = to1mod3((int)(S / ratio));
+            while (S < rows && items(S, Sb) > cap) {
+                S += 3;
+                Sb = to1mod3((int)(S / ratio));
+            }
             if (const char* ev = std::getenv("FLMISR_SEG_ROWS")) {   // tuning override (S = 1 mod 3)
                 const int v = std::atoi(ev);
-                if (v >= 4) S = v + ((1 - v % 3) + 3) % 3;
+                if (v >= 4) { S = to1mod3(v); Sb = to1mod3((int)(S / ratio)); }
             }
-            if (S > rows) S = rows + ((1 - rows % 3) + 3) % 3;   // smallest >= rows with S = 1 mod 3
+            S = std::min(S, rows + ((1 - rows % 3) + 3) % 3);     // smallest >= rows with S = 1 mod 3
+            Sb = std::min(Sb, S);
             sp.seg_rows = S;
-            sp.nsegs = (rows + S - 1) / S;
+            sp.seg_b = Sb;
+            sp.nseg_i = nseg_int(S, Sb);
+            if (rows <= 2 * Sb) sp.seg_rows = Sb;   // short bands: interior strips in seg_b pieces too
+            sp.nseg_b = (rows + Sb - 1) / Sb;
+            sp.n_int = sp.ni * sp.nseg_i;
+            sp.nitems = sp.n_int + sp.ne * sp.nseg_b;
+            sp.nsegs = sp.nseg_i;
             // hoisted constants: D = sum q rs - eps N, R = sum gamma q rs - eps sum_d gamma_d n_d,
             // curvature sums carry eps^2 (p = 1) or 2 (p = 2)
             const double eps = c.l1_eps;
@@ -400,7 +426,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     b.X[0] = p->mem + 1 * fl; b.X[1] = p->mem + 2 * fl;
     b.P[0] = p->mem + 3 * fl; b.P[1] = p->mem + 4 * fl;
     b.R[0] = p->mem + 5 * fl; b.R[1] = p->mem + 6 * fl;
-    const size_t nsblk = p->stream_path ? ((size_t)sp.nstrips * sp.nsegs + sp.wpb - 1) / sp.wpb : 0;
+    const size_t nsblk = p->stream_path ? ((size_t)sp.nitems + sp.wpb - 1) / sp.wpb : 0;
     const long long nlr_px = (long long)K * c.lr_h * c.lr_w, nhr_px = (long long)p->H * p->W;
     const size_t ngblk = fast ? 0 : std::max<size_t>(gen_blocks(nlr_px), gen_blocks(nhr_px));
     const size_t ntiles = std::max<size_t>(std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk), ngblk);
@@ -670,11 +696,13 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
     // the device) is one CUDA graph, captured on the first call and replayed into the caller's stream.
     flmisr_status st = FLMISR_OK;
     // the loop body; with profiling, event records between the kernels (captured as graph nodes)
-    auto loop = [&](cudaStream_t ls, int ev0) -> flmisr_status {
+    auto loop = [&](cudaStream_t ls, int ev0, bool captured) -> flmisr_status {
         int e = ev0;
         // external event nodes: inside a captured graph a plain record is only an internal dependency
         auto m = [&]() -> cudaError_t {
-            return prof ? cudaEventRecordWithFlags(pr.ev[e++], ls, cudaEventRecordExternal) : cudaSuccess;
+            if (!prof) return cudaSuccess;
+            return captured ? cudaEventRecordWithFlags(pr.ev[e++], ls, cudaEventRecordExternal)
+                            : cudaEventRecord(pr.ev[e++], ls);
         };
         flmisr_status r = enqueue_value_grad(p, PH_INIT, ls);
         if (r != FLMISR_OK) return r;
@@ -693,7 +721,7 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
         if (!ge) {
             cudaStream_t cs = p->stream;   // capture needs a non-legacy stream
             CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-            st = loop(cs, ev);
+            st = loop(cs, ev, true);
             cudaGraph_t graph = nullptr;
             cudaError_t ce = cudaStreamEndCapture(cs, &graph);
             if (st != FLMISR_OK) {
@@ -707,7 +735,7 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
         }
         CUDA_TRY(cudaGraphLaunch(ge, s));
     } else {
-        st = loop(s, ev);
+        st = loop(s, ev, false);
         if (st != FLMISR_OK) return st;
     }
     if (prof) ev += 1 + 2 * p->cfg.n_iter;

@@ -49,6 +49,10 @@ struct StencilParams {
     float ka[3], kb[3];          // kappa(P,Q) = ka[P+1] * kb[Q+1] (KR <= 1; KR = 0 zero-padded)
     float lgam[MAXBW * MAXBW];   // lambda * gamma(dy,dx)
     int nstrips, nsegs, seg_rows, wpb;   // 128-column warp strips (step 124), row segments, warps/CTA
+    // work items (one warp each): n_int = ni * nseg_i segments of seg_rows rows on the ni interior
+    // strips, then ne * nseg_b segments of seg_b rows on the ne edge strips (column 0 / column W-1),
+    // which run the slower border code and therefore get shorter segments (one balanced wave)
+    int ni, ne, nseg_i, nseg_b, seg_b, n_int, nitems;
     double gcls[4];              // gamma of BTV class dx+dy = 1..4 (fp64, applied to the CTA sums)
     // affine correction of the raw CTA sums before the scalar logic: tot = raw * aff[k] + aff[4+k]
     double aff_vg[2 * NSLOT], aff_uc[2 * NSLOT];
@@ -56,10 +60,10 @@ struct StencilParams {
 
 // Streaming kernels (flmisr_stream.cu): strips of SCOLS columns per warp, stepping by SSTEP.
 #ifndef FLMISR_SWPB
-#define FLMISR_SWPB 8
+#define FLMISR_SWPB 16
 #endif
 #ifndef FLMISR_SMINB
-#define FLMISR_SMINB 2
+#define FLMISR_SMINB 1
 #endif
 constexpr int SWPB = FLMISR_SWPB;    // warps per CTA of the streaming kernels
 constexpr int SMINB = FLMISR_SMINB;  // resident CTAs per SM they are compiled for (register budget)

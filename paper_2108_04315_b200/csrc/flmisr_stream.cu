@@ -26,6 +26,7 @@
 // Constant terms (eps of every Charbonnier term, eps^2 of rho''/psi'') are hoisted into the affine
 // correction of the CTA sums (StencilParams::aff_*).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "flmisr_common.cuh"
@@ -195,8 +196,32 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp) {
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     g.lane = threadIdx.x & 31;
     const int gw = blockIdx.x * SWPB + warp;
-    g.live = gw < sp.nstrips * sp.nsegs;
-    const int strip = g.live ? gw % sp.nstrips : 0, seg = g.live ? gw / sp.nstrips : 0;
+    g.live = gw < sp.nitems;
+    // work item -> (strip, rows [r_lo, r_hi)); see StencilParams: border pieces (band edges, edge
+    // strips) are seg_b rows, interior pieces seg_rows rows
+    int strip = 0, seg = 0, nseg = 1;
+    g.r_lo = g.r_hi = sp.row_lo;
+    if (g.live && gw < sp.n_int) {            // interior strip 1 .. ni: seg_b | seg_rows ... | seg_b
+        strip = 1 + gw % sp.ni;
+        seg = gw / sp.ni;
+        nseg = sp.nseg_i;
+        if (seg == 0) {
+            g.r_hi = min(sp.row_lo + sp.seg_b, sp.row_hi);
+        } else if (seg == nseg - 1) {
+            g.r_lo = max(sp.row_hi - sp.seg_b, sp.row_lo + sp.seg_b);
+            g.r_hi = sp.row_hi;
+        } else {
+            g.r_lo = sp.row_lo + sp.seg_b + (seg - 1) * sp.seg_rows;
+            g.r_hi = min(g.r_lo + sp.seg_rows, sp.row_hi - sp.seg_b);
+        }
+    } else if (g.live) {                      // edge strip 0 / nstrips-1: seg_b rows each
+        const int e = gw - sp.n_int;
+        strip = (sp.ne == 1 || (e & 1) == 0) ? 0 : sp.nstrips - 1;
+        seg = e / sp.ne;
+        nseg = sp.nseg_b;
+        g.r_lo = sp.row_lo + seg * sp.seg_b;
+        g.r_hi = min(g.r_lo + sp.seg_b, sp.row_hi);
+    }
     g.cbase = strip * SSTEP;
     g.col0 = g.cbase + 4 * g.lane;
     g.strip0 = strip == 0;
@@ -209,8 +234,6 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp) {
     g.cv4 = g.col0 + 4 < sp.W;
     g.rstrip = g.cbase + SCOLS > sp.W;
     g.llast = min(max((sp.W - 1 - g.cbase) >> 2, 0), 31);
-    g.r_lo = sp.row_lo + seg * sp.seg_rows;
-    g.r_hi = min(g.r_lo + sp.seg_rows, sp.row_hi);
     if (!g.live) g.r_hi = g.r_lo;
     // rows whose new x/p this segment writes: owned rows, plus the band's halo rows for the first /
     // last segment of a band with a neighbour on that side (bit-identical to the neighbour's owned
@@ -218,7 +241,7 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp) {
     g.w_lo = g.r_lo;
     g.w_hi = g.r_hi;
     if (g.live && seg == 0 && sp.row_lo > 0) g.w_lo = sp.store_lo;
-    if (g.live && seg == sp.nsegs - 1 && sp.row_hi < sp.H) g.w_hi = sp.store_hi;
+    if (g.live && seg == nseg - 1 && sp.row_hi < sp.H) g.w_hi = sp.store_hi;
     // interior warps: no image border, every row they touch (r_lo - 2 .. r_hi + 2) is an owned row of
     // the band, so they need no clamps, no halo buffers and no masks beyond the strip's output columns
     g.border = g.strip0 || g.rstrip || g.r_lo < sp.row_lo + 3 || g.r_hi > sp.row_hi - 3;
@@ -472,7 +495,7 @@ struct VG {
 #pragma unroll
         for (int s = 0; s < 3; ++s) GA[s] = GB[s] = GD[s] = GE[s] = z;
         t0 = g.r_lo - 2;
-        nstep = sp.seg_rows + 2;   // multiple of 3 (seg_rows = 1 mod 3)
+        nstep = (g.r_hi - g.r_lo + 4) / 3 * 3;   // rows r_lo - 2 .. r_hi - 1, rounded up to the unroll
         if (!BORDER) {
             const size_t o = (size_t)(t0 - sp.store_lo) * sp.pitch + g.cbase;
             ix = X0 + o + 2 * (size_t)sp.pitch;
@@ -495,14 +518,40 @@ struct VG {
     }
 };
 
+// Programmatic dependent launch: the streaming kernels are launched with programmatic stream
+// serialization, so the next kernel's CTAs may be scheduled onto SMs this grid has already left;
+// every kernel waits for its predecessor's completion (and memory flush) before touching any data.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+#ifdef FLMISR_TIMING
+// diagnostic build only: per-warp (start ns, end ns, smid | border << 16) of the last k_vg_stream launch
+__device__ unsigned long long g_warp_time[3 * 16384];
+__device__ unsigned long long g_cta_time[3 * 2048];   // per CTA: entry, after the CTA reduction, last-CTA finish
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
+#ifdef FLMISR_TIMING
+    if (threadIdx.x == 0 && blockIdx.x < 2048) g_cta_time[3 * blockIdx.x] = gtimer();
+#endif
     ScgState* st = b.st;
     if (phase != PH_DEBUG && st->done) return;
     const int xcur = st->xcur, rcur = st->rcur;
     const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
     const Geo g = geometry(sp);
+#ifdef FLMISR_TIMING
+    const unsigned long long t_start = gtimer();
+#endif
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
@@ -529,8 +578,33 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp
         acc[2] = a_rr;
         acc[3] = a_rro;
     }
+#ifdef FLMISR_TIMING
+    if (g.lane == 0) {
+        const int gw = blockIdx.x * SWPB + (threadIdx.x >> 5);
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        if (gw < 16384) {
+            g_warp_time[3 * gw] = t_start;
+            g_warp_time[3 * gw + 1] = gtimer();
+            g_warp_time[3 * gw + 2] = smid | ((unsigned long long)g.border << 16) | ((unsigned long long)g.live << 17) |
+                                      ((unsigned long long)(g.cbase / SSTEP) << 20) |
+                                      ((unsigned long long)(g.r_lo - sp.row_lo) << 36);
+        }
+    }
+#endif
     double tot[NSLOT];
+#ifdef FLMISR_TIMING
+    const bool last = reduce_partials(acc, b.part, gridDim.x, blockIdx.x, &st->counter, tot);
+    if (threadIdx.x == 0 && blockIdx.x < 2048) g_cta_time[3 * blockIdx.x + 1] = gtimer();
+    if (last) {
+        finish_scalars<0>(sp, b, tot, phase);
+        if (threadIdx.x == 0 && blockIdx.x < 2048) g_cta_time[3 * blockIdx.x + 2] = gtimer();
+    } else if (threadIdx.x == 0 && blockIdx.x < 2048) {
+        g_cta_time[3 * blockIdx.x + 2] = 0;
+    }
+#else
     if (reduce_partials(acc, b.part, gridDim.x, blockIdx.x, &st->counter, tot)) finish_scalars<0>(sp, b, tot, phase);
+#endif
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -671,7 +745,7 @@ struct UC {
 #pragma unroll
         for (int c = 0; c < 4; ++c) cb[c] = z;
         t0 = g.r_lo - 2;
-        nstep = sp.seg_rows + 2;
+        nstep = (g.r_hi - g.r_lo + 4) / 3 * 3;
         if (!BORDER) {
             const size_t o = (size_t)(t0 - sp.store_lo) * sp.pitch + g.cbase;
             ix = X0 + o + 2 * (size_t)sp.pitch;
@@ -697,6 +771,7 @@ struct UC {
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter();
     ScgState* st = b.st;
     if (phase != PH_DEBUG) {
         if (st->done) return;
@@ -743,6 +818,11 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp
     }
 }
 
+bool pdl_enabled() {
+    static const bool on = std::getenv("FLMISR_NO_PDL") == nullptr;
+    return on;
+}
+
 template <typename K>
 cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers& b, int phase, cudaStream_t s) {
     // opt in to > 48 KB of dynamic shared memory once per kernel instantiation (per device)
@@ -758,14 +838,23 @@ cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers
         if (e != cudaSuccess) return e;
         if (ndone < 64) done[ndone++] = key;
     }
-    kernel<<<(nw + SWPB - 1) / SWPB, SWPB * 32, RING_SMEM, s>>>(sp, b, phase);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((nw + SWPB - 1) / SWPB);
+    cfg.blockDim = dim3(SWPB * 32);
+    cfg.dynamicSmemBytes = RING_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, sp, b, phase);
 }
 
 }  // namespace
 
 #define FL_SCASE(K, BW_, PN_) \
-    case BW_ * 10 + PN_: return launch_ring(K<BW_, PN_>, sp.nstrips * sp.nsegs, sp, b, phase, s);
+    case BW_ * 10 + PN_: return launch_ring(K<BW_, PN_>, sp.nitems, sp, b, phase, s);
 
 cudaError_t launch_value_grad_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
                                      cudaStream_t s) {
@@ -786,3 +875,14 @@ cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, c
 }
 
 }  // namespace flmisr
+
+#ifdef FLMISR_TIMING
+extern "C" int flmisr_debug_warp_timing(unsigned long long* host, int n) {
+    if (n > 3 * 16384) n = 3 * 16384;
+    return (int)cudaMemcpyFromSymbol(host, flmisr::g_warp_time, (size_t)n * sizeof(unsigned long long));
+}
+extern "C" int flmisr_debug_cta_timing(unsigned long long* host, int n) {
+    if (n > 3 * 2048) n = 3 * 2048;
+    return (int)cudaMemcpyFromSymbol(host, flmisr::g_cta_time, (size_t)n * sizeof(unsigned long long));
+}
+#endif
