@@ -124,8 +124,10 @@ flmisr_status flmisr_finish(flmisr_plan_t plan, flmisr_report* report);
 /*
  * flmisr_profile: per-kernel CUDA-event timing on the launching stream.  enable = 1 turns it on and
  * resets the counters, 0 turns it off and resets, -1 only reads.  out8 (nullable, host, 8 doubles)
- * receives {launches, total ms} for: [0] value+gradient kernel, [1] update+curvature kernel,
- * [2] setup+finalize (ingest, x0, state, output), [3] whole reconstructions.
+ * receives {launches, total ms} for: [0] value+gradient kernel (or, when the plan runs the SCG loop as
+ * one persistent kernel, that kernel: one launch per reconstruction), [1] update+curvature kernel
+ * (0 launches in the persistent mode), [2] setup+finalize (ingest, x0, state, output), [3] whole
+ * reconstructions.
  */
 flmisr_status flmisr_profile(flmisr_plan_t plan, int32_t enable, double* out8);
 
@@ -165,9 +167,11 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
  * bytes to the other ranks, e.g. over the torch process group; S:288 coordinator role). */
 flmisr_status flmisr_nccl_unique_id(void* out128);
 
-/* HR geometry of a plan: H, W, owned rows [row_lo, row_hi), and whether the fast path is used. */
+/* HR geometry of a plan: H, W, owned rows [row_lo, row_hi); fast_path = 0 general-geometry kernels,
+ * 1 tiled polyphase kernels, 2 streaming polyphase kernels; loop_kernel = 1 when the SCG loop runs as
+ * one persistent cooperative kernel (streaming path, world 1).  Any output may be NULL. */
 flmisr_status flmisr_plan_info(flmisr_plan_t plan, int32_t* H, int32_t* W, int32_t* row_lo, int32_t* row_hi,
-                               int32_t* fast_path);
+                               int32_t* fast_path, int32_t* loop_kernel);
 
 /* ------------------------------------------------------------------------------------------
  * Streaming capture-reconstruct pipeline (fig:capture: each view is

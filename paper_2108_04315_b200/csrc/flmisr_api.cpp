@@ -132,6 +132,8 @@ struct flmisr_plan_s {
     cudaGraphExec_t graph_exec = nullptr;   // the captured SCG loop (world == 1)
     cudaGraphExec_t graph_exec_prof = nullptr;   // the same with per-kernel event records
     int no_graph = 0;                       // FLMISR_NO_GRAPH=1: always launch eagerly
+    int persist = 0;                        // 1: the SCG loop runs as one persistent cooperative kernel
+    int prof_mode = 0;                      // layout of the profiling marks of the last call (0 per-kernel, 1 loop)
     flmisr_pipeline_s* pipe = nullptr;      // the pipeline driving this plan, if any
 };
 
@@ -430,9 +432,10 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     const long long nlr_px = (long long)K * c.lr_h * c.lr_w, nhr_px = (long long)p->H * p->W;
     const size_t ngblk = fast ? 0 : std::max<size_t>(gen_blocks(nlr_px), gen_blocks(nhr_px));
     const size_t ntiles = std::max<size_t>(std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk), ngblk);
-    const size_t npart = std::max<size_t>(NSLOT * ntiles, (size_t)NSLOT * world);
+    // x2: the persistent loop kernel double-buffers its per-CTA slots by phase parity
+    const size_t npart = std::max<size_t>(2 * NSLOT * ntiles, (size_t)NSLOT * world);
     const size_t ntrace = (size_t)(c.n_iter + 1) * 6;
-    const size_t nd = npart + NSLOT + ntrace + (size_t)NSLOT * world;
+    const size_t nd = npart + NSLOT + ntrace + (size_t)NSLOT * world + 1;   // + the grid-barrier counter
     e = cudaMalloc(&p->dmem, nd * sizeof(double));
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc partials: ") + cudaGetErrorString(e)));
     cudaMemset(p->dmem, 0, nd * sizeof(double));
@@ -440,6 +443,16 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     b.rank_sums = p->dmem + npart;
     b.trace = p->dmem + npart + NSLOT;
     p->gathered = p->dmem + npart + NSLOT + ntrace;
+    b.gbar = reinterpret_cast<unsigned*>(p->dmem + nd - 1);
+    {   // opt-in (FLMISR_PERSIST=1): the whole SCG loop as one cooperative kernel (streaming path, one
+        // GPU).  It removes the per-phase kernel boundary and last-CTA reduction (~11 us per phase) but
+        // its single large body loses ~10% of per-phase throughput to register allocation (DESIGN.md
+        // 7.2), so the per-phase kernels stay the default
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c.device);
+        const char* pe = std::getenv("FLMISR_PERSIST");
+        p->persist = p->stream_path && world == 1 && !virt && coop && pe && std::atoi(pe) != 0;
+    }
     e = cudaMalloc(&p->st, sizeof(ScgState));
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc state: ") + cudaGetErrorString(e)));
     cudaMemset(p->st, 0, sizeof(ScgState));
@@ -553,8 +566,9 @@ flmisr_status flmisr_nccl_unique_id(void* out128) {
 }
 
 flmisr_status flmisr_plan_info(flmisr_plan_t p, int32_t* H, int32_t* W, int32_t* row_lo, int32_t* row_hi,
-                               int32_t* fast_path) {
+                               int32_t* fast_path, int32_t* loop_kernel) {
     if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    if (loop_kernel) *loop_kernel = p->persist;
     if (H) *H = p->H;
     if (W) *W = p->W;
     if (row_lo) *row_lo = p->row_lo;
@@ -715,8 +729,23 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
         }
         return FLMISR_OK;
     };
-    const bool use_graph = p->cfg.world == 1 && !p->no_graph;
-    if (use_graph) {
+    bool looped = false;
+    if (p->persist) {   // one cooperative kernel for the init pass and all n_iter passes
+        cudaError_t le = launch_scg_loop_stream(p->bw, p->pn, p->sp, p->b, s);
+        if (le == cudaSuccess) {
+            looped = true;
+            CUDA_TRY(mark());   // ev2: end of the loop kernel
+            p->prof_mode = 1;
+        } else if (le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorNotSupported) {
+            cudaGetLastError();   // not co-resident on this device / context: per-kernel launches instead
+            p->persist = 0;
+        } else {
+            return fail(FLMISR_ERR_CUDA, std::string("persistent SCG loop launch: ") + cudaGetErrorString(le));
+        }
+    }
+    const bool use_graph = !looped && p->cfg.world == 1 && !p->no_graph;
+    if (looped) {
+    } else if (use_graph) {
         cudaGraphExec_t& ge = prof ? p->graph_exec_prof : p->graph_exec;
         if (!ge) {
             cudaStream_t cs = p->stream;   // capture needs a non-legacy stream
@@ -738,7 +767,10 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
         st = loop(s, ev, false);
         if (st != FLMISR_OK) return st;
     }
-    if (prof) ev += 1 + 2 * p->cfg.n_iter;
+    if (!looped) {
+        p->prof_mode = 0;
+        if (prof) ev += 1 + 2 * p->cfg.n_iter;
+    }
     // a12: fuse (owned rows; rank 0 gathers the bands for world > 1)
     if (hr_out) CUDA_TRY(launch_finalize(p->sp, b, hr_out, p->W, p->row_lo, p->row_hi, s));
     if (p->cfg.world > 1) {
@@ -783,7 +815,17 @@ flmisr_status flmisr_finish(flmisr_plan_t p, flmisr_report* rep) {
         if (rep->f_trace) std::memcpy(rep->f_trace, p->trace_host, ntrace * sizeof(double));
     }
     Prof& pr = p->prof;
-    if (pr.enabled && p->prof_marks >= 4) {
+    if (pr.enabled && p->prof_mode == 1 && p->prof_marks >= 4) {
+        // marks: 0 start, 1 setup end, 2 loop kernel end, 3 last
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr.ev[0], pr.ev[1]); pr.ms[2] += ms;
+        cudaEventElapsedTime(&ms, pr.ev[1], pr.ev[2]); pr.ms[0] += ms; pr.n[0] += 1;
+        cudaEventElapsedTime(&ms, pr.ev[2], pr.ev[3]); pr.ms[2] += ms;
+        cudaEventElapsedTime(&ms, pr.ev[0], pr.ev[3]); pr.ms[3] += ms; pr.n[3] += 1;
+        pr.n[2] += 1;
+        cudaError_t pe = cudaGetLastError();
+        if (pe != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("profiling events: ") + cudaGetErrorString(pe));
+    } else if (pr.enabled && p->prof_marks >= 4) {
         // marks: 0 start, 1 setup end, 2 init value/grad end, then (curv end, value end) per pass, last
         float ms = 0.f;
         cudaEventElapsedTime(&ms, pr.ev[0], pr.ev[1]); pr.ms[2] += ms;

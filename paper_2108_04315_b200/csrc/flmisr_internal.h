@@ -85,6 +85,7 @@ struct Buffers {
     float* send_top;             // owned top eta rows of the r candidate, for the upper neighbour
     float* send_bot;
     int eta;                     // halo rows per side
+    unsigned* gbar;              // grid-barrier arrival counter of the persistent loop kernel (zeroed per call)
 };
 
 enum Phase : int { PH_ITER = 0, PH_INIT = 1, PH_DEBUG = 2 };
@@ -98,6 +99,8 @@ cudaError_t launch_value_grad_stream(int bw, int pn, const StencilParams& sp, co
                                      cudaStream_t s);
 cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
                                       cudaStream_t s);
+// the whole SCG loop (init pass + n_iter passes) as one cooperative persistent kernel (world == 1)
+cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, cudaStream_t s);
 cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s);  // world > 1
 cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s);   // world > 1
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,

@@ -320,7 +320,9 @@ __global__ void k_scalar_after_curv(Buffers b, int world) {
     scg_after_curv(s, t);
 }
 
-__global__ void k_state_init(ScgState* s, double lam0, double lambda_reg, int n_iter, long long npix, int rules) {
+__global__ void k_state_init(ScgState* s, double lam0, double lambda_reg, int n_iter, long long npix, int rules,
+                             unsigned* gbar) {
+    if (gbar) *gbar = 0u;
     s->f = 0; s->f_new = 0; s->lam = lam0; s->lamb = 0; s->delta = 0; s->pp = 0; s->mu = 0;
     s->alpha = 0; s->beta = 0; s->rr = 0; s->lambda_reg = lambda_reg;
     for (int i = 0; i < 8; ++i) s->dbg[i] = 0;
@@ -477,7 +479,7 @@ cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s
 
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,
                               int rules, cudaStream_t s) {
-    k_state_init<<<1, 1, 0, s>>>(b.st, lam0, lambda_reg, n_iter, npix, rules);
+    k_state_init<<<1, 1, 0, s>>>(b.st, lam0, lambda_reg, n_iter, npix, rules, b.gbar);
     return cudaGetLastError();
 }
 

@@ -487,7 +487,9 @@ struct VG {
         if (t + NST < t0 + nstep) issue(rs_, t + NST);
     }
 
-    __device__ __forceinline__ void run() {
+    // par: the ring's current mbarrier phase parity (all stages advance together); carried across
+    // runs when one kernel streams several phases through the same ring
+    __device__ __forceinline__ void run(uint32_t& par) {
         const float2 z = F2(0.f, 0.f);
         accd = rr = rro = z;
 #pragma unroll
@@ -508,7 +510,6 @@ struct VG {
         // rows t0, t0+1 of x' (the window before the first step) by direct loads
         set_x(0, ld4<BORDER>(rowp(X0, sp, t0), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0), g.col0, sp.W));
         set_x(1, ld4<BORDER>(rowp(X0, sp, t0 + 1), g.col0, sp.W), ld4<BORDER>(rowp(P0, sp, t0 + 1), g.col0, sp.W));
-        uint32_t par = 0;
         for (int t = t0; t < t0 + nstep; t += 3) {
             step<0>(t, par);
             step<1>(t + 1, par);
@@ -526,85 +527,57 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
-#ifdef FLMISR_TIMING
-// diagnostic build only: per-warp (start ns, end ns, smid | border << 16) of the last k_vg_stream launch
-__device__ unsigned long long g_warp_time[3 * 16384];
-__device__ unsigned long long g_cta_time[3 * 2048];   // per CTA: entry, after the CTA reduction, last-CTA finish
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
+
+#ifdef FLMISR_PHASE_NOINLINE   // tuning build: separate register allocation per phase body
+#define FL_PHASE_INLINE __noinline__
+#else
+#define FL_PHASE_INLINE __forceinline__
 #endif
+
+// One value+gradient phase of this CTA's warps: acc = this thread's share of {D, R (gamma-weighted),
+// <r',r'>, <r',r_old>} (summed over the CTA and the grid by the caller).
+template <int BW, int PN>
+__device__ FL_PHASE_INLINE void vg_phase(const StencilParams& sp, const Buffers& b, const Geo& g, const Ring& ring,
+                                         int xcur, int rcur, float alpha, uint32_t& par, double (&acc)[NSLOT]) {
+    const float* X = pick(b.X, xcur);
+    const float* P = pick(b.P, xcur);
+    const float* Ro = pick(b.R, rcur);
+    float* Rn = pick(b.R, rcur ^ 1);
+    float ad = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, a_rr = 0.f, a_rro = 0.f;
+    if (!g.live) {
+    } else if (g.border) {
+        VG<BW, PN, true> v(sp, b, g, ring, X, P, Ro, Rn, alpha);
+        v.run(par);
+        ad = msum(v.accd, g); v0 = msum(v.vb[0], g); v1 = msum(v.vb[1], g); v2 = msum(v.vb[2], g);
+        v3 = msum(v.vb[3], g); a_rr = msum(v.rr, g); a_rro = msum(v.rro, g);
+    } else {
+        VG<BW, PN, false> v(sp, b, g, ring, X, P, Ro, Rn, alpha);
+        v.run(par);
+        ad = msum(v.accd, g); v0 = msum(v.vb[0], g); v1 = msum(v.vb[1], g); v2 = msum(v.vb[2], g);
+        v3 = msum(v.vb[3], g); a_rr = msum(v.rr, g); a_rro = msum(v.rro, g);
+    }
+    acc[0] = ad;
+    acc[1] = sp.gcls[0] * v0 + sp.gcls[1] * v1 + sp.gcls[2] * v2 + sp.gcls[3] * v3;
+    acc[2] = a_rr;
+    acc[3] = a_rro;
+}
 
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter();
-#ifdef FLMISR_TIMING
-    if (threadIdx.x == 0 && blockIdx.x < 2048) g_cta_time[3 * blockIdx.x] = gtimer();
-#endif
     ScgState* st = b.st;
     if (phase != PH_DEBUG && st->done) return;
     const int xcur = st->xcur, rcur = st->rcur;
     const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
     const Geo g = geometry(sp);
-#ifdef FLMISR_TIMING
-    const unsigned long long t_start = gtimer();
-#endif
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
-    {
-        const float* X = pick(b.X, xcur);
-        const float* P = pick(b.P, xcur);
-        const float* Ro = pick(b.R, rcur);
-        float* Rn = pick(b.R, rcur ^ 1);
-        float ad = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, a_rr = 0.f, a_rro = 0.f;
-        if (!g.live) {
-        } else if (g.border) {
-            VG<BW, PN, true> v(sp, b, g, ring, X, P, Ro, Rn, alpha);
-            v.run();
-            ad = msum(v.accd, g); v0 = msum(v.vb[0], g); v1 = msum(v.vb[1], g); v2 = msum(v.vb[2], g);
-            v3 = msum(v.vb[3], g); a_rr = msum(v.rr, g); a_rro = msum(v.rro, g);
-        } else {
-            VG<BW, PN, false> v(sp, b, g, ring, X, P, Ro, Rn, alpha);
-            v.run();
-            ad = msum(v.accd, g); v0 = msum(v.vb[0], g); v1 = msum(v.vb[1], g); v2 = msum(v.vb[2], g);
-            v3 = msum(v.vb[3], g); a_rr = msum(v.rr, g); a_rro = msum(v.rro, g);
-        }
-        acc[0] = ad;
-        acc[1] = sp.gcls[0] * v0 + sp.gcls[1] * v1 + sp.gcls[2] * v2 + sp.gcls[3] * v3;
-        acc[2] = a_rr;
-        acc[3] = a_rro;
-    }
-#ifdef FLMISR_TIMING
-    if (g.lane == 0) {
-        const int gw = blockIdx.x * SWPB + (threadIdx.x >> 5);
-        unsigned smid;
-        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-        if (gw < 16384) {
-            g_warp_time[3 * gw] = t_start;
-            g_warp_time[3 * gw + 1] = gtimer();
-            g_warp_time[3 * gw + 2] = smid | ((unsigned long long)g.border << 16) | ((unsigned long long)g.live << 17) |
-                                      ((unsigned long long)(g.cbase / SSTEP) << 20) |
-                                      ((unsigned long long)(g.r_lo - sp.row_lo) << 36);
-        }
-    }
-#endif
+    uint32_t par = 0;
+    vg_phase<BW, PN>(sp, b, g, ring, xcur, rcur, alpha, par, acc);
     double tot[NSLOT];
-#ifdef FLMISR_TIMING
-    const bool last = reduce_partials(acc, b.part, gridDim.x, blockIdx.x, &st->counter, tot);
-    if (threadIdx.x == 0 && blockIdx.x < 2048) g_cta_time[3 * blockIdx.x + 1] = gtimer();
-    if (last) {
-        finish_scalars<0>(sp, b, tot, phase);
-        if (threadIdx.x == 0 && blockIdx.x < 2048) g_cta_time[3 * blockIdx.x + 2] = gtimer();
-    } else if (threadIdx.x == 0 && blockIdx.x < 2048) {
-        g_cta_time[3 * blockIdx.x + 2] = 0;
-    }
-#else
     if (reduce_partials(acc, b.part, gridDim.x, blockIdx.x, &st->counter, tot)) finish_scalars<0>(sp, b, tot, phase);
-#endif
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -739,7 +712,9 @@ struct UC {
         }
     }
 
-    __device__ __forceinline__ void run() {
+    // par: the ring's current mbarrier phase parity (all stages advance together); carried across
+    // runs when one kernel streams several phases through the same ring
+    __device__ __forceinline__ void run(uint32_t& par) {
         const float2 z = F2(0.f, 0.f);
         cd = pp = mu = z;
 #pragma unroll
@@ -758,7 +733,6 @@ struct UC {
                 ld4<BORDER>(rrowp(b, R0, sp, t0), g.col0, sp.W));
         set_row(1, t0 + 1, ld4<BORDER>(rowp(X0, sp, t0 + 1), g.col0, sp.W),
                 ld4<BORDER>(rowp(P0, sp, t0 + 1), g.col0, sp.W), ld4<BORDER>(rrowp(b, R0, sp, t0 + 1), g.col0, sp.W));
-        uint32_t par = 0;
         for (int t = t0; t < t0 + nstep; t += 3) {
             step<0>(t, par);
             step<1>(t + 1, par);
@@ -767,6 +741,36 @@ struct UC {
         }
     }
 };
+
+// One update+curvature phase of this CTA's warps: acc = {sum rho'' (A p)^2, BTV curvature
+// (gamma-weighted), <p,p>, <p,r>} at the new (x, p).
+template <int BW, int PN>
+__device__ FL_PHASE_INLINE void uc_phase(const StencilParams& sp, const Buffers& b, const Geo& g, const Ring& ring,
+                                         int xcur, int rcur, float au, float be, uint32_t& par,
+                                         double (&acc)[NSLOT]) {
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, c4 = 0.f, a_pp = 0.f, a_mu = 0.f;
+    const float* X = pick(b.X, xcur);
+    const float* P = pick(b.P, xcur);
+    const float* R = pick(b.R, rcur);
+    float* Xn = pick(b.X, xcur ^ 1);
+    float* Pn = pick(b.P, xcur ^ 1);
+    if (!g.live) {
+    } else if (g.border) {
+        UC<BW, PN, true> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
+        u.run(par);
+        c0 = msum(u.cd, g); c1 = msum(u.cb[0], g); c2 = msum(u.cb[1], g); c3 = msum(u.cb[2], g);
+        c4 = msum(u.cb[3], g); a_pp = msum(u.pp, g); a_mu = msum(u.mu, g);
+    } else {
+        UC<BW, PN, false> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
+        u.run(par);
+        c0 = msum(u.cd, g); c1 = msum(u.cb[0], g); c2 = msum(u.cb[1], g); c3 = msum(u.cb[2], g);
+        c4 = msum(u.cb[3], g); a_pp = msum(u.pp, g); a_mu = msum(u.mu, g);
+    }
+    acc[0] = c0;
+    acc[1] = sp.gcls[0] * c1 + sp.gcls[1] * c2 + sp.gcls[2] * c3 + sp.gcls[3] * c4;
+    acc[2] = a_pp;
+    acc[3] = a_mu;
+}
 
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp, Buffers b, int phase) {
@@ -787,35 +791,156 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
-    {
-        float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f, c4 = 0.f, a_pp = 0.f, a_mu = 0.f;
-        const float* X = pick(b.X, xcur);
-        const float* P = pick(b.P, xcur);
-        const float* R = pick(b.R, rcur);
-        float* Xn = pick(b.X, xcur ^ 1);
-        float* Pn = pick(b.P, xcur ^ 1);
-        if (!g.live) {
-        } else if (g.border) {
-            UC<BW, PN, true> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
-            u.run();
-            c0 = msum(u.cd, g); c1 = msum(u.cb[0], g); c2 = msum(u.cb[1], g); c3 = msum(u.cb[2], g);
-            c4 = msum(u.cb[3], g); a_pp = msum(u.pp, g); a_mu = msum(u.mu, g);
-        } else {
-            UC<BW, PN, false> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
-            u.run();
-            c0 = msum(u.cd, g); c1 = msum(u.cb[0], g); c2 = msum(u.cb[1], g); c3 = msum(u.cb[2], g);
-            c4 = msum(u.cb[3], g); a_pp = msum(u.pp, g); a_mu = msum(u.mu, g);
-        }
-        acc[0] = c0;
-        acc[1] = sp.gcls[0] * c1 + sp.gcls[1] * c2 + sp.gcls[2] * c3 + sp.gcls[3] * c4;
-        acc[2] = a_pp;
-        acc[3] = a_mu;
-    }
+    uint32_t par = 0;
+    uc_phase<BW, PN>(sp, b, g, ring, xcur, rcur, au, be, par, acc);
     double tot[NSLOT];
     if (reduce_partials(acc, b.part, gridDim.x, blockIdx.x, &st->counter, tot)) {
         if (threadIdx.x == 0 && phase != PH_DEBUG) st->xcur = xcur ^ 1;
         finish_scalars<1>(sp, b, tot, phase);
     }
+}
+
+// ------------------------------------------------------------------------------------------------
+// The whole SCG loop in one persistent cooperative kernel (world == 1): one CTA per SM streams
+// every phase of Alg. 1 through the same ring; phases are separated by a grid barrier after which
+// EVERY CTA sums the per-CTA slots in the same fixed order and runs the same scalar logic on its own
+// shared-memory copy of the state (bit-identical in all CTAs), so no CTA waits on a serial last-CTA
+// reduction or on kernel teardown and relaunch.  CTA 0 writes the trace and the final state.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+#ifdef FLMISR_TIMING
+// diagnostic build only: per (phase, CTA): CTA work end, arrival, release, scalars done (globaltimer ns)
+__device__ unsigned long long g_loop_time[64 * 256 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define FL_TMARK(ep, k) \
+    if (threadIdx.x == 0 && (ep) < 64 && blockIdx.x < 256) g_loop_time[((ep) * 256 + blockIdx.x) * 4 + (k)] = gtimer();
+#else
+#define FL_TMARK(ep, k)
+#endif
+
+// grid-wide sum of acc over all threads of all CTAs in a fixed order; result in tot (all threads)
+__device__ void grid_sum(const double (&acc)[NSLOT], double* part, unsigned* gbar, unsigned epoch,
+                         double (&tot)[NSLOT]) {
+    __shared__ double sred[32][NSLOT];
+    __shared__ double stot[NSLOT];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int G = gridDim.x;
+    double* slot = part + (size_t)(epoch & 1) * NSLOT * G;   // double-buffered by phase parity
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        const double v = warp_sum(acc[k]);
+        if (lane == 0) sred[warp][k] = v;
+    }
+    __syncthreads();
+    FL_TMARK(epoch, 0)
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) {
+            double v = 0.0;
+            for (int w = 0; w < nw; ++w) v += sred[w][k];
+            slot[(size_t)k * G + blockIdx.x] = v;
+        }
+        __threadfence();   // release: this CTA's phase output (ordered by the barrier above) and slots
+        atomicAdd(gbar, 1u);
+        FL_TMARK(epoch, 1)
+        const unsigned target = (epoch + 1) * (unsigned)G;
+        unsigned long long spins = 0;
+        while (ld_acquire_u32(gbar) < target) {
+            if (++spins > (1ull << 31)) __trap();   // a lost CTA: fail loudly instead of hanging the device
+        }
+        __threadfence();
+        FL_TMARK(epoch, 2)
+    }
+    __syncthreads();
+    // every CTA: slot j of CTA j by thread j, fixed shuffle tree, fixed cross-warp order
+    double loc[NSLOT];
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) loc[k] = 0.0;
+    for (int j = threadIdx.x; j < G; j += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) loc[k] += ld_relaxed_gpu(slot + (size_t)k * G + j);
+    }
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        const double v = warp_sum(loc[k]);
+        if (lane == 0) sred[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NSLOT) {
+        double v = 0.0;
+        for (int w = 0; w < nw; ++w) v += sred[w][threadIdx.x];
+        stot[threadIdx.x] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) tot[k] = stot[k];
+    FL_TMARK(epoch, 3)
+    // the next phase reads other CTAs' generic-proxy stores through the bulk-copy (async) proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int WHICH>
+__device__ __forceinline__ void affine(const StencilParams& sp, double (&t)[NSLOT]) {
+    const double* aff = WHICH == 0 ? sp.aff_vg : sp.aff_uc;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) t[k] = t[k] * aff[k] + aff[NSLOT + k];
+}
+
+template <int BW, int PN>
+__global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_loop(const __grid_constant__ StencilParams sp,
+                                                                const __grid_constant__ Buffers b) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ ScgState S;
+    const Geo g = geometry(sp);
+    Ring ring;
+    ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
+    if (threadIdx.x == 0) S = *b.st;
+    __syncthreads();
+    double* trace = blockIdx.x == 0 ? b.trace : nullptr;
+    uint32_t par = 0;
+    unsigned epoch = 0;
+    double acc[NSLOT], tot[NSLOT];
+    // state fields are read from shared memory through a lane-0 shuffle so the compiler sees them as
+    // warp-uniform: the buffer pointers derived from xcur / rcur then stay in uniform registers and
+    // the bulk copies take them directly (no per-copy register-to-uniform waterfall)
+    auto ui = [](int v) { return __shfl_sync(0xffffffffu, v, 0); };
+    auto uf = [](float v) { return __shfl_sync(0xffffffffu, v, 0); };
+    // pass 0 is the init value+gradient (f0 = J(x0), r0 = -grad J(x0)); every later pass is
+    // [update+curvature if the last step was accepted] + value+gradient.  One call site per phase body.
+    for (int pass = 0; !ui(S.done); ++pass) {
+        if (pass > 0) {
+            if (ui(S.success)) {   // update x, p and the curvature at the new direction
+                uc_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f), par, acc);
+                grid_sum(acc, b.part, b.gbar, epoch++, tot);
+                if (threadIdx.x == 0) {
+                    S.xcur ^= 1;
+                    affine<1>(sp, tot);
+                    scg_after_curv(&S, tot);
+                }
+            } else if (threadIdx.x == 0) {   // rejected step: delta is reused
+                scg_pre_value(&S);
+            }
+            __syncthreads();
+            if (ui(S.done)) break;
+        }
+        vg_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par, acc);
+        grid_sum(acc, b.part, b.gbar, epoch++, tot);
+        if (threadIdx.x == 0) {
+            affine<0>(sp, tot);
+            scg_after_value(&S, tot, trace, pass > 0 ? PH_ITER : PH_INIT);
+        }
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *b.st = S;
 }
 
 bool pdl_enabled() {
@@ -856,11 +981,48 @@ cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers
 #define FL_SCASE(K, BW_, PN_) \
     case BW_ * 10 + PN_: return launch_ring(K<BW_, PN_>, sp.nitems, sp, b, phase, s);
 
+template <typename K>
+cudaError_t launch_loop(K kernel, int nw, const StencilParams& sp, const Buffers& b, cudaStream_t s) {
+    static const void* done[64];
+    static int ndone = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(kernel) ^ (uintptr_t)dev);
+    bool configured = false;
+    for (int i = 0; i < ndone; ++i) configured = configured || done[i] == key;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
+        if (e != cudaSuccess) return e;
+        if (ndone < 64) done[ndone++] = key;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((nw + SWPB - 1) / SWPB);
+    cfg.blockDim = dim3(SWPB * 32);
+    cfg.dynamicSmemBytes = RING_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // every CTA co-resident: the grid barrier cannot deadlock
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, sp, b);
+}
+
 cudaError_t launch_value_grad_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
                                      cudaStream_t s) {
     switch (bw * 10 + pn) {
         FL_SCASE(k_vg_stream, 1, 1) FL_SCASE(k_vg_stream, 1, 2) FL_SCASE(k_vg_stream, 2, 1)
         FL_SCASE(k_vg_stream, 2, 2) FL_SCASE(k_vg_stream, 3, 1) FL_SCASE(k_vg_stream, 3, 2)
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, cudaStream_t s) {
+    switch (bw * 10 + pn) {
+#define FL_LCASE(BW_, PN_) \
+    case BW_ * 10 + PN_: return launch_loop(k_scg_loop<BW_, PN_>, sp.nitems, sp, b, s);
+        FL_LCASE(1, 1) FL_LCASE(1, 2) FL_LCASE(2, 1) FL_LCASE(2, 2) FL_LCASE(3, 1) FL_LCASE(3, 2)
+#undef FL_LCASE
         default: return cudaErrorInvalidValue;
     }
 }
@@ -877,12 +1039,8 @@ cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, c
 }  // namespace flmisr
 
 #ifdef FLMISR_TIMING
-extern "C" int flmisr_debug_warp_timing(unsigned long long* host, int n) {
-    if (n > 3 * 16384) n = 3 * 16384;
-    return (int)cudaMemcpyFromSymbol(host, flmisr::g_warp_time, (size_t)n * sizeof(unsigned long long));
-}
-extern "C" int flmisr_debug_cta_timing(unsigned long long* host, int n) {
-    if (n > 3 * 2048) n = 3 * 2048;
-    return (int)cudaMemcpyFromSymbol(host, flmisr::g_cta_time, (size_t)n * sizeof(unsigned long long));
+extern "C" int flmisr_debug_loop_timing(unsigned long long* host, int n) {
+    if (n > 64 * 256 * 4) n = 64 * 256 * 4;
+    return (int)cudaMemcpyFromSymbol(host, flmisr::g_loop_time, (size_t)n * sizeof(unsigned long long));
 }
 #endif

@@ -70,7 +70,7 @@ def _load():
     lib.flmisr_destroy.argtypes = [vp]
     lib.flmisr_last_error.restype = C.c_char_p
     lib.flmisr_nccl_unique_id.argtypes = [vp]
-    lib.flmisr_plan_info.argtypes = [vp] + [C.POINTER(C.c_int32)] * 5
+    lib.flmisr_plan_info.argtypes = [vp] + [C.POINTER(C.c_int32)] * 6
     lib.flmisr_debug_apply.argtypes = [vp, C.c_int32, vp, vp, vp, vp, C.POINTER(C.c_double)]
     lib.flmisr_band.argtypes = [C.c_int32] * 4 + [C.POINTER(C.c_int32)] * 2
     lib.flmisr_plan_virtual.argtypes = [C.POINTER(Config), C.POINTER(vp)]
@@ -164,9 +164,9 @@ class Plan:
         self._pipes = weakref.WeakSet()   # pipelines driving this plan (destroyed first)
         self._h = C.c_void_p()
         _check((_lib.flmisr_plan_virtual if virtual else _lib.flmisr_plan)(C.byref(cfg), C.byref(self._h)))
-        vals = [C.c_int32() for _ in range(5)]
+        vals = [C.c_int32() for _ in range(6)]
         _check(_lib.flmisr_plan_info(self._h, *[C.byref(v) for v in vals]))
-        self.H, self.W, self.row_lo, self.row_hi, self.fast_path = [v.value for v in vals]
+        self.H, self.W, self.row_lo, self.row_hi, self.fast_path, self.loop_kernel = [v.value for v in vals]
 
     def destroy(self):
         for pipe in list(getattr(self, "_pipes", ())):

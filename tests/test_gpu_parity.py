@@ -196,3 +196,27 @@ def test_tiled_and_streaming_paths_agree(orc, name, monkeypatch):
     g = orc.grad(pb, x.astype(np.float64), y.astype(np.float64))
     for o in outs:
         assert rel(o, -g) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["c1", "strips", "ragged_s"])
+def test_persistent_loop_kernel_matches(orc, name, monkeypatch):
+    """FLMISR_PERSIST=1: the whole SCG loop as one cooperative kernel with a grid barrier per phase and
+    the scalar logic replicated in every CTA.  Same oracle bar; same accept/reject sequence and f trace
+    as the per-phase kernels (the fixed-order sums differ only in their association order)."""
+    lr_h, lr_w, mag, psf, sh, pn, lam, w = CASES[name]
+    truth = synth.phantom(mag * lr_h, mag * lr_w, seed=33)
+    y = synth.detector_stack(truth, mag, sh, 1 / 255, seed=33).astype(np.float32)
+    pl0, pb = make(orc, name, n_iter=20)
+    assert pl0.loop_kernel == 0
+    h0, r0 = pl0.reconstruct(dev(y))
+    monkeypatch.setenv("FLMISR_PERSIST", "1")
+    pl1, _ = make(orc, name, n_iter=20)
+    assert pl1.loop_kernel == 1
+    h1, r1 = pl1.reconstruct(dev(y))
+    h1b, _ = pl1.reconstruct(dev(y))
+    assert torch.equal(h1, h1b)                                   # deterministic
+    xo, tr, st = orc.scg(pb, y.astype(np.float64), 20)
+    assert rel(h1.cpu().numpy(), xo) <= 1e-3
+    np.testing.assert_array_equal(r1["trace"][:, 5], tr[:, 5])
+    np.testing.assert_allclose(r1["trace"][:, 1], r0["trace"][:, 1], rtol=1e-6)
+    assert rel(h1.cpu().numpy(), h0.cpu().numpy()) <= 1e-5

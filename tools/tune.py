@@ -31,7 +31,11 @@ for _ in range(a.reps):
     flush.zero_()
     pl.reconstruct(yd, out=out)
 p = pl.profile(0)
-print(json.dumps({"lib": os.path.basename(flmisr.LIB_PATH), "seg_rows": os.environ.get("FLMISR_SEG_ROWS", "auto"),
-                  "vg_us": 1000 * p["value_grad"]["ms"] / p["value_grad"]["launches"],
-                  "uc_us": 1000 * p["update_curv"]["ms"] / p["update_curv"]["launches"],
-                  "recon_ms": p["reconstruct"]["ms"] / p["reconstruct"]["launches"]}), flush=True)
+out = {"lib": os.path.basename(flmisr.LIB_PATH), "seg_rows": os.environ.get("FLMISR_SEG_ROWS", "auto"),
+       "loop_kernel": pl.loop_kernel, "recon_ms": p["reconstruct"]["ms"] / p["reconstruct"]["launches"]}
+if p["update_curv"]["launches"]:
+    out.update(vg_us=1000 * p["value_grad"]["ms"] / p["value_grad"]["launches"],
+               uc_us=1000 * p["update_curv"]["ms"] / p["update_curv"]["launches"])
+else:
+    out.update(loop_ms=p["value_grad"]["ms"] / p["value_grad"]["launches"])
+print(json.dumps(out), flush=True)
