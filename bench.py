@@ -380,15 +380,36 @@ def run_flmisr(args):
     peak, peak_src = load_peaks()
     vg = prof["value_grad"]
     uc = prof["update_curv"]
-    vg_ms = vg["ms"] / max(vg["launches"], 1)
-    uc_ms = uc["ms"] / max(uc["launches"], 1)
-    achieved = BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(cfg, {}).get("value_grad")
-    launches_per_step = 5 + 2 * n_iter
+            traffic = json.load(f).get(cfg, {})
+    if uc["launches"]:   # per-phase kernels (default): the dominant kernel is value+gradient
+        vg_ms = vg["ms"] / max(vg["launches"], 1)
+        uc_ms = uc["ms"] / max(uc["launches"], 1)
+        roof = {"bound": "hbm", "achieved": BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9, "peak": peak,
+                "unit": "GB/s", "traffic": (traffic or {}).get("value_grad"), "kernel": "k_vg_stream",
+                "algorithmic_bytes_per_launch": BYTES_VALUE_GRAD * npx, "avg_launch_ms": vg_ms,
+                "peak_source": peak_src}
+        kernels = {"value_grad": {"avg_ms": vg_ms, "launches": vg["launches"],
+                                  "gbs": BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9},
+                   "update_curv": {"avg_ms": uc_ms, "launches": uc["launches"],
+                                   "gbs": BYTES_UPDATE_CURV * npx / (uc_ms / 1000.0) / 1e9}}
+    else:                # FLMISR_PERSIST=1: one cooperative kernel runs the whole loop
+        acc_flags = rep["trace"][:, 5]
+        n_vg = len(acc_flags)                      # init + every pass
+        n_uc = int(acc_flags[:-1].sum())           # pass k updates iff pass k-1 was accepted
+        loop_bytes = (BYTES_VALUE_GRAD * n_vg + BYTES_UPDATE_CURV * n_uc) * npx
+        loop_ms = vg["ms"] / max(vg["launches"], 1)
+        roof = {"bound": "hbm", "achieved": loop_bytes / (loop_ms / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
+                "traffic": (traffic or {}).get("scg_loop"), "kernel": "k_scg_loop",
+                "algorithmic_bytes_per_launch": loop_bytes, "avg_launch_ms": loop_ms, "peak_source": peak_src}
+        kernels = {"scg_loop": {"avg_ms": loop_ms, "launches": vg["launches"], "value_grad_phases": n_vg,
+                                "update_curv_phases": n_uc}}
+    roof["frac"] = roof["achieved"] / peak
+    kernels["setup_finalize_ms_per_step"] = prof["setup_finalize"]["ms"] / max(prof["setup_finalize"]["launches"], 1)
+    launches_per_step = 5 + 2 * n_iter if uc["launches"] else 6
     line = {
         "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -401,15 +422,8 @@ def run_flmisr(args):
                    (f"row bands x{world} (NCCL halo + allgather)" if partitioned else f"replicas x{world}")},
         "scg_iters_per_s": value * n_iter,
         "accepted_fraction": float(np.mean(accepted)) / n_iter if n_iter else None,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_value_grad",
-                     "algorithmic_bytes_per_launch": BYTES_VALUE_GRAD * npx, "avg_launch_ms": vg_ms,
-                     "peak_source": peak_src},
-        "kernels": {"value_grad": {"avg_ms": vg_ms, "launches": vg["launches"],
-                                   "gbs": BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9},
-                    "update_curv": {"avg_ms": uc_ms, "launches": uc["launches"],
-                                    "gbs_if_full": BYTES_UPDATE_CURV * npx / (uc_ms / 1000.0) / 1e9 if uc_ms else None},
-                    "setup_finalize_ms_per_step": prof["setup_finalize"]["ms"] / max(prof["setup_finalize"]["launches"], 1)},
+        "roofline": roof,
+        "kernels": kernels,
         "clocks": clocks,
         "e2e": e2e,
         "e2e_serial": e2e_serial,
