@@ -396,7 +396,7 @@ def run_flmisr(args):
                                   "gbs": BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9},
                    "update_curv": {"avg_ms": uc_ms, "launches": uc["launches"],
                                    "gbs": BYTES_UPDATE_CURV * npx / (uc_ms / 1000.0) / 1e9}}
-    else:                # FLMISR_PERSIST=1: one cooperative kernel runs the whole loop
+    else:                # default on one GPU: one cooperative kernel runs the whole loop
         acc_flags = rep["trace"][:, 5]
         n_vg = len(acc_flags)                      # init + every pass
         n_uc = int(acc_flags[:-1].sum())           # pass k updates iff pass k-1 was accepted
@@ -406,7 +406,30 @@ def run_flmisr(args):
                 "traffic": (traffic or {}).get("scg_loop"), "kernel": "k_scg_loop",
                 "algorithmic_bytes_per_launch": loop_bytes, "avg_launch_ms": loop_ms, "peak_source": peak_src}
         kernels = {"scg_loop": {"avg_ms": loop_ms, "launches": vg["launches"], "value_grad_phases": n_vg,
-                                "update_curv_phases": n_uc}}
+                                "update_curv_phases": n_uc,
+                                "avg_phase_us": 1000 * loop_ms / (n_vg + n_uc),
+                                "gbs": loop_bytes / (loop_ms / 1000.0) / 1e9}}
+        # context: the same phases as separate kernels (FLMISR_NO_PERSIST=1), outside the timed region
+        os.environ["FLMISR_NO_PERSIST"] = "1"
+        try:
+            pk = flmisr.Plan(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, n_iter=n_iter,
+                             device=local)
+        finally:
+            del os.environ["FLMISR_NO_PERSIST"]
+        for _ in range(2):
+            pk.reconstruct(y_d, out=out_d)
+        pk.profile(1)
+        for _ in range(3):
+            flush.zero_()
+            pk.reconstruct(y_d, out=out_d)
+        pp = pk.profile(0)
+        pk.destroy()
+        pv = pp["value_grad"]["ms"] / max(pp["value_grad"]["launches"], 1)
+        pu = pp["update_curv"]["ms"] / max(pp["update_curv"]["launches"], 1)
+        kernels["per_phase_kernels"] = {
+            "value_grad": {"avg_ms": pv, "gbs": BYTES_VALUE_GRAD * npx / (pv / 1000.0) / 1e9},
+            "update_curv": {"avg_ms": pu, "gbs": BYTES_UPDATE_CURV * npx / (pu / 1000.0) / 1e9},
+            "note": "FLMISR_NO_PERSIST=1 (per-phase kernels, deferred reduction), 3 reconstructions, not timed"}
     roof["frac"] = roof["achieved"] / peak
     kernels["setup_finalize_ms_per_step"] = prof["setup_finalize"]["ms"] / max(prof["setup_finalize"]["launches"], 1)
     launches_per_step = 5 + 2 * n_iter if uc["launches"] else 6

@@ -407,6 +407,9 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     ip.t0y = (float)(mag * c.shifts[0]);
     ip.t0x = (float)(mag * c.shifts[1]);
     ip.perm = sp.perm = p->stream_path;
+    // streaming kernels on one GPU: per-CTA slots are reduced by every CTA of the next kernel instead of
+    // by the last CTA of the producing one (no serial last-CTA tail)
+    sp.deferred = p->stream_path && c.world == 1 && std::getenv("FLMISR_NO_DEFER") == nullptr;
 
     // ---- device memory ----
     auto cleanup_fail = [&](flmisr_status st) { flmisr_destroy(p); return st; };
@@ -444,14 +447,12 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     b.trace = p->dmem + npart + NSLOT;
     p->gathered = p->dmem + npart + NSLOT + ntrace;
     b.gbar = reinterpret_cast<unsigned*>(p->dmem + nd - 1);
-    {   // opt-in (FLMISR_PERSIST=1): the whole SCG loop as one cooperative kernel (streaming path, one
-        // GPU).  It removes the per-phase kernel boundary and last-CTA reduction (~11 us per phase) but
-        // its single large body loses ~10% of per-phase throughput to register allocation (DESIGN.md
-        // 7.2), so the per-phase kernels stay the default
+    {   // the whole SCG loop as one cooperative kernel (streaming path, one GPU):
+        // removes the per-phase kernel boundary and reduction tail.  FLMISR_NO_PERSIST=1 falls back to
+        // the per-phase kernels (deferred reduction), which bench.py uses for the per-kernel split.
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c.device);
-        const char* pe = std::getenv("FLMISR_PERSIST");
-        p->persist = p->stream_path && world == 1 && !virt && coop && pe && std::atoi(pe) != 0;
+        p->persist = p->stream_path && world == 1 && !virt && coop && std::getenv("FLMISR_NO_PERSIST") == nullptr;
     }
     e = cudaMalloc(&p->st, sizeof(ScgState));
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc state: ") + cudaGetErrorString(e)));
@@ -771,6 +772,8 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
         p->prof_mode = 0;
         if (prof) ev += 1 + 2 * p->cfg.n_iter;
     }
+    // deferred reduction: the last value+gradient kernel's scalar step is still pending
+    if (p->sp.deferred) CUDA_TRY(launch_settle(p->sp, b, s));
     // a12: fuse (owned rows; rank 0 gathers the bands for world > 1)
     if (hr_out) CUDA_TRY(launch_finalize(p->sp, b, hr_out, p->W, p->row_lo, p->row_hi, s));
     if (p->cfg.world > 1) {

@@ -32,7 +32,14 @@ struct ScgState {
     unsigned int counter;        // CTA arrival counter (last-CTA reduction), reset by the last CTA
     int rules;                   // SCG variant bits (flmisr_config.scg_rules): 1 PR+ restart, 2 Netlab scale rules
     double curv;                 // last exact curvature p^T Hess J p (Netlab rules recompute delta from it)
+    // deferred reduction (streaming kernels, world == 1): the kernel that produced per-CTA slots leaves
+    // them pending; the next kernel reduces them in every CTA and applies the scalar step on entry
+    int pend;                    // 0 none, PEND_VG_INIT, PEND_VG_ITER, PEND_UC
+    int pend_n;                  // CTAs (slots) of the producing kernel
+    int seq;                     // producing-kernel counter: slots live in part[(seq & 1) * NSLOT * pend_n ...]
+    int pad2;
 };
+enum Pending : int { PEND_NONE = 0, PEND_VG_INIT = 1, PEND_VG_ITER = 2, PEND_UC = 3 };
 
 struct StencilParams {
     int H, W, pitch;             // global HR size, row pitch (floats) of every HR buffer
@@ -56,6 +63,7 @@ struct StencilParams {
     double gcls[4];              // gamma of BTV class dx+dy = 1..4 (fp64, applied to the CTA sums)
     // affine correction of the raw CTA sums before the scalar logic: tot = raw * aff[k] + aff[4+k]
     double aff_vg[2 * NSLOT], aff_uc[2 * NSLOT];
+    int deferred;                // streaming kernels: deferred reduction (world == 1), see ScgState::pend
 };
 
 // Streaming kernels (flmisr_stream.cu): strips of SCOLS columns per warp, stepping by SSTEP.
@@ -99,6 +107,8 @@ cudaError_t launch_value_grad_stream(int bw, int pn, const StencilParams& sp, co
                                      cudaStream_t s);
 cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, int phase,
                                       cudaStream_t s);
+// deferred mode: apply the last kernel's pending scalar step (one CTA) before the state is read back
+cudaError_t launch_settle(const StencilParams& sp, const Buffers& b, cudaStream_t s);
 // the whole SCG loop (init pass + n_iter passes) as one cooperative persistent kernel (world == 1)
 cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, cudaStream_t s);
 cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s);  // world > 1

@@ -331,6 +331,7 @@ __global__ void k_state_init(ScgState* s, double lam0, double lambda_reg, int n_
     s->xcur = 0; s->rcur = 0; s->accepted = 0; s->converged_at = -1; s->failed_stage = 0; s->failed_iter = -1;
     s->counter = 0;
     s->rules = rules; s->curv = 0;
+    s->pend = 0; s->pend_n = 0; s->seq = 0;
 }
 
 // ------------------------------------------------------------------------------------------------

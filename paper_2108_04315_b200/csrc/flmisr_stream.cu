@@ -528,6 +528,80 @@ __device__ __forceinline__ void pdl_enter() {
 }
 
 
+// ---- deferred reduction (sp.deferred): producers publish per-CTA slots, consumers settle them ----
+// every thread: fixed-order sum over the G slots at slot[k * G + j] (thread j takes slot j, ...)
+__device__ __forceinline__ void slot_sum(const double* slot, int G, double (&tot)[NSLOT]) {
+    __shared__ double sred2[32][NSLOT];
+    __shared__ double stot2[NSLOT];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double loc[NSLOT];
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) loc[k] = 0.0;
+    for (int j = threadIdx.x; j < G; j += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) loc[k] += ld_relaxed_gpu(slot + (size_t)k * G + j);
+    }
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        const double v = warp_sum(loc[k]);
+        if (lane == 0) sred2[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NSLOT) {
+        double v = 0.0;
+        for (int w = 0; w < nw; ++w) v += sred2[w][threadIdx.x];
+        stot2[threadIdx.x] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) tot[k] = stot2[k];
+}
+
+// all threads of a CTA: S <- the global state with the pending scalar step applied (identical in every
+// CTA: same slots, same order, same arithmetic); CTA 0 owns the trace
+__device__ __forceinline__ void settle(const StencilParams& sp, const Buffers& b, ScgState& S) {
+    if (threadIdx.x == 0) S = *b.st;
+    __syncthreads();
+    // warp-uniform copies (lane-0 shuffles) of everything that steers control flow
+    const int pend = __shfl_sync(0xffffffffu, S.pend, 0);
+    if (pend == PEND_NONE) return;
+    const int G = __shfl_sync(0xffffffffu, S.pend_n, 0), seq = __shfl_sync(0xffffffffu, S.seq, 0);
+    double tot[NSLOT];
+    slot_sum(b.part + (size_t)(seq & 1) * NSLOT * G, G, tot);
+    if (threadIdx.x == 0) {
+        double* trace = blockIdx.x == 0 ? b.trace : nullptr;
+        const double* aff = pend == PEND_UC ? sp.aff_uc : sp.aff_vg;
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) tot[k] = tot[k] * aff[k] + aff[NSLOT + k];
+        if (pend == PEND_UC) {
+            S.xcur ^= 1;
+            scg_after_curv(&S, tot);
+        } else {
+            scg_after_value(&S, tot, trace, pend == PEND_VG_INIT ? PH_INIT : PH_ITER);
+        }
+        S.pend = PEND_NONE;
+    }
+    __syncthreads();
+}
+
+// all threads: this CTA's slot of the next sequence number (no atomics, no fence: the consumer is the
+// next kernel, ordered by the kernel boundary)
+__device__ __forceinline__ void publish(const double (&acc)[NSLOT], double* part, int seq) {
+    __shared__ double sred3[32][NSLOT];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        const double v = warp_sum(acc[k]);
+        if (lane == 0) sred3[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NSLOT) {
+        double v = 0.0;
+        for (int w = 0; w < nw; ++w) v += sred3[w][threadIdx.x];
+        part[(size_t)(seq & 1) * NSLOT * gridDim.x + (size_t)threadIdx.x * gridDim.x + blockIdx.x] = v;
+    }
+}
+
 #ifdef FLMISR_PHASE_NOINLINE   // tuning build: separate register allocation per phase body
 #define FL_PHASE_INLINE __noinline__
 #else
@@ -565,17 +639,46 @@ __device__ FL_PHASE_INLINE void vg_phase(const StencilParams& sp, const Buffers&
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ ScgState S;
     pdl_enter();
     ScgState* st = b.st;
-    if (phase != PH_DEBUG && st->done) return;
-    const int xcur = st->xcur, rcur = st->rcur;
-    const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
+    const bool deferred = sp.deferred && phase != PH_DEBUG;
+    int xcur, rcur, seq = 0;
+    float alpha;
+    // every branch condition below goes through a lane-0 shuffle: a condition the compiler cannot
+    // prove warp-uniform makes every later instruction potentially divergent, which forces the bulk
+    // copies into per-lane waterfall loops and the address arithmetic out of the uniform datapath
+    if (deferred) {   // apply the previous kernel's pending scalar step (every CTA, identically)
+        settle(sp, b, S);
+        if (__shfl_sync(0xffffffffu, S.done, 0)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) *st = S;
+            return;
+        }
+        xcur = S.xcur; rcur = S.rcur; alpha = S.alpha_f; seq = S.seq + 1;
+    } else {
+        if (phase != PH_DEBUG && __shfl_sync(0xffffffffu, st->done, 0)) return;
+        xcur = st->xcur; rcur = st->rcur; alpha = st->alpha_f;
+    }
+    // lane-0 shuffles: the compiler sees these as warp-uniform (uniform buffer pointers for the copies)
+    xcur = __shfl_sync(0xffffffffu, xcur, 0);
+    rcur = __shfl_sync(0xffffffffu, rcur, 0);
+    alpha = phase == PH_ITER ? __shfl_sync(0xffffffffu, alpha, 0) : 0.0f;
     const Geo g = geometry(sp);
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
     uint32_t par = 0;
     vg_phase<BW, PN>(sp, b, g, ring, xcur, rcur, alpha, par, acc);
+    if (deferred) {
+        publish(acc, b.part, seq);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            S.pend = phase == PH_INIT ? PEND_VG_INIT : PEND_VG_ITER;
+            S.pend_n = gridDim.x;
+            S.seq = seq;
+            *st = S;
+        }
+        return;
+    }
     double tot[NSLOT];
     if (reduce_partials(acc, b.part, gridDim.x, blockIdx.x, &st->counter, tot)) finish_scalars<0>(sp, b, tot, phase);
 }
@@ -775,29 +878,64 @@ __device__ FL_PHASE_INLINE void uc_phase(const StencilParams& sp, const Buffers&
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ ScgState S;
     pdl_enter();
     ScgState* st = b.st;
-    if (phase != PH_DEBUG) {
-        if (st->done) return;
-        if (!st->success) {   // rejected step: delta is reused, only the scalar pre-value step runs
-            if (sp.world == 1 && blockIdx.x == 0 && threadIdx.x == 0) scg_pre_value(st);
+    const bool deferred = sp.deferred && phase != PH_DEBUG;
+    int xcur, rcur, seq = 0;
+    float au, be;
+    if (deferred) {   // apply the previous kernel's pending scalar step (every CTA, identically)
+        settle(sp, b, S);
+        if (__shfl_sync(0xffffffffu, S.done || !S.success, 0)) {   // finished, or rejected: delta reused
+            if (threadIdx.x == 0 && !S.done) scg_pre_value(&S);
+            if (blockIdx.x == 0 && threadIdx.x == 0) *st = S;
             return;
         }
+        xcur = S.xcur; rcur = S.rcur; au = S.alpha_upd_f; be = S.beta_f; seq = S.seq + 1;
+    } else {
+        if (phase != PH_DEBUG) {
+            if (__shfl_sync(0xffffffffu, st->done, 0)) return;
+            if (!__shfl_sync(0xffffffffu, st->success, 0)) {   // rejected step: delta is reused
+                if (sp.world == 1 && blockIdx.x == 0 && threadIdx.x == 0) scg_pre_value(st);
+                return;
+            }
+        }
+        xcur = st->xcur; rcur = st->rcur;
+        au = phase == PH_DEBUG ? 0.0f : st->alpha_upd_f;
+        be = phase == PH_DEBUG ? 0.0f : st->beta_f;
     }
-    const int xcur = st->xcur, rcur = st->rcur;
-    const float au = (phase == PH_DEBUG) ? 0.0f : st->alpha_upd_f;
-    const float be = (phase == PH_DEBUG) ? 0.0f : st->beta_f;
+    xcur = __shfl_sync(0xffffffffu, xcur, 0);
+    rcur = __shfl_sync(0xffffffffu, rcur, 0);
+    au = __shfl_sync(0xffffffffu, au, 0);
+    be = __shfl_sync(0xffffffffu, be, 0);
     const Geo g = geometry(sp);
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
     uint32_t par = 0;
     uc_phase<BW, PN>(sp, b, g, ring, xcur, rcur, au, be, par, acc);
+    if (deferred) {
+        publish(acc, b.part, seq);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            S.pend = PEND_UC;
+            S.pend_n = gridDim.x;
+            S.seq = seq;
+            *st = S;
+        }
+        return;
+    }
     double tot[NSLOT];
     if (reduce_partials(acc, b.part, gridDim.x, blockIdx.x, &st->counter, tot)) {
         if (threadIdx.x == 0 && phase != PH_DEBUG) st->xcur = xcur ^ 1;
         finish_scalars<1>(sp, b, tot, phase);
     }
+}
+
+__global__ void k_settle(StencilParams sp, Buffers b) {
+    pdl_enter();
+    __shared__ ScgState S;
+    settle(sp, b, S);
+    if (threadIdx.x == 0) *b.st = S;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1015,6 +1153,19 @@ cudaError_t launch_value_grad_stream(int bw, int pn, const StencilParams& sp, co
         FL_SCASE(k_vg_stream, 2, 2) FL_SCASE(k_vg_stream, 3, 1) FL_SCASE(k_vg_stream, 3, 2)
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_settle(const StencilParams& sp, const Buffers& b, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(512);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_settle, sp, b);
 }
 
 cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, cudaStream_t s) {

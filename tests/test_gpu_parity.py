@@ -200,18 +200,19 @@ def test_tiled_and_streaming_paths_agree(orc, name, monkeypatch):
 
 @pytest.mark.parametrize("name", ["c1", "strips", "ragged_s"])
 def test_persistent_loop_kernel_matches(orc, name, monkeypatch):
-    """FLMISR_PERSIST=1: the whole SCG loop as one cooperative kernel with a grid barrier per phase and
-    the scalar logic replicated in every CTA.  Same oracle bar; same accept/reject sequence and f trace
-    as the per-phase kernels (the fixed-order sums differ only in their association order)."""
+    """The default streaming plan runs the whole SCG loop as one cooperative kernel (grid barrier per
+    phase, scalar logic replicated in every CTA); FLMISR_NO_PERSIST=1 runs per-phase kernels with the
+    deferred reduction.  Same oracle bar; same accept/reject sequence and f trace in both modes (the
+    fixed-order sums differ only in their association order)."""
     lr_h, lr_w, mag, psf, sh, pn, lam, w = CASES[name]
     truth = synth.phantom(mag * lr_h, mag * lr_w, seed=33)
     y = synth.detector_stack(truth, mag, sh, 1 / 255, seed=33).astype(np.float32)
-    pl0, pb = make(orc, name, n_iter=20)
+    pl1, pb = make(orc, name, n_iter=20)
+    assert pl1.loop_kernel == 1
+    monkeypatch.setenv("FLMISR_NO_PERSIST", "1")
+    pl0, _ = make(orc, name, n_iter=20)
     assert pl0.loop_kernel == 0
     h0, r0 = pl0.reconstruct(dev(y))
-    monkeypatch.setenv("FLMISR_PERSIST", "1")
-    pl1, _ = make(orc, name, n_iter=20)
-    assert pl1.loop_kernel == 1
     h1, r1 = pl1.reconstruct(dev(y))
     h1b, _ = pl1.reconstruct(dev(y))
     assert torch.equal(h1, h1b)                                   # deterministic
