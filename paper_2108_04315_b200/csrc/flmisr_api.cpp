@@ -312,6 +312,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
                 if (dy || dx) sp.gam[dy * MAXBW + dx] = (float)std::pow(c.btv_alpha, dx + dy);
         for (int cl = 0; cl < 4; ++cl) sp.gcls[cl] = std::pow(c.btv_alpha, cl + 1);
         for (int i = 0; i < MAXBW * MAXBW; ++i) sp.lgam[i] = (float)(c.lambda * (double)sp.gam[i]);
+        for (int cl = 0; cl < 4; ++cl) sp.lgc[cl] = (float)(c.lambda * (double)(float)std::pow(c.btv_alpha, cl + 1));
         // identity affine correction (tiled kernels compute complete values)
         for (int k = 0; k < NSLOT; ++k) {
             sp.aff_vg[k] = 1.0; sp.aff_vg[NSLOT + k] = 0.0;
@@ -619,13 +620,17 @@ flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float
                                  (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w * sizeof(float),
                                  cudaMemcpyDeviceToDevice, s));
     }
+    bool p_zeroed = false;
     if (x0) {
         CUDA_TRY(launch_hr_copy(x0 + (size_t)p->store_lo * p->W, p->W, 0, b.X[0], p->pitch, p->sp.perm, srows, p->W, s));
-    } else {
-        CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s));
+    } else {   // the permuted-layout x0 kernel writes p0 = 0 in the same pass
+        CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s, b.P[0]));
+        p_zeroed = init_x0_zeroes_p(p->ip);
     }
-    CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
-    CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
+    if (!p_zeroed) CUDA_TRY(cudaMemsetAsync(b.P[0], 0, p->hr_bytes, s));
+    // r_old = R[0] only enters the init pass's <r0, r_old>, which the scalar logic ignores; bands still
+    // clear it (their halo logic reads rows of it before the first exchange)
+    if (p->cfg.world > 1) CUDA_TRY(cudaMemsetAsync(b.R[0], 0, p->hr_bytes, s));
     CUDA_TRY(launch_state_init(b, p->cfg.scg_lambda0, p->cfg.lambda, p->cfg.n_iter, (long long)p->H * p->W,
                                p->cfg.scg_rules, s));
     return FLMISR_OK;
@@ -773,7 +778,7 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
         if (prof) ev += 1 + 2 * p->cfg.n_iter;
     }
     // deferred reduction: the last value+gradient kernel's scalar step is still pending
-    if (p->sp.deferred) CUDA_TRY(launch_settle(p->sp, b, s));
+    if (p->sp.deferred && !looped) CUDA_TRY(launch_settle(p->sp, b, s));
     // a12: fuse (owned rows; rank 0 gathers the bands for world > 1)
     if (hr_out) CUDA_TRY(launch_finalize(p->sp, b, hr_out, p->W, p->row_lo, p->row_hi, s));
     if (p->cfg.world > 1) {

@@ -55,6 +55,7 @@ struct StencilParams {
     // streaming (separable-kappa) kernels, flmisr_stream.cu
     float ka[3], kb[3];          // kappa(P,Q) = ka[P+1] * kb[Q+1] (KR <= 1; KR = 0 zero-padded)
     float lgam[MAXBW * MAXBW];   // lambda * gamma(dy,dx)
+    float lgc[4];                // lambda * alpha^c of BTV class c = dx + dy (1..4): 4 distinct weights
     int nstrips, nsegs, seg_rows, wpb;   // 128-column warp strips (step 124), row segments, warps/CTA
     // work items (one warp each): n_int = ni * nseg_i segments of seg_rows rows on the ni interior
     // strips, then ne * nseg_b segments of seg_b rows on the ne edge strips (column 0 / column W-1),
@@ -161,7 +162,9 @@ cudaError_t launch_hr_copy(const float* src, int src_pitch, int src_perm, float*
                            int rows, int W, cudaStream_t s);
 cudaError_t launch_ingest(const IngestParams& ip, const float* lr, float* Y, cudaStream_t s);
 cudaError_t launch_egest(const IngestParams& ip, const float* Yhr, float* lr, cudaStream_t s);   // debug
-cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s);
+// x0 into X (buffer layout); P0 non-null: also zero it in the same pass (returns whether it did)
+cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s, float* P0 = nullptr);
+bool init_x0_zeroes_p(const IngestParams& ip);
 // uint16 detector frames -> fp32 (pipeline input; in and out 16-B aligned)
 cudaError_t launch_u16_to_f32(const uint16_t* in, float* out, long long n, float scale, cudaStream_t s);
 cudaError_t launch_finalize(const StencilParams& sp, const Buffers& b, float* out, int out_pitch, int row_lo,

@@ -513,14 +513,29 @@ __device__ __forceinline__ float bilerp_x0(const IngestParams& ip, const float* 
            fa * (1.f - fc) * __ldg(y + (size_t)ia1 * ip.lr_w + ic0) + fa * fc * __ldg(y + (size_t)ia1 * ip.lr_w + ic1);
 }
 
-__global__ void k_init_x0_perm(IngestParams ip, const float* __restrict__ lr, float* __restrict__ X) {
+// x0 (reading 14) for one group of four columns of one row, in the permuted layout, plus p0 = 0 in the
+// same pass (P0 nullable).  The row interpolation (a0, a1, fa) is shared by the four columns.
+__global__ void k_init_x0_perm(IngestParams ip, const float* __restrict__ lr, float* __restrict__ X,
+                               float* __restrict__ P0) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     const int gy = ip.store_lo + blockIdx.y;
     if (4 * q >= ip.W || gy >= ip.store_hi) return;
-    const int c = 4 * q;
-    *reinterpret_cast<float4*>(X + (size_t)(gy - ip.store_lo) * ip.pitch + c) =
-        make_float4(bilerp_x0(ip, lr, gy, c), bilerp_x0(ip, lr, gy, c + 2), bilerp_x0(ip, lr, gy, c + 1),
-                    bilerp_x0(ip, lr, gy, c + 3));
+    const float a = ((float)gy - ip.t0y) / (float)ip.mag;
+    const float a0 = floorf(a), fa = a - a0;
+    const float* r0 = lr + (size_t)clampi((int)a0, 0, ip.lr_h - 1) * ip.lr_w;
+    const float* r1 = lr + (size_t)clampi((int)a0 + 1, 0, ip.lr_h - 1) * ip.lr_w;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float c = ((float)(4 * q + j) - ip.t0x) / (float)ip.mag;
+        const float c0 = floorf(c), fc = c - c0;
+        const int ic0 = clampi((int)c0, 0, ip.lr_w - 1), ic1 = clampi((int)c0 + 1, 0, ip.lr_w - 1);
+        v[j] = (1.f - fa) * (1.f - fc) * __ldg(r0 + ic0) + (1.f - fa) * fc * __ldg(r0 + ic1) +
+               fa * (1.f - fc) * __ldg(r1 + ic0) + fa * fc * __ldg(r1 + ic1);
+    }
+    const size_t o = (size_t)(gy - ip.store_lo) * ip.pitch + 4 * q;
+    *reinterpret_cast<float4*>(X + o) = make_float4(v[0], v[2], v[1], v[3]);
+    if (P0) *reinterpret_cast<float4*>(P0 + o) = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 __global__ void k_finalize_perm(StencilParams sp, Buffers b, float* __restrict__ out, int out_pitch, int row_lo,
@@ -557,9 +572,10 @@ cudaError_t launch_hr_copy(const float* src, int src_pitch, int src_perm, float*
     k_hr_copy<<<rowgrid(W, rows), 256, 0, s>>>(src, src_pitch, src_perm, dst, dst_pitch, dst_perm, W);
     return cudaGetLastError();
 }
-cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s) {
+bool init_x0_zeroes_p(const IngestParams& ip) { return vec4_ok(ip.perm, ip.W, ip.pitch); }
+cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s, float* P0) {
     if (vec4_ok(ip.perm, ip.W, ip.pitch))
-        k_init_x0_perm<<<rowgrid(ip.W / 4, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X);
+        k_init_x0_perm<<<rowgrid(ip.W / 4, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X, P0);
     else
         k_init_x0<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X);
     return cudaGetLastError();

@@ -406,7 +406,7 @@ struct VG {
 #pragma unroll
                 for (int dx = 0; dx < BW; ++dx) {
                     if (dy == 0 && dx == 0) continue;
-                    const float lg = sp.lgam[dy * MAXBW + dx];
+                    const float lg = sp.lgc[dx + dy - 1];   // 4 distinct class weights (fewer uniform registers)
                     const int cls = dx + dy - 1;
                     const float2 D = F2(XA[sq].y, X4[sq]), E = F2(XB[sq].y, X5[sq]);
                     const float2 pA = dx == 0 ? XA[sq] : (dx == 1 ? XB[sq] : D);
