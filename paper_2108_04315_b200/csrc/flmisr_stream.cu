@@ -987,15 +987,15 @@ __device__ void grid_sum(const double (&acc)[NSLOT], double* part, unsigned* gba
             for (int w = 0; w < nw; ++w) v += sred[w][k];
             slot[(size_t)k * G + blockIdx.x] = v;
         }
-        __threadfence();   // release: this CTA's phase output (ordered by the barrier above) and slots
-        atomicAdd(gbar, 1u);
+        // release-reduction: this CTA's phase output (ordered before it by the barrier above,
+        // cumulativity) and its slots become visible to any CTA that acquires the count
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
         FL_TMARK(epoch, 1)
         const unsigned target = (epoch + 1) * (unsigned)G;
         unsigned long long spins = 0;
         while (ld_acquire_u32(gbar) < target) {
             if (++spins > (1ull << 31)) __trap();   // a lost CTA: fail loudly instead of hanging the device
         }
-        __threadfence();
         FL_TMARK(epoch, 2)
     }
     __syncthreads();
