@@ -38,7 +38,13 @@ WORKLOADS = {
     "C2": "C2: K=4 LR 1024x1024 -> x2 SR 2048x2048 (4.2 MP HR), 50 SCG passes",
     "C3": "C3: K=4 LR 2048x2048 -> x2 SR 4096x4096 (16.8 MP HR), 20 SCG passes",
     "C4": "C4: K=9 LR 2048x2048 -> x3 SR 6144x6144 (37.7 MP HR), 20 SCG passes",
+    "G3": "G3: K=4 LR 2048x2048 at quarter-pixel shifts (general-geometry path) -> x2 4096x4096, 20 SCG passes",
 }
+# general-geometry path (flmisr_general.cu): algorithmic bytes per HR pixel of the two-kernel phases
+# for K = mag^2 frames (LR pixels = HR pixels): residual x,p,y,w 16 + gradient w,x,p,r_old,r_new 20;
+# update x,p,r -> x,p 20 + data curvature x,p,y 12
+BYTES_GEN_VALUE_GRAD = 36
+BYTES_GEN_UPDATE_CURV = 32
 # algorithmic HBM bytes per HR pixel per launch
 BYTES_VALUE_GRAD = 20   # read x, p, Y, r_old; write r_new
 BYTES_UPDATE_CURV = 24  # read x, p, r, Y; write x, p
@@ -110,7 +116,7 @@ _INPUTS = {}
 def make_inputs(cfg: str):
     if cfg not in _INPUTS:
         c = synth.CONFIGS[cfg]
-        y, sh, _ = synth.make_stack(c["lr"], c["mag"], seed=c["seed"])
+        y, sh, _ = synth.make_stack(c["lr"], c["mag"], seed=c["seed"], shifts=c.get("shifts"))
         _INPUTS[cfg] = (y, sh, c)
     return _INPUTS[cfg]
 
@@ -385,17 +391,21 @@ def run_flmisr(args):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(cfg, {})
-    if uc["launches"]:   # per-phase kernels (default): the dominant kernel is value+gradient
+    if uc["launches"]:   # per-phase kernels: the dominant launch is value+gradient
         vg_ms = vg["ms"] / max(vg["launches"], 1)
         uc_ms = uc["ms"] / max(uc["launches"], 1)
-        roof = {"bound": "hbm", "achieved": BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9, "peak": peak,
-                "unit": "GB/s", "traffic": (traffic or {}).get("value_grad"), "kernel": "k_vg_stream",
-                "algorithmic_bytes_per_launch": BYTES_VALUE_GRAD * npx, "avg_launch_ms": vg_ms,
+        general = pl.fast_path == 0
+        bvg = BYTES_GEN_VALUE_GRAD if general else BYTES_VALUE_GRAD
+        buc = BYTES_GEN_UPDATE_CURV if general else BYTES_UPDATE_CURV
+        roof = {"bound": "hbm", "achieved": bvg * npx / (vg_ms / 1000.0) / 1e9, "peak": peak,
+                "unit": "GB/s", "traffic": None if general else (traffic or {}).get("value_grad"),
+                "kernel": "k_gen2_residual + k_gen2_grad" if general else "k_vg_stream",
+                "algorithmic_bytes_per_launch": bvg * npx, "avg_launch_ms": vg_ms,
                 "peak_source": peak_src}
         kernels = {"value_grad": {"avg_ms": vg_ms, "launches": vg["launches"],
-                                  "gbs": BYTES_VALUE_GRAD * npx / (vg_ms / 1000.0) / 1e9},
+                                  "gbs": bvg * npx / (vg_ms / 1000.0) / 1e9},
                    "update_curv": {"avg_ms": uc_ms, "launches": uc["launches"],
-                                   "gbs": BYTES_UPDATE_CURV * npx / (uc_ms / 1000.0) / 1e9}}
+                                   "gbs": buc * npx / (uc_ms / 1000.0) / 1e9}}
     else:                # default on one GPU: one cooperative kernel runs the whole loop
         acc_flags = rep["trace"][:, 5]
         n_vg = len(acc_flags)                      # init + every pass
@@ -470,7 +480,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="flmisr", choices=["flmisr", "reference"])
-    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4"])
+    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4", "G3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned", "stream"],
                     help="N > 1: independent projections per rank (default) or row bands of one projection; "

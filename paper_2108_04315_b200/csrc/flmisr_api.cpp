@@ -434,7 +434,11 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     b.R[0] = p->mem + 5 * fl; b.R[1] = p->mem + 6 * fl;
     const size_t nsblk = p->stream_path ? ((size_t)sp.nitems + sp.wpb - 1) / sp.wpb : 0;
     const long long nlr_px = (long long)K * c.lr_h * c.lr_w, nhr_px = (long long)p->H * p->W;
-    const size_t ngblk = fast ? 0 : std::max<size_t>(gen_blocks(nlr_px), gen_blocks(nhr_px));
+    int gcap = 148;
+    cudaDeviceGetAttribute(&gcap, cudaDevAttrMultiProcessorCount, c.device);
+    gcap *= 8;   // general path: grid-stride CTAs, 8 per SM
+    const size_t ngblk = fast ? 0 : std::max<size_t>(gen_blocks_lr(K, c.lr_h, c.lr_w, gcap),
+                                                     gen_blocks_hr(p->W, p->row_hi - p->row_lo, gcap));
     const size_t ntiles = std::max<size_t>(std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk), ngblk);
     // x2: the persistent loop kernel double-buffers its per-CTA slots by phase parity
     const size_t npart = std::max<size_t>(2 * NSLOT * ntiles, (size_t)NSLOT * world);
@@ -474,8 +478,8 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         GenParams& gp = p->gp;
         gp.k = K; gp.lr_h = c.lr_h; gp.lr_w = c.lr_w; gp.mag = mag;
         gp.R = R; gp.kd = 2 * R + 2;
-        gp.nblk_lr = (int)gen_blocks(nlr_px);
-        gp.nblk_hr = (int)gen_blocks(nhr_px);
+        gp.nblk_lr = (int)gen_blocks_lr(K, c.lr_h, c.lr_w, gcap);
+        gp.nblk_hr = (int)gen_blocks_hr(p->W, p->row_hi - p->row_lo, gcap);
         gp.fy_lo = 0; gp.fx_lo = 0; gp.fy_hi = p->H - 1; gp.fx_hi = p->W - 1;
         const size_t ntap = (size_t)K * gp.kd * gp.kd;
         std::vector<float> taps(ntap);

@@ -11,6 +11,7 @@
 // on LR pixels).  Each pair of passes ends in one last-CTA reduction that feeds the same on-device
 // SCG scalar logic as the fast paths.  Correctness first: one pixel per thread, taps from a small
 // device table; the fast paths carry the performance.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -78,23 +79,49 @@ __device__ __forceinline__ float fwd_sample(const StencilParams& sp, const GenPa
     return z;
 }
 
-// transpose of the clamped strided correlation at HR pixel (vy, vx), from LR-layout weights w
+// transpose of the clamped strided correlation at HR pixel (vy, vx), from LR-layout weights w.
+// Interior pixels: for frame i only the taps with P = vy - s_iy (mod mag) and Q = vx - s_ix (mod mag)
+// reach v (ceil(kd/mag)^2 of the kd^2 taps).  Border pixels also collect the clamped virtual
+// positions v' (clamp(v') = v) through the generic fold loop.
 __device__ float adj_gather(const StencilParams& sp, const GenParams& gp, const float* __restrict__ w, int vy, int vx) {
+    float g = 0.0f;
+    const int mag = gp.mag;
+    if (vy > 0 && vy < sp.H - 1 && vx > 0 && vx < sp.W - 1) {
+        for (int i = 0; i < gp.k; ++i) {
+            const int dyi = vy - gp.sy[i] + gp.R, dxi = vx - gp.sx[i] + gp.R;   // >= 0 for the taps below
+            const int p0 = -gp.R + ((dyi % mag) + mag) % mag;
+            const int q0 = -gp.R + ((dxi % mag) + mag) % mag;
+            const float* wi = w + (size_t)i * gp.lr_h * gp.lr_w;
+            for (int Pp = p0; Pp <= gp.R + 1; Pp += mag) {
+                const int ny = vy - gp.sy[i] - Pp;
+                if (ny < 0) continue;
+                const int a = ny / mag;
+                if (a >= gp.lr_h) continue;
+                for (int Qq = q0; Qq <= gp.R + 1; Qq += mag) {
+                    const int nx = vx - gp.sx[i] - Qq;
+                    if (nx < 0) continue;
+                    const int b = nx / mag;
+                    if (b >= gp.lr_w) continue;
+                    g = fmaf(tapk(gp, i, Pp, Qq), __ldg(wi + (size_t)a * gp.lr_w + b), g);
+                }
+            }
+        }
+        return g;
+    }
     const int ylo = vy == 0 ? gp.fy_lo : vy, yhi = vy == sp.H - 1 ? gp.fy_hi : vy;
     const int xlo = vx == 0 ? gp.fx_lo : vx, xhi = vx == sp.W - 1 ? gp.fx_hi : vx;
-    float g = 0.0f;
     for (int yy = ylo; yy <= yhi; ++yy)
         for (int xx = xlo; xx <= xhi; ++xx)
             for (int i = 0; i < gp.k; ++i)
                 for (int Pp = -gp.R; Pp <= gp.R + 1; ++Pp) {
                     const int ny = yy - gp.sy[i] - Pp;
-                    if (ny < 0 || ny % gp.mag) continue;
-                    const int a = ny / gp.mag;
+                    if (ny < 0 || ny % mag) continue;
+                    const int a = ny / mag;
                     if (a >= gp.lr_h) continue;
                     for (int Qq = -gp.R; Qq <= gp.R + 1; ++Qq) {
                         const int nx = xx - gp.sx[i] - Qq;
-                        if (nx < 0 || nx % gp.mag) continue;
-                        const int b = nx / gp.mag;
+                        if (nx < 0 || nx % mag) continue;
+                        const int b = nx / mag;
                         if (b >= gp.lr_w) continue;
                         g = fmaf(tapk(gp, i, Pp, Qq), __ldg(w + ((size_t)i * gp.lr_h + a) * gp.lr_w + b), g);
                     }
@@ -256,6 +283,305 @@ __global__ void __launch_bounds__(GT) k_gen_curv_data(StencilParams sp, GenParam
     }
 }
 
+// ================================================================================================
+// Tiled general-path kernels (the hot loop).  Same arithmetic as the per-pixel reference kernels
+// above (which stay for the debug entries and the image-border folds), with the operands staged
+// in shared memory: LR tiles of 32 x 8 pixels of one frame read their HR footprint of x' once;
+// HR tiles of 64 x 16 pixels read x' (+ halo 2) and, frame by frame, the LR window of rho' that
+// reaches them.  R = PSF radius (kappa offsets [-R, R+1]); mag is a runtime stride <= 4.
+// ================================================================================================
+constexpr int LTX = 32, LTY = 8;                  // LR tile
+constexpr int HTX = 64, HTY = 16, HH = 2;         // HR tile, BTV halo
+constexpr int MAXMAG = 4;
+
+__device__ __forceinline__ int floordiv(int a, int m) { return a >= 0 ? a / m : -((-a + m - 1) / m); }
+
+// HR footprint of an LR tile of frame i: rows hy0 .. hy0 + nr - 1, cols hx0 .. hx0 + nc - 1 (clamped reads)
+template <int R>
+struct Foot {
+    static constexpr int KD = 2 * R + 2;
+    static constexpr int NR = MAXMAG * (LTY - 1) + KD, NC = MAXMAG * (LTX - 1) + KD;
+};
+
+// stage fma(a, B, A) (or A when B == nullptr) of the footprint into xs (row stride nc)
+__device__ __forceinline__ void load_foot(const StencilParams& sp, const float* __restrict__ A,
+                                          const float* __restrict__ B, float a, int hy0, int hx0, int nr, int nc,
+                                          float* xs) {
+    // 1-D blocks of LTX * LTY threads: warp w takes rows w, w + LTY, ..., its lanes the columns
+    for (int r = (int)(threadIdx.x >> 5); r < nr; r += LTY) {
+        const int u = clampi(hy0 + r, 0, sp.H - 1);
+        const float* ra = A + (size_t)(u - sp.store_lo) * sp.pitch;
+        const float* rb = B ? B + (size_t)(u - sp.store_lo) * sp.pitch : nullptr;
+        for (int c = (int)(threadIdx.x & 31); c < nc; c += LTX) {
+            const int v = clampi(hx0 + c, 0, sp.W - 1);
+            xs[r * nc + c] = rb ? fmaf(a, __ldg(rb + v), __ldg(ra + v)) : __ldg(ra + v);
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ float foot_dot(const float* ks, const float* xs, int nc, int r0, int c0) {
+    constexpr int KD = 2 * R + 2;
+    float z = 0.0f;
+#pragma unroll
+    for (int P = 0; P < KD; ++P)
+#pragma unroll
+        for (int Q = 0; Q < KD; ++Q) z = fmaf(ks[P * KD + Q], xs[(r0 + P) * nc + c0 + Q], z);
+    return z;
+}
+
+// LR tile t of the grid-stride loops: frame, first LR row and column
+__device__ __forceinline__ void lr_tile(const GenParams& gp, int t, int& i, int& a0, int& b0) {
+    const int ntx = (gp.lr_w + LTX - 1) / LTX, nty = (gp.lr_h + LTY - 1) / LTY;
+    i = t / (ntx * nty);
+    const int rem = t - i * ntx * nty, by = rem / ntx;
+    a0 = by * LTY;
+    b0 = (rem - by * ntx) * LTX;
+}
+__device__ __forceinline__ int lr_tiles(const GenParams& gp) {
+    return ((gp.lr_w + LTX - 1) / LTX) * ((gp.lr_h + LTY - 1) / LTY) * gp.k;
+}
+
+template <int PN, int R, int MAG>
+__global__ void __launch_bounds__(LTX * LTY) k_gen2_residual(StencilParams sp, GenParams gp, Buffers b, int phase) {
+    constexpr int KD = 2 * R + 2;
+    constexpr int mag = MAG;   // compile-time stride: divisions and residues become shifts / multiplies
+    __shared__ float xs[Foot<R>::NR * Foot<R>::NC];
+    __shared__ float ks[KD * KD];
+    ScgState* st = b.st;
+    if (phase != PH_DEBUG && st->done) return;
+    const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
+    const float* X = pick(b.X, st->xcur);
+    const float* P = pick(b.P, st->xcur);
+    const int nr = mag * (LTY - 1) + KD, nc = mag * (LTX - 1) + KD;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    float acc[NSLOT] = {0.f, 0.f, 0.f, 0.f};
+    for (int t = blockIdx.x; t < lr_tiles(gp); t += gridDim.x) {   // grid-stride: few CTAs, few partials
+        int i, a0, b0;
+        lr_tile(gp, t, i, a0, b0);
+        __syncthreads();   // the previous tile's footprint is consumed
+        load_foot(sp, X, P, alpha, mag * a0 + gp.sy[i] - R, mag * b0 + gp.sx[i] - R, nr, nc, xs);
+        if (tid < KD * KD) ks[tid] = __ldg(gp.taps + (size_t)i * KD * KD + tid);
+        __syncthreads();
+        const int a = a0 + ty, c = b0 + tx;
+        if (a < gp.lr_h && c < gp.lr_w) {
+            const size_t idx = ((size_t)i * gp.lr_h + a) * gp.lr_w + c;
+            const float e = foot_dot<R>(ks, xs, nc, mag * ty, mag * tx) - __ldg(gp.lr + idx);
+            float v, d1;
+            Pen<PN>::val_d1(e, sp.eps, sp.eps2, v, d1);
+            gp.w[idx] = d1;
+            acc[0] += v;
+        }
+    }
+    block_partials(acc, gp.part_a, gridDim.x, blockIdx.x);
+}
+
+template <int PN, int R, int MAG>
+__global__ void __launch_bounds__(LTX * LTY) k_gen2_curv_data(StencilParams sp, GenParams gp, Buffers b, int phase) {
+    constexpr int KD = 2 * R + 2;
+    constexpr int mag = MAG;
+    __shared__ float xs[Foot<R>::NR * Foot<R>::NC];
+    __shared__ float ps[Foot<R>::NR * Foot<R>::NC];
+    __shared__ float ks[KD * KD];
+    ScgState* st = b.st;
+    if (phase != PH_DEBUG && (st->done || !st->success)) return;
+    const int xcur = st->xcur;
+    const float* Xn = pick(b.X, xcur ^ 1);
+    const float* Pn = pick(b.P, xcur ^ 1);
+    const int nr = mag * (LTY - 1) + KD, nc = mag * (LTX - 1) + KD;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    double accd[NSLOT] = {0.0, 0.0, 0.0, 0.0}, tot[NSLOT];
+    float cd = 0.0f;
+    for (int t = blockIdx.x; t < lr_tiles(gp); t += gridDim.x) {
+        int i, a0, b0;
+        lr_tile(gp, t, i, a0, b0);
+        __syncthreads();
+        const int hy0 = mag * a0 + gp.sy[i] - R, hx0 = mag * b0 + gp.sx[i] - R;
+        load_foot(sp, Xn, nullptr, 0.0f, hy0, hx0, nr, nc, xs);
+        load_foot(sp, Pn, nullptr, 0.0f, hy0, hx0, nr, nc, ps);
+        if (tid < KD * KD) ks[tid] = __ldg(gp.taps + (size_t)i * KD * KD + tid);
+        __syncthreads();
+        const int a = a0 + ty, c = b0 + tx;
+        if (a < gp.lr_h && c < gp.lr_w) {
+            const size_t idx = ((size_t)i * gp.lr_h + a) * gp.lr_w + c;
+            const float e = foot_dot<R>(ks, xs, nc, mag * ty, mag * tx) - __ldg(gp.lr + idx);
+            const float ap = foot_dot<R>(ks, ps, nc, mag * ty, mag * tx);
+            cd = fmaf(Pen<PN>::d2(e, sp.eps2) * ap, ap, cd);
+        }
+    }
+    accd[0] = cd;
+    if (reduce_partials(accd, b.part, gridDim.x, blockIdx.x, &st->counter, tot)) {
+        tot[1] = sum_slot(gp.part_a, 1, gp.nblk_hr);
+        tot[2] = sum_slot(gp.part_a, 2, gp.nblk_hr);
+        tot[3] = sum_slot(gp.part_a, 3, gp.nblk_hr);
+        if (threadIdx.x == 0 && phase != PH_DEBUG) st->xcur = xcur ^ 1;
+        finish_scalars<1>(sp, b, tot, phase);
+    }
+}
+
+// thread t of an HR tile handles column t % HTX of rows t / HTX + {0, 4, 8, 12}
+constexpr int HNT = 256, HRPT = HTY * HTX / HNT;   // 4 pixels per thread
+constexpr int XSC = HTX + 2 * HH;                   // x' tile row stride (halo HH each side)
+
+template <int PN, int R, int MAG>
+__global__ void __launch_bounds__(HNT) k_gen2_grad(StencilParams sp, GenParams gp, Buffers b, int phase) {
+    constexpr int KD = 2 * R + 2;
+    constexpr int WR = HTY + KD + 1, WC = HTX + KD + 1;   // LR window bound for mag >= 1
+    __shared__ float xs[(HTY + 2 * HH) * XSC];
+    __shared__ float ws[WR * WC];
+    ScgState* st = b.st;
+    if (phase != PH_DEBUG && st->done) return;
+    const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
+    const int xcur = st->xcur, rcur = st->rcur;
+    const float* X = pick(b.X, xcur);
+    const float* P = pick(b.P, xcur);
+    const float* Ro = pick(b.R, rcur);
+    float* Rn = pick(b.R, rcur ^ 1);
+    constexpr int mag = MAG;
+    const int tid = threadIdx.x;
+    const int ntx = (sp.W + HTX - 1) / HTX, nty = (sp.row_hi - sp.row_lo + HTY - 1) / HTY;
+    const int cx = tid % HTX, ry = tid / HTX;
+    float acc[NSLOT] = {0.f, 0.f, 0.f, 0.f};   // -, R, <r',r'>, <r',r_old>
+    for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {   // grid-stride over HR tiles
+    const int ty0 = sp.row_lo + (t / ntx) * HTY, tx0 = (t % ntx) * HTX;
+    __syncthreads();   // the previous tile's x' and window are consumed
+    for (int e = tid; e < (HTY + 2 * HH) * XSC; e += HNT) {
+        const int r = e / XSC, c = e - r * XSC;
+        const int u = clampi(ty0 - HH + r, 0, sp.H - 1), v = clampi(tx0 - HH + c, 0, sp.W - 1);
+        const size_t o = (size_t)(u - sp.store_lo) * sp.pitch + v;
+        xs[e] = fmaf(alpha, __ldg(P + o), __ldg(X + o));
+    }
+    float g[HRPT];
+#pragma unroll
+    for (int k = 0; k < HRPT; ++k) g[k] = 0.0f;
+    // data term: rho' of every frame gathered through the residue-class taps (interior pixels)
+    for (int i = 0; i < gp.k; ++i) {
+        const int sy = gp.sy[i], sx = gp.sx[i];
+        const int alo = floordiv(ty0 - sy - (R + 1), mag), ahi = floordiv(ty0 + HTY - 1 - sy + R, mag);
+        const int blo = floordiv(tx0 - sx - (R + 1), mag), bhi = floordiv(tx0 + HTX - 1 - sx + R, mag);
+        const int wr = ahi - alo + 1, wc = bhi - blo + 1;
+        __syncthreads();   // previous frame's window consumed (and x' staged, first time)
+        const float* wi = gp.w + (size_t)i * gp.lr_h * gp.lr_w;
+        for (int e = tid; e < wr * wc; e += HNT) {
+            const int r = e / wc, c = e - r * wc;
+            const int a = alo + r, bb = blo + c;
+            ws[r * WC + c] = (a >= 0 && a < gp.lr_h && bb >= 0 && bb < gp.lr_w) ? __ldg(wi + (size_t)a * gp.lr_w + bb)
+                                                                                 : 0.0f;
+        }
+        __syncthreads();
+        const float* ti = gp.taps + (size_t)i * KD * KD;
+        const int vx = tx0 + cx;
+        const int q0 = ((vx - sx + R) % mag + mag) % mag;   // first Q' (= Q + R) in the residue class
+#pragma unroll
+        for (int k = 0; k < HRPT; ++k) {
+            const int vy = ty0 + ry + 4 * k;
+            const int p0 = ((vy - sy + R) % mag + mag) % mag;
+            float acc = 0.0f;
+            for (int Pp = p0; Pp < KD; Pp += mag) {
+                const int a = (vy - sy - (Pp - R) - alo * mag) / mag;   // window row (exact division)
+                for (int Qq = q0; Qq < KD; Qq += mag) {
+                    const int c = (vx - sx - (Qq - R) - blo * mag) / mag;
+                    acc = fmaf(__ldg(ti + Pp * KD + Qq), ws[a * WC + c], acc);
+                }
+            }
+            g[k] += acc;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < HRPT; ++k) {
+        const int vy = ty0 + ry + 4 * k, vx = tx0 + cx;
+        if (vy >= sp.row_hi || vx >= sp.W) continue;
+        float gd = g[k];
+        if (vy == 0 || vy == sp.H - 1 || vx == 0 || vx == sp.W - 1) gd = adj_gather(sp, gp, gp.w, vy, vx);   // folds
+        const int ly = ry + 4 * k + HH, lx = cx + HH;
+        const float xv = xs[ly * XSC + lx];
+        float gb = 0.0f;
+        for (int o = 0; o < gp.noff; ++o) {   // BTV offset list, valid pairs only (|dx|, dy <= HH)
+            const int dy = gp.offy[o], dx = gp.offx[o];
+            const float gm = gp.ogam[o];
+            if (vy + dy < sp.H && vx + dx >= 0 && vx + dx < sp.W) {
+                float v, d1;
+                charb_val_d1(xv - xs[(ly + dy) * XSC + lx + dx], sp.eps, sp.eps2, v, d1);
+                acc[1] = fmaf(gm, v, acc[1]);
+                gb = fmaf(gm, d1, gb);
+            }
+            if (vy - dy >= 0 && vx - dx >= 0 && vx - dx < sp.W)
+                gb = fmaf(-gm, charb_d1(xs[(ly - dy) * XSC + lx - dx] - xv, sp.eps2), gb);
+        }
+        const float rn = -fmaf(sp.lam, gb, gd);
+        const size_t o = (size_t)(vy - sp.store_lo) * sp.pitch + vx;
+        Rn[o] = rn;
+        acc[2] = fmaf(rn, rn, acc[2]);
+        acc[3] = fmaf(rn, __ldg(Ro + o), acc[3]);
+    }
+    }   // tiles
+    double accd[NSLOT] = {acc[0], acc[1], acc[2], acc[3]}, tot[NSLOT];
+    if (reduce_partials(accd, b.part, gridDim.x, blockIdx.x, &st->counter, tot)) {
+        tot[0] = sum_slot(gp.part_a, 0, gp.nblk_lr);
+        finish_scalars<0>(sp, b, tot, phase);
+    }
+}
+
+template <int PN>
+__global__ void __launch_bounds__(HNT) k_gen2_update(StencilParams sp, GenParams gp, Buffers b, int phase) {
+    __shared__ float xs[(HTY + 2 * HH) * XSC];
+    __shared__ float ps[(HTY + 2 * HH) * XSC];
+    ScgState* st = b.st;
+    if (phase != PH_DEBUG) {
+        if (st->done) return;
+        if (!st->success) {   // rejected step: delta is reused, only the scalar pre-value step runs
+            if (blockIdx.x == 0 && threadIdx.x == 0) scg_pre_value(st);
+            return;
+        }
+    }
+    const int xcur = st->xcur, rcur = st->rcur;
+    const float au = (phase == PH_DEBUG) ? 0.0f : st->alpha_upd_f;
+    const float be = (phase == PH_DEBUG) ? 0.0f : st->beta_f;
+    const float* X = pick(b.X, xcur);
+    const float* P = pick(b.P, xcur);
+    const float* R = pick(b.R, rcur);
+    float* Xn = pick(b.X, xcur ^ 1);
+    float* Pn = pick(b.P, xcur ^ 1);
+    const int tid = threadIdx.x;
+    const int ntx = (sp.W + HTX - 1) / HTX, nty = (sp.row_hi - sp.row_lo + HTY - 1) / HTY;
+    const int cx = tid % HTX, ry = tid / HTX;
+    float acc[NSLOT] = {0.f, 0.f, 0.f, 0.f};   // -, curv BTV, <p,p>, <p,r>
+    for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {   // grid-stride over HR tiles
+    const int ty0 = sp.row_lo + (t / ntx) * HTY, tx0 = (t % ntx) * HTX;
+    __syncthreads();
+    for (int e = tid; e < (HTY + 2 * HH) * XSC; e += HNT) {   // new x, p on the tile + halo
+        const int r = e / XSC, c = e - r * XSC;
+        const int u = clampi(ty0 - HH + r, 0, sp.H - 1), v = clampi(tx0 - HH + c, 0, sp.W - 1);
+        const size_t o = (size_t)(u - sp.store_lo) * sp.pitch + v;
+        const float pv = __ldg(P + o);
+        xs[e] = fmaf(au, pv, __ldg(X + o));
+        ps[e] = fmaf(be, pv, __ldg(R + o));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < HRPT; ++k) {
+        const int uy = ty0 + ry + 4 * k, ux = tx0 + cx;
+        if (uy >= sp.row_hi || ux >= sp.W) continue;
+        const int ly = ry + 4 * k + HH, lx = cx + HH;
+        const float xn = xs[ly * XSC + lx], pn = ps[ly * XSC + lx];
+        const size_t o = (size_t)(uy - sp.store_lo) * sp.pitch + ux;
+        Xn[o] = xn;
+        Pn[o] = pn;
+        acc[2] = fmaf(pn, pn, acc[2]);
+        acc[3] = fmaf(pn, __ldg(R + o), acc[3]);
+        for (int q = 0; q < gp.noff; ++q) {
+            const int dy = gp.offy[q], dx = gp.offx[q];
+            if (uy + dy < sp.H && ux + dx >= 0 && ux + dx < sp.W) {
+                const int j = (ly + dy) * XSC + lx + dx;
+                const float tt = xn - xs[j], dp = pn - ps[j];
+                acc[1] = fmaf(gp.ogam[q] * charb_d2(tt, sp.eps2), dp * dp, acc[1]);
+            }
+        }
+    }
+    }   // tiles
+    block_partials(acc, gp.part_a, gridDim.x, blockIdx.x);
+}
+
 // ---- debug: forward and adjoint on natural-layout HR buffers -------------------------------------
 __global__ void k_gen_forward(StencilParams sp, GenParams gp, const float* __restrict__ x, float* __restrict__ y) {
     const long long n = (long long)gp.k * gp.lr_h * gp.lr_w;
@@ -295,27 +621,57 @@ inline unsigned nblk(long long n) { return (unsigned)((n + GT - 1) / GT); }
 
 }  // namespace
 
+namespace {
+dim3 lr_grid(const GenParams& gp) { return dim3(gp.nblk_lr); }
+dim3 hr_grid(const StencilParams&, const GenParams& gp) { return dim3(gp.nblk_hr); }
+}  // namespace
+
+// grid-stride CTAs of the tiled passes: all tiles, capped at `cap` CTAs (a few waves of the device)
+unsigned gen_blocks_lr(int k, int lr_h, int lr_w, int cap) {
+    const long long n = (long long)((lr_w + LTX - 1) / LTX) * ((lr_h + LTY - 1) / LTY) * k;
+    return (unsigned)std::min<long long>(n, cap);
+}
+unsigned gen_blocks_hr(int W, int rows, int cap) {
+    const long long n = (long long)((W + HTX - 1) / HTX) * ((rows + HTY - 1) / HTY);
+    return (unsigned)std::min<long long>(n, cap);
+}
+
+#define FL_GEN_RM(KERNEL, PN_, R_, GRID, BLOCK)                                                      \
+    switch (gp.mag) {                                                                               \
+        case 1: KERNEL<PN_, R_, 1><<<GRID, BLOCK, 0, s>>>(sp, gp, b, phase); break;                \
+        case 2: KERNEL<PN_, R_, 2><<<GRID, BLOCK, 0, s>>>(sp, gp, b, phase); break;                \
+        case 3: KERNEL<PN_, R_, 3><<<GRID, BLOCK, 0, s>>>(sp, gp, b, phase); break;                \
+        case 4: KERNEL<PN_, R_, 4><<<GRID, BLOCK, 0, s>>>(sp, gp, b, phase); break;                \
+        default: return cudaErrorInvalidValue;                                                      \
+    }
+#define FL_GEN_R(KERNEL, PN_, GRID, BLOCK)                                                            \
+    switch (gp.R) {                                                                                 \
+        case 0: FL_GEN_RM(KERNEL, PN_, 0, GRID, BLOCK) break;                                      \
+        case 1: FL_GEN_RM(KERNEL, PN_, 1, GRID, BLOCK) break;                                      \
+        case 2: FL_GEN_RM(KERNEL, PN_, 2, GRID, BLOCK) break;                                      \
+        default: return cudaErrorInvalidValue;                                                      \
+    }
+
 cudaError_t launch_gen_value_grad(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
                                   int phase, cudaStream_t s) {
-    const long long nlr = (long long)gp.k * gp.lr_h * gp.lr_w, nhr = (long long)sp.H * sp.W;
-    if (pn == 2) k_gen_residual<2><<<nblk(nlr), GT, 0, s>>>(sp, gp, b, phase);
-    else k_gen_residual<1><<<nblk(nlr), GT, 0, s>>>(sp, gp, b, phase);
     (void)bw;   // the general kernels walk the plan's BTV offset list (quadrant or Farsiu)
-    if (pn == 2) k_gen_grad<2><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase);
-    else k_gen_grad<1><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase);
+    const dim3 lb(LTX * LTY);
+    if (pn == 2) { FL_GEN_R(k_gen2_residual, 2, lr_grid(gp), lb) } else { FL_GEN_R(k_gen2_residual, 1, lr_grid(gp), lb) }
+    if (pn == 2) { FL_GEN_R(k_gen2_grad, 2, hr_grid(sp, gp), HNT) } else { FL_GEN_R(k_gen2_grad, 1, hr_grid(sp, gp), HNT) }
     return cudaGetLastError();
 }
 
 cudaError_t launch_gen_update_curv(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
                                    int phase, cudaStream_t s) {
-    const long long nlr = (long long)gp.k * gp.lr_h * gp.lr_w, nhr = (long long)sp.H * sp.W;
     (void)bw;
-    if (pn == 2) k_gen_update<2><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase);
-    else k_gen_update<1><<<nblk(nhr), GT, 0, s>>>(sp, gp, b, phase);
-    if (pn == 2) k_gen_curv_data<2><<<nblk(nlr), GT, 0, s>>>(sp, gp, b, phase);
-    else k_gen_curv_data<1><<<nblk(nlr), GT, 0, s>>>(sp, gp, b, phase);
+    const dim3 lb(LTX * LTY);
+    if (pn == 2) k_gen2_update<2><<<hr_grid(sp, gp), HNT, 0, s>>>(sp, gp, b, phase);
+    else k_gen2_update<1><<<hr_grid(sp, gp), HNT, 0, s>>>(sp, gp, b, phase);
+    if (pn == 2) { FL_GEN_R(k_gen2_curv_data, 2, lr_grid(gp), lb) } else { FL_GEN_R(k_gen2_curv_data, 1, lr_grid(gp), lb) }
     return cudaGetLastError();
 }
+#undef FL_GEN_R
+#undef FL_GEN_RM
 
 cudaError_t launch_gen_forward(const StencilParams& sp, const GenParams& gp, const float* x, float* y, cudaStream_t s) {
     k_gen_forward<<<nblk((long long)gp.k * gp.lr_h * gp.lr_w), GT, 0, s>>>(sp, gp, x, y);

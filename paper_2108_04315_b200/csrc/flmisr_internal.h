@@ -152,6 +152,8 @@ cudaError_t launch_gen_forward(const StencilParams& sp, const GenParams& gp, con
 cudaError_t launch_gen_adjoint(const StencilParams& sp, const GenParams& gp, const float* w, float* g, cudaStream_t s);
 cudaError_t launch_gen_interp(const StencilParams& sp, const GenParams& gp, float* out, int out_pitch, cudaStream_t s);
 unsigned gen_blocks(long long n);
+unsigned gen_blocks_lr(int k, int lr_h, int lr_w, int cap);   // CTAs of the tiled LR-pixel passes
+unsigned gen_blocks_hr(int W, int rows, int cap);             // CTAs of the tiled HR-pixel passes
 
 // Streaming-path column layout: each aligned group of 4 columns is stored as (c0, c2, c1, c3).
 __host__ __device__ __forceinline__ int phys_col(int c, int perm) {

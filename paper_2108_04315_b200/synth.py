@@ -114,10 +114,13 @@ def detector_stack(truth: np.ndarray, mag: int, shifts: np.ndarray, sigma_n: flo
     return out
 
 
-def make_stack(lr: int, mag: int, seed: int, sigma_n: float = 1.0 / 255.0, lr_w: int | None = None):
-    """(stack fp32 k x lr x lr_w, shifts k x 2, truth fp64) for a BASELINE config."""
+def make_stack(lr: int, mag: int, seed: int, sigma_n: float = 1.0 / 255.0, lr_w: int | None = None,
+               shifts=None):
+    """(stack fp32 k x lr x lr_w, shifts k x 2, truth fp64) for a BASELINE config.  Fractional HR
+    phases of `shifts` are sampled at the floor lattice position (inputs only need the workload's
+    shape and statistics; the reconstruction models the given shifts exactly)."""
     lr_w = lr if lr_w is None else lr_w
-    sh = shift_pattern(mag)
+    sh = shift_pattern(mag) if shifts is None else np.asarray(shifts, dtype=np.float64)
     truth = phantom(mag * lr, mag * lr_w, seed)
     y = detector_stack(truth, mag, sh, sigma_n, seed).astype(np.float32)
     return y, sh, truth
@@ -135,4 +138,8 @@ CONFIGS = {
     "C2": dict(lr=1024, mag=2, n_iter=50, seed=2109),
     "C3": dict(lr=2048, mag=2, n_iter=20, seed=2110),
     "C4": dict(lr=2048, mag=3, n_iter=20, seed=2111),
+    # general-geometry path at C3 size: K = 4 frames at quarter-pixel detector
+    # positions (fractional HR phases, a different composed kernel per frame)
+    "G3": dict(lr=2048, mag=2, n_iter=20, seed=2112,
+               shifts=((0.0, 0.0), (0.25, 0.5), (0.5, 0.25), (0.75, 0.75))),
 }
