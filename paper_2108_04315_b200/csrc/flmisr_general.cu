@@ -303,25 +303,43 @@ struct Foot {
     static constexpr int NR = MAXMAG * (LTY - 1) + KD, NC = MAXMAG * (LTX - 1) + KD;
 };
 
-// stage fma(a, B, A) (or A when B == nullptr) of the footprint into xs (row stride nc)
+// stage fma(a, B, A) (or A when B == nullptr) of the footprint into xs (row stride nc).  Fixed trip
+// counts (warp w: rows w, w + LTY, ...; lane: columns lane, lane + 32, ...) so every load of a thread
+// is issued before the first store (the loads are latency-bound, not bandwidth-bound)
+template <int R, int MAG>
 __device__ __forceinline__ void load_foot(const StencilParams& sp, const float* __restrict__ A,
-                                          const float* __restrict__ B, float a, int hy0, int hx0, int nr, int nc,
-                                          float* xs) {
-    // 1-D blocks of LTX * LTY threads: warp w takes rows w, w + LTY, ..., its lanes the columns
-    for (int r = (int)(threadIdx.x >> 5); r < nr; r += LTY) {
+                                          const float* __restrict__ B, float a, int hy0, int hx0, float* xs) {
+    constexpr int KD = 2 * R + 2;
+    constexpr int NR = MAG * (LTY - 1) + KD, NC = MAG * (LTX - 1) + KD;
+    constexpr int NRJ = (NR + LTY - 1) / LTY, NCQ = (NC + 31) / 32;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float v[NRJ][NCQ];
+#pragma unroll
+    for (int j = 0; j < NRJ; ++j) {
+        const int r = w + LTY * j;
         const int u = clampi(hy0 + r, 0, sp.H - 1);
         const float* ra = A + (size_t)(u - sp.store_lo) * sp.pitch;
         const float* rb = B ? B + (size_t)(u - sp.store_lo) * sp.pitch : nullptr;
-        for (int c = (int)(threadIdx.x & 31); c < nc; c += LTX) {
-            const int v = clampi(hx0 + c, 0, sp.W - 1);
-            xs[r * nc + c] = rb ? fmaf(a, __ldg(rb + v), __ldg(ra + v)) : __ldg(ra + v);
+#pragma unroll
+        for (int q = 0; q < NCQ; ++q) {
+            const int c = lane + 32 * q;
+            const int vv = clampi(hx0 + c, 0, sp.W - 1);
+            v[j][q] = (r < NR && c < NC) ? (rb ? fmaf(a, __ldg(rb + vv), __ldg(ra + vv)) : __ldg(ra + vv)) : 0.0f;
         }
     }
+#pragma unroll
+    for (int j = 0; j < NRJ; ++j)
+#pragma unroll
+        for (int q = 0; q < NCQ; ++q) {
+            const int r = w + LTY * j, c = lane + 32 * q;
+            if (r < NR && c < NC) xs[r * NC + c] = v[j][q];
+        }
 }
 
-template <int R>
-__device__ __forceinline__ float foot_dot(const float* ks, const float* xs, int nc, int r0, int c0) {
+template <int R, int MAG>
+__device__ __forceinline__ float foot_dot(const float* ks, const float* xs, int r0, int c0) {
     constexpr int KD = 2 * R + 2;
+    constexpr int nc = MAG * (LTX - 1) + KD;
     float z = 0.0f;
 #pragma unroll
     for (int P = 0; P < KD; ++P)
@@ -353,20 +371,19 @@ __global__ void __launch_bounds__(LTX * LTY) k_gen2_residual(StencilParams sp, G
     const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
     const float* X = pick(b.X, st->xcur);
     const float* P = pick(b.P, st->xcur);
-    const int nr = mag * (LTY - 1) + KD, nc = mag * (LTX - 1) + KD;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     float acc[NSLOT] = {0.f, 0.f, 0.f, 0.f};
     for (int t = blockIdx.x; t < lr_tiles(gp); t += gridDim.x) {   // grid-stride: few CTAs, few partials
         int i, a0, b0;
         lr_tile(gp, t, i, a0, b0);
         __syncthreads();   // the previous tile's footprint is consumed
-        load_foot(sp, X, P, alpha, mag * a0 + gp.sy[i] - R, mag * b0 + gp.sx[i] - R, nr, nc, xs);
+        load_foot<R, MAG>(sp, X, P, alpha, mag * a0 + gp.sy[i] - R, mag * b0 + gp.sx[i] - R, xs);
         if (tid < KD * KD) ks[tid] = __ldg(gp.taps + (size_t)i * KD * KD + tid);
         __syncthreads();
         const int a = a0 + ty, c = b0 + tx;
         if (a < gp.lr_h && c < gp.lr_w) {
             const size_t idx = ((size_t)i * gp.lr_h + a) * gp.lr_w + c;
-            const float e = foot_dot<R>(ks, xs, nc, mag * ty, mag * tx) - __ldg(gp.lr + idx);
+            const float e = foot_dot<R, MAG>(ks, xs, mag * ty, mag * tx) - __ldg(gp.lr + idx);
             float v, d1;
             Pen<PN>::val_d1(e, sp.eps, sp.eps2, v, d1);
             gp.w[idx] = d1;
@@ -388,7 +405,6 @@ __global__ void __launch_bounds__(LTX * LTY) k_gen2_curv_data(StencilParams sp, 
     const int xcur = st->xcur;
     const float* Xn = pick(b.X, xcur ^ 1);
     const float* Pn = pick(b.P, xcur ^ 1);
-    const int nr = mag * (LTY - 1) + KD, nc = mag * (LTX - 1) + KD;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     double accd[NSLOT] = {0.0, 0.0, 0.0, 0.0}, tot[NSLOT];
     float cd = 0.0f;
@@ -397,15 +413,15 @@ __global__ void __launch_bounds__(LTX * LTY) k_gen2_curv_data(StencilParams sp, 
         lr_tile(gp, t, i, a0, b0);
         __syncthreads();
         const int hy0 = mag * a0 + gp.sy[i] - R, hx0 = mag * b0 + gp.sx[i] - R;
-        load_foot(sp, Xn, nullptr, 0.0f, hy0, hx0, nr, nc, xs);
-        load_foot(sp, Pn, nullptr, 0.0f, hy0, hx0, nr, nc, ps);
+        load_foot<R, MAG>(sp, Xn, nullptr, 0.0f, hy0, hx0, xs);
+        load_foot<R, MAG>(sp, Pn, nullptr, 0.0f, hy0, hx0, ps);
         if (tid < KD * KD) ks[tid] = __ldg(gp.taps + (size_t)i * KD * KD + tid);
         __syncthreads();
         const int a = a0 + ty, c = b0 + tx;
         if (a < gp.lr_h && c < gp.lr_w) {
             const size_t idx = ((size_t)i * gp.lr_h + a) * gp.lr_w + c;
-            const float e = foot_dot<R>(ks, xs, nc, mag * ty, mag * tx) - __ldg(gp.lr + idx);
-            const float ap = foot_dot<R>(ks, ps, nc, mag * ty, mag * tx);
+            const float e = foot_dot<R, MAG>(ks, xs, mag * ty, mag * tx) - __ldg(gp.lr + idx);
+            const float ap = foot_dot<R, MAG>(ks, ps, mag * ty, mag * tx);
             cd = fmaf(Pen<PN>::d2(e, sp.eps2) * ap, ap, cd);
         }
     }
@@ -427,8 +443,10 @@ template <int PN, int R, int MAG>
 __global__ void __launch_bounds__(HNT) k_gen2_grad(StencilParams sp, GenParams gp, Buffers b, int phase) {
     constexpr int KD = 2 * R + 2;
     constexpr int WR = HTY + KD + 1, WC = HTX + KD + 1;   // LR window bound for mag >= 1
+    constexpr int FC = 4;                                   // frames per staged chunk
     __shared__ float xs[(HTY + 2 * HH) * XSC];
-    __shared__ float ws[WR * WC];
+    __shared__ float ws[FC][WR * WC];
+    __shared__ float ts[GMAXK * KD * KD];   // every frame's taps
     ScgState* st = b.st;
     if (phase != PH_DEBUG && st->done) return;
     const float alpha = (phase == PH_ITER) ? st->alpha_f : 0.0f;
@@ -439,52 +457,105 @@ __global__ void __launch_bounds__(HNT) k_gen2_grad(StencilParams sp, GenParams g
     float* Rn = pick(b.R, rcur ^ 1);
     constexpr int mag = MAG;
     const int tid = threadIdx.x;
+    for (int e = tid; e < gp.k * KD * KD; e += HNT) ts[e] = __ldg(gp.taps + e);   // ordered by the tile loop's barriers
     const int ntx = (sp.W + HTX - 1) / HTX, nty = (sp.row_hi - sp.row_lo + HTY - 1) / HTY;
     const int cx = tid % HTX, ry = tid / HTX;
     float acc[NSLOT] = {0.f, 0.f, 0.f, 0.f};   // -, R, <r',r'>, <r',r_old>
     for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {   // grid-stride over HR tiles
     const int ty0 = sp.row_lo + (t / ntx) * HTY, tx0 = (t % ntx) * HTX;
-    __syncthreads();   // the previous tile's x' and window are consumed
-    for (int e = tid; e < (HTY + 2 * HH) * XSC; e += HNT) {
-        const int r = e / XSC, c = e - r * XSC;
-        const int u = clampi(ty0 - HH + r, 0, sp.H - 1), v = clampi(tx0 - HH + c, 0, sp.W - 1);
-        const size_t o = (size_t)(u - sp.store_lo) * sp.pitch + v;
-        xs[e] = fmaf(alpha, __ldg(P + o), __ldg(X + o));
+    const bool inner = ty0 >= HH && ty0 + HTY + HH <= sp.H && tx0 >= HH && tx0 + HTX + HH <= sp.W;
+    __syncthreads();   // the previous tile's x' and windows are consumed
+    const int w8 = tid >> 5, lane = tid & 31;
+    {   // x' on the tile + halo: warp w rows w, w + 8, w + 16; lanes columns (every load before any store)
+        constexpr int XR = HTY + 2 * HH, XRJ = (XR + 7) / 8, XCQ = (XSC + 31) / 32;
+        float v[XRJ][XCQ];
+#pragma unroll
+        for (int j = 0; j < XRJ; ++j) {
+            const int r = w8 + 8 * j;
+            const int u = clampi(ty0 - HH + r, 0, sp.H - 1);
+            const size_t ro = (size_t)(u - sp.store_lo) * sp.pitch;
+#pragma unroll
+            for (int q = 0; q < XCQ; ++q) {
+                const int c = lane + 32 * q;
+                const size_t o = ro + clampi(tx0 - HH + c, 0, sp.W - 1);
+                v[j][q] = (r < XR && c < XSC) ? fmaf(alpha, __ldg(P + o), __ldg(X + o)) : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < XRJ; ++j)
+#pragma unroll
+            for (int q = 0; q < XCQ; ++q) {
+                const int r = w8 + 8 * j, c = lane + 32 * q;
+                if (r < XR && c < XSC) xs[r * XSC + c] = v[j][q];
+            }
     }
     float g[HRPT];
 #pragma unroll
     for (int k = 0; k < HRPT; ++k) g[k] = 0.0f;
-    // data term: rho' of every frame gathered through the residue-class taps (interior pixels)
-    for (int i = 0; i < gp.k; ++i) {
-        const int sy = gp.sy[i], sx = gp.sx[i];
-        const int alo = floordiv(ty0 - sy - (R + 1), mag), ahi = floordiv(ty0 + HTY - 1 - sy + R, mag);
-        const int blo = floordiv(tx0 - sx - (R + 1), mag), bhi = floordiv(tx0 + HTX - 1 - sx + R, mag);
-        const int wr = ahi - alo + 1, wc = bhi - blo + 1;
-        __syncthreads();   // previous frame's window consumed (and x' staged, first time)
-        const float* wi = gp.w + (size_t)i * gp.lr_h * gp.lr_w;
-        for (int e = tid; e < wr * wc; e += HNT) {
-            const int r = e / wc, c = e - r * wc;
-            const int a = alo + r, bb = blo + c;
-            ws[r * WC + c] = (a >= 0 && a < gp.lr_h && bb >= 0 && bb < gp.lr_w) ? __ldg(wi + (size_t)a * gp.lr_w + bb)
-                                                                                 : 0.0f;
+    // data term: rho' of every frame gathered through the residue-class taps (interior pixels), the
+    // frames' LR windows staged FC at a time (one barrier pair per chunk)
+    const int vx = tx0 + cx;
+    for (int i0 = 0; i0 < gp.k; i0 += FC) {
+        if (i0 > 0) __syncthreads();   // the previous chunk's windows are consumed
+        constexpr int WRJ = (WR + 7) / 8, WCQ = (WC + 31) / 32;
+#pragma unroll
+        for (int f = 0; f < FC; ++f) {
+            const int i = i0 + f;
+            if (i >= gp.k) break;
+            const int sy = gp.sy[i], sx = gp.sx[i];
+            const int alo = floordiv(ty0 - sy - (R + 1), mag), ahi = floordiv(ty0 + HTY - 1 - sy + R, mag);
+            const int blo = floordiv(tx0 - sx - (R + 1), mag), bhi = floordiv(tx0 + HTX - 1 - sx + R, mag);
+            const int wr = ahi - alo + 1, wc = bhi - blo + 1;
+            const float* wi = gp.w + (size_t)i * gp.lr_h * gp.lr_w;
+            float v[WRJ][WCQ];
+#pragma unroll
+            for (int j = 0; j < WRJ; ++j)
+#pragma unroll
+                for (int q = 0; q < WCQ; ++q) {
+                    const int r = w8 + 8 * j, c = lane + 32 * q;
+                    const int la = alo + r, lb = blo + c;
+                    v[j][q] = (r < wr && c < wc && (unsigned)la < (unsigned)gp.lr_h && (unsigned)lb < (unsigned)gp.lr_w)
+                                  ? __ldg(wi + (size_t)la * gp.lr_w + lb) : 0.0f;
+                }
+#pragma unroll
+            for (int j = 0; j < WRJ; ++j)
+#pragma unroll
+                for (int q = 0; q < WCQ; ++q) {
+                    const int r = w8 + 8 * j, c = lane + 32 * q;
+                    if (r < wr && c < wc) ws[f][r * WC + c] = v[j][q];
+                }
         }
         __syncthreads();
-        const float* ti = gp.taps + (size_t)i * KD * KD;
-        const int vx = tx0 + cx;
-        const int q0 = ((vx - sx + R) % mag + mag) % mag;   // first Q' (= Q + R) in the residue class
 #pragma unroll
-        for (int k = 0; k < HRPT; ++k) {
-            const int vy = ty0 + ry + 4 * k;
-            const int p0 = ((vy - sy + R) % mag + mag) % mag;
-            float acc = 0.0f;
-            for (int Pp = p0; Pp < KD; Pp += mag) {
-                const int a = (vy - sy - (Pp - R) - alo * mag) / mag;   // window row (exact division)
-                for (int Qq = q0; Qq < KD; Qq += mag) {
-                    const int c = (vx - sx - (Qq - R) - blo * mag) / mag;
-                    acc = fmaf(__ldg(ti + Pp * KD + Qq), ws[a * WC + c], acc);
+        for (int f = 0; f < FC; ++f) {
+            const int i = i0 + f;
+            if (i >= gp.k) break;
+            const int sy = gp.sy[i], sx = gp.sx[i];
+            const int alo = floordiv(ty0 - sy - (R + 1), mag), blo = floordiv(tx0 - sx - (R + 1), mag);
+            const float* ti = ts + i * KD * KD;
+            const float* wf = ws[f];
+            const int q0 = ((vx - sx + R) % mag + mag) % mag;   // first Q' (= Q + R) in the residue class
+#pragma unroll
+            for (int k = 0; k < HRPT; ++k) {
+                const int vy = ty0 + ry + 4 * k;
+                const int p0 = ((vy - sy + R) % mag + mag) % mag;
+                float ga = 0.0f;
+                constexpr int NT = (KD + mag - 1) / mag;   // taps per axis in one residue class (at most)
+#pragma unroll
+                for (int jp = 0; jp < NT; ++jp) {
+                    const int Pp = p0 + jp * mag;
+                    if (Pp >= KD) break;
+                    const int a = (vy - sy - (Pp - R) - alo * mag) / mag;   // window row (exact division)
+#pragma unroll
+                    for (int jq = 0; jq < NT; ++jq) {
+                        const int Qq = q0 + jq * mag;
+                        if (Qq >= KD) break;
+                        const int c = (vx - sx - (Qq - R) - blo * mag) / mag;
+                        ga = fmaf(ti[Pp * KD + Qq], wf[a * WC + c], ga);
+                    }
                 }
+                g[k] += ga;
             }
-            g[k] += acc;
         }
     }
 #pragma unroll
@@ -496,17 +567,29 @@ __global__ void __launch_bounds__(HNT) k_gen2_grad(StencilParams sp, GenParams g
         const int ly = ry + 4 * k + HH, lx = cx + HH;
         const float xv = xs[ly * XSC + lx];
         float gb = 0.0f;
-        for (int o = 0; o < gp.noff; ++o) {   // BTV offset list, valid pairs only (|dx|, dy <= HH)
-            const int dy = gp.offy[o], dx = gp.offx[o];
-            const float gm = gp.ogam[o];
-            if (vy + dy < sp.H && vx + dx >= 0 && vx + dx < sp.W) {
+        if (inner) {   // every pair of the tile lies inside the image: no validity tests
+            for (int o = 0; o < gp.noff; ++o) {
+                const int dy = gp.offy[o], dx = gp.offx[o];
+                const float gm = gp.ogam[o];
                 float v, d1;
                 charb_val_d1(xv - xs[(ly + dy) * XSC + lx + dx], sp.eps, sp.eps2, v, d1);
                 acc[1] = fmaf(gm, v, acc[1]);
                 gb = fmaf(gm, d1, gb);
-            }
-            if (vy - dy >= 0 && vx - dx >= 0 && vx - dx < sp.W)
                 gb = fmaf(-gm, charb_d1(xs[(ly - dy) * XSC + lx - dx] - xv, sp.eps2), gb);
+            }
+        } else {
+            for (int o = 0; o < gp.noff; ++o) {   // BTV offset list, valid pairs only (|dx|, dy <= HH)
+                const int dy = gp.offy[o], dx = gp.offx[o];
+                const float gm = gp.ogam[o];
+                if (vy + dy < sp.H && vx + dx >= 0 && vx + dx < sp.W) {
+                    float v, d1;
+                    charb_val_d1(xv - xs[(ly + dy) * XSC + lx + dx], sp.eps, sp.eps2, v, d1);
+                    acc[1] = fmaf(gm, v, acc[1]);
+                    gb = fmaf(gm, d1, gb);
+                }
+                if (vy - dy >= 0 && vx - dx >= 0 && vx - dx < sp.W)
+                    gb = fmaf(-gm, charb_d1(xs[(ly - dy) * XSC + lx - dx] - xv, sp.eps2), gb);
+            }
         }
         const float rn = -fmaf(sp.lam, gb, gd);
         const size_t o = (size_t)(vy - sp.store_lo) * sp.pitch + vx;
@@ -549,6 +632,7 @@ __global__ void __launch_bounds__(HNT) k_gen2_update(StencilParams sp, GenParams
     for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {   // grid-stride over HR tiles
     const int ty0 = sp.row_lo + (t / ntx) * HTY, tx0 = (t % ntx) * HTX;
     __syncthreads();
+#pragma unroll
     for (int e = tid; e < (HTY + 2 * HH) * XSC; e += HNT) {   // new x, p on the tile + halo
         const int r = e / XSC, c = e - r * XSC;
         const int u = clampi(ty0 - HH + r, 0, sp.H - 1), v = clampi(tx0 - HH + c, 0, sp.W - 1);
