@@ -56,7 +56,7 @@ typedef struct {
     double btv_alpha;    /* 0 < alpha < 1, gamma(d) = alpha^(dx+dy) (Eq. prior; 0.4 at P:271)   */
     int32_t btv_window;  /* w in [1, 3]: offsets dx, dy in [0, w-1] (Eq. prior, reading 6/7)   */
     int32_t n_iter;      /* SCG loop passes incl. rejected ones (20 at P:271)      */
-    double scg_sigma0;   /* Moller sigma0; unused: curvature is exact (reading 16)      */
+    double scg_sigma0;   /* Moller sigma0 of the FD curvature probe (curv_mode = 1)      */
     double scg_lambda0;  /* Moller initial scale lambda_1 > 0; 1e-6                      */
     int32_t rank, world; /* row band `rank` of `world` partitions; world = 1: no NCCL    */
     const void* nccl_unique_id; /* host, 128-byte ncclUniqueId (same on all ranks) or NULL if world == 1 */
@@ -65,6 +65,9 @@ typedef struct {
     int32_t btv_offsets; /* 0: the paper's quadrant dx, dy in [0, w-1] (reading 6);
                             1: Farsiu's set dy = m in [0, w-1], dx = l in [-(w-1), w-1], l + m >= 0,
                             gamma = alpha^(|l|+m) (the [BTV] citation); general path, world 1 */
+    int32_t curv_mode;   /* 0: exact curvature p^T Hess J p (reading 16); 1: the paper's finite-difference
+                            probe sigma = scg_sigma0 / |p|, delta = p^T (grad J(x + sigma p) - grad J(x))
+                            / sigma, both gradients in fp64 (general path, world 1)     */
     int32_t scg_rules;   /* bit mask: 1 = PR+ restart (beta <- max(beta, 0)); 2 = Netlab scale
                             rules (delta = curv + lam |p|^2 each pass; lam x4 at Delta < 0.25, x1/2 at
                             Delta > 0.75, bounded to [1e-15, 1e100]); 0 = Moller literal (reading 11) */

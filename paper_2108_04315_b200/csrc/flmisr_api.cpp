@@ -192,6 +192,11 @@ flmisr_status validate(const flmisr_config* c, bool virt) {
     if (c->btv_offsets != 0 && c->btv_offsets != 1)
         return fail(FLMISR_ERR_CONFIG, "btv_offsets must be 0 (quadrant, P:136) or 1 (Farsiu)");
     if (c->scg_rules < 0 || c->scg_rules > 3) return fail(FLMISR_ERR_CONFIG, "scg_rules must be in [0, 3]");
+    if (c->curv_mode != 0 && c->curv_mode != 1) return fail(FLMISR_ERR_CONFIG, "curv_mode must be 0 (exact) or 1 (FD)");
+    if (c->curv_mode == 1 && !(c->scg_sigma0 > 0.0 && std::isfinite(c->scg_sigma0)))
+        return fail(FLMISR_ERR_CONFIG, "curv_mode = 1 needs scg_sigma0 > 0 (S:362)");
+    if (c->curv_mode == 1 && c->world > 1)
+        return fail(FLMISR_ERR_CONFIG, "the finite-difference curvature (curv_mode = 1) runs on the general path: world must be 1");
     if (c->btv_offsets == 1 && c->world > 1)
         return fail(FLMISR_ERR_CONFIG, "Farsiu BTV offsets (btv_offsets = 1) run on the general path: world must be 1");
     return FLMISR_OK;
@@ -231,7 +236,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         if (frame_of_phase[ph] >= 0) fast = false;
         else frame_of_phase[ph] = i;
     }
-    if (std::getenv("FLMISR_FORCE_GENERAL") || c.btv_offsets == 1) fast = false;
+    if (std::getenv("FLMISR_FORCE_GENERAL") || c.btv_offsets == 1 || c.curv_mode == 1) fast = false;
     if (!fast && c.world > 1)
         return fail(FLMISR_ERR_CONFIG,
                     "row-band partitioning (world > 1) needs the polyphase fast path (K = mag^2 frames with distinct "
@@ -505,7 +510,10 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
                 gp.ogam[gp.noff] = (float)std::pow(c.btv_alpha, std::abs(dx) + dy);
                 ++gp.noff;
             }
-        const size_t gbytes = ntap * sizeof(float) + 2 * (size_t)nlr_px * sizeof(float);
+        gp.fd = c.curv_mode == 1;
+        gp.sigma0 = c.scg_sigma0;
+        const size_t gbytes = ntap * sizeof(float) + 2 * (size_t)nlr_px * sizeof(float) +
+                              (gp.fd ? (size_t)nlr_px * sizeof(double) + sizeof(double) : 0);
         e = cudaMalloc(&p->gmem, gbytes);
         if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc general-path buffers"));
         e = cudaMalloc(&p->gpart, (size_t)NSLOT * ngblk * sizeof(double));
@@ -514,6 +522,11 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         gp.taps = p->gmem;
         gp.lr = p->gmem + ntap;
         gp.w = p->gmem + ntap + nlr_px;
+        gp.wd = nullptr;
+        if (gp.fd) {   // 8-byte aligned after the fp32 arrays
+            const uintptr_t end = reinterpret_cast<uintptr_t>(p->gmem + ntap + 2 * nlr_px);
+            gp.wd = reinterpret_cast<double*>((end + 7) / 8 * 8);
+        }
         gp.part_a = p->gpart;
     }
 

@@ -666,6 +666,124 @@ __global__ void __launch_bounds__(HNT) k_gen2_update(StencilParams sp, GenParams
     block_partials(acc, gp.part_a, gridDim.x, blockIdx.x);
 }
 
+// ================================================================================================
+// Paper-literal finite-difference curvature (NEXT-4, Alg. 1 lines 6-11):
+//   sigma = sigma0 / |p|,  delta = p^T (grad J(x + sigma p) - grad J(x)) / sigma
+// with both gradients evaluated per pixel in fp64 from the fp32 iterate (in fp32 the probe
+// displacement sigma p is below one ulp of x, reading 16).  Replaces the data-curvature pass.
+// ================================================================================================
+__device__ __forceinline__ double fd_rho1(int pn, double eps, double t) {
+    return pn == 2 ? 2.0 * t : t / sqrt(fma(t, t, eps * eps));
+}
+__device__ __forceinline__ double fd_psi1(double eps, double t) { return t / sqrt(fma(t, t, eps * eps)); }
+
+// sigma of this pass from the update pass's per-CTA <p,p> slots (same fixed order in every CTA)
+__device__ double fd_sigma(const GenParams& gp) {
+    __shared__ double s_sig;
+    if (threadIdx.x == 0) {
+        double pp = 0.0;
+        for (int j = 0; j < gp.nblk_hr; ++j) pp += __ldcg(gp.part_a + (size_t)2 * gp.nblk_hr + j);
+        s_sig = gp.sigma0 / sqrt(pp);
+    }
+    __syncthreads();
+    return s_sig;
+}
+
+__device__ double fd_fwd(const StencilParams& sp, const GenParams& gp, const float* X, const float* P, double sig,
+                         int i, int a, int b) {
+    const int by = gp.mag * a + gp.sy[i], bx = gp.mag * b + gp.sx[i];
+    double z = 0.0;
+    for (int Pp = -gp.R; Pp <= gp.R + 1; ++Pp) {
+        const int u = clampi(by + Pp, 0, sp.H - 1);
+        for (int Qq = -gp.R; Qq <= gp.R + 1; ++Qq) {
+            const size_t o = (size_t)(u - sp.store_lo) * sp.pitch + clampi(bx + Qq, 0, sp.W - 1);
+            z = fma((double)tapk(gp, i, Pp, Qq), fma(sig, (double)__ldg(P + o), (double)__ldg(X + o)), z);
+        }
+    }
+    return z;
+}
+
+template <int PN>
+__global__ void __launch_bounds__(GT) k_gen_fd_residual(StencilParams sp, GenParams gp, Buffers b, int phase) {
+    ScgState* st = b.st;
+    if (phase != PH_DEBUG && (st->done || !st->success)) return;
+    const int xcur = st->xcur;
+    const float* Xn = pick(b.X, xcur ^ 1);
+    const float* Pn = pick(b.P, xcur ^ 1);
+    const double sig = fd_sigma(gp);
+    const long long n = (long long)gp.k * gp.lr_h * gp.lr_w;
+    const long long idx = (long long)blockIdx.x * GT + threadIdx.x;
+    if (idx >= n) return;
+    const int i = (int)(idx / ((long long)gp.lr_h * gp.lr_w));
+    const int rem = (int)(idx - (long long)i * gp.lr_h * gp.lr_w);
+    const int a = rem / gp.lr_w, c = rem - a * gp.lr_w;
+    const double y = (double)__ldg(gp.lr + idx);
+    const double e1 = fd_fwd(sp, gp, Xn, Pn, 0.0, i, a, c) - y;
+    const double e2 = fd_fwd(sp, gp, Xn, Pn, sig, i, a, c) - y;
+    gp.wd[idx] = fd_rho1(PN, (double)sp.eps, e2) - fd_rho1(PN, (double)sp.eps, e1);
+}
+
+template <int PN>
+__global__ void __launch_bounds__(GT) k_gen_fd_grad(StencilParams sp, GenParams gp, Buffers b, int phase) {
+    ScgState* st = b.st;
+    if (phase != PH_DEBUG && (st->done || !st->success)) return;
+    const int xcur = st->xcur;
+    const float* Xn = pick(b.X, xcur ^ 1);
+    const float* Pn = pick(b.P, xcur ^ 1);
+    const double sig = fd_sigma(gp), eps = sp.eps;
+    double accd[NSLOT] = {0.0, 0.0, 0.0, 0.0}, tot[NSLOT];
+    const long long idx = (long long)blockIdx.x * GT + threadIdx.x;
+    if (idx < (long long)sp.H * sp.W) {
+        const int vy = (int)(idx / sp.W), vx = (int)(idx - (long long)vy * sp.W);
+        // data term: transpose of the clamped correlation applied to rho'(e2) - rho'(e1), in fp64
+        const int ylo = vy == 0 ? gp.fy_lo : vy, yhi = vy == sp.H - 1 ? gp.fy_hi : vy;
+        const int xlo = vx == 0 ? gp.fx_lo : vx, xhi = vx == sp.W - 1 ? gp.fx_hi : vx;
+        double gd = 0.0;
+        for (int yy = ylo; yy <= yhi; ++yy)
+            for (int xx = xlo; xx <= xhi; ++xx)
+                for (int i = 0; i < gp.k; ++i)
+                    for (int Pp = -gp.R; Pp <= gp.R + 1; ++Pp) {
+                        const int ny = yy - gp.sy[i] - Pp;
+                        if (ny < 0 || ny % gp.mag) continue;
+                        const int a = ny / gp.mag;
+                        if (a >= gp.lr_h) continue;
+                        for (int Qq = -gp.R; Qq <= gp.R + 1; ++Qq) {
+                            const int nx = xx - gp.sx[i] - Qq;
+                            if (nx < 0 || nx % gp.mag) continue;
+                            const int bb = nx / gp.mag;
+                            if (bb >= gp.lr_w) continue;
+                            gd = fma((double)tapk(gp, i, Pp, Qq), gp.wd[((size_t)i * gp.lr_h + a) * gp.lr_w + bb], gd);
+                        }
+                    }
+        // BTV: psi'(D x2) - psi'(D x1) per valid pair, x2 = x + sigma p
+        auto X1 = [&](int y, int x) { return (double)__ldg(Xn + (size_t)(y - sp.store_lo) * sp.pitch + x); };
+        auto X2 = [&](int y, int x) {
+            const size_t o = (size_t)(y - sp.store_lo) * sp.pitch + x;
+            return fma(sig, (double)__ldg(Pn + o), (double)__ldg(Xn + o));
+        };
+        double gb = 0.0;
+        const double x1 = X1(vy, vx), x2 = X2(vy, vx);
+        for (int o = 0; o < gp.noff; ++o) {
+            const int dy = gp.offy[o], dx = gp.offx[o];
+            const double gm = (double)gp.ogam[o];
+            if (vy + dy < sp.H && vx + dx >= 0 && vx + dx < sp.W)
+                gb += gm * (fd_psi1(eps, x2 - X2(vy + dy, vx + dx)) - fd_psi1(eps, x1 - X1(vy + dy, vx + dx)));
+            if (vy - dy >= 0 && vx - dx >= 0 && vx - dx < sp.W)
+                gb -= gm * (fd_psi1(eps, X2(vy - dy, vx - dx) - x2) - fd_psi1(eps, X1(vy - dy, vx - dx) - x1));
+        }
+        const double pv = (double)__ldg(Pn + (size_t)(vy - sp.store_lo) * sp.pitch + vx);
+        accd[0] = pv * (gd + (double)sp.lam * gb);
+    }
+    if (reduce_partials(accd, b.part, gridDim.x, blockIdx.x, &st->counter, tot)) {
+        tot[0] = tot[0] / sig;   // delta = p^T (grad J(x + sigma p) - grad J(x)) / sigma (BTV included)
+        tot[1] = 0.0;
+        tot[2] = sum_slot(gp.part_a, 2, gp.nblk_hr);
+        tot[3] = sum_slot(gp.part_a, 3, gp.nblk_hr);
+        if (threadIdx.x == 0 && phase != PH_DEBUG) st->xcur = xcur ^ 1;
+        finish_scalars<1>(sp, b, tot, phase);
+    }
+}
+
 // ---- debug: forward and adjoint on natural-layout HR buffers -------------------------------------
 __global__ void k_gen_forward(StencilParams sp, GenParams gp, const float* __restrict__ x, float* __restrict__ y) {
     const long long n = (long long)gp.k * gp.lr_h * gp.lr_w;
@@ -751,6 +869,17 @@ cudaError_t launch_gen_update_curv(int bw, int pn, const StencilParams& sp, cons
     const dim3 lb(LTX * LTY);
     if (pn == 2) k_gen2_update<2><<<hr_grid(sp, gp), HNT, 0, s>>>(sp, gp, b, phase);
     else k_gen2_update<1><<<hr_grid(sp, gp), HNT, 0, s>>>(sp, gp, b, phase);
+    if (gp.fd) {   // paper-literal finite-difference curvature in fp64 instead of the exact data curvature
+        const unsigned nl = nblk((long long)gp.k * gp.lr_h * gp.lr_w), nh = nblk((long long)sp.H * sp.W);
+        if (pn == 2) {
+            k_gen_fd_residual<2><<<nl, GT, 0, s>>>(sp, gp, b, phase);
+            k_gen_fd_grad<2><<<nh, GT, 0, s>>>(sp, gp, b, phase);
+        } else {
+            k_gen_fd_residual<1><<<nl, GT, 0, s>>>(sp, gp, b, phase);
+            k_gen_fd_grad<1><<<nh, GT, 0, s>>>(sp, gp, b, phase);
+        }
+        return cudaGetLastError();
+    }
     if (pn == 2) { FL_GEN_R(k_gen2_curv_data, 2, lr_grid(gp), lb) } else { FL_GEN_R(k_gen2_curv_data, 1, lr_grid(gp), lb) }
     return cudaGetLastError();
 }

@@ -140,6 +140,9 @@ struct GenParams {
     double* part_a;              // NSLOT x max(nblk) partials of the first pass of each pair
     int sy[GMAXK], sx[GMAXK];    // integer HR phase floor(mag * shift_i)
     int integer_phase[GMAXK];    // 1: mag * shift_i is integral (interpolation fusion inserts the frame)
+    int fd;                      // 1: paper-literal FD curvature (NEXT-4) instead of the exact data curvature
+    double sigma0;               // FD probe: sigma = sigma0 / |p|
+    double* wd;                  // FD: rho'(e(x + sigma p)) - rho'(e(x)) per LR pixel (fp64)
     int noff;                    // BTV offsets d = (offy, offx), offy >= 0 (quadrant or Farsiu set)
     int offy[GMAXOFF], offx[GMAXOFF];
     float ogam[GMAXOFF];         // gamma(d)

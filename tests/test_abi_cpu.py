@@ -53,6 +53,9 @@ def cfg(**kw):
     (dict(k=65, shifts=np.zeros((65, 2))), "k <= 64"),
     (dict(btv_offsets=2), "btv_offsets"),
     (dict(scg_rules=4), "scg_rules"),
+    (dict(curv_mode=2), "curv_mode"),
+    (dict(curv_mode=1, scg_sigma0=0.0), "scg_sigma0"),
+    (dict(curv_mode=1, world=2, rank=0, nccl_id=b"\0" * 128), "world must be 1"),
     (dict(btv_offsets=1, world=2, rank=0, nccl_id=b"\0" * 128), "world must be 1"),
 ])
 def test_config_errors_raised_before_gpu_work(fl, kw, msg):
