@@ -442,8 +442,9 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     int gcap = 148;
     cudaDeviceGetAttribute(&gcap, cudaDevAttrMultiProcessorCount, c.device);
     gcap *= 8;   // general path: grid-stride CTAs, 8 per SM
-    const size_t ngblk = fast ? 0 : std::max<size_t>(gen_blocks_lr(K, c.lr_h, c.lr_w, gcap),
-                                                     gen_blocks_hr(p->W, p->row_hi - p->row_lo, gcap));
+    const size_t ngblk = fast ? 0 : std::max<size_t>(std::max<size_t>(gen_blocks_lr(K, c.lr_h, c.lr_w, gcap),
+                                                                       gen_blocks_hr(p->W, p->row_hi - p->row_lo, gcap)),
+                                                     gen3_blocks(p->W, p->H, gcap));
     const size_t ntiles = std::max<size_t>(std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk), ngblk);
     // x2: the persistent loop kernel double-buffers its per-CTA slots by phase parity
     const size_t npart = std::max<size_t>(2 * NSLOT * ntiles, (size_t)NSLOT * world);
@@ -510,6 +511,30 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
                 gp.ogam[gp.noff] = (float)std::pow(c.btv_alpha, std::abs(dx) + dy);
                 ++gp.noff;
             }
+        // fused tiled kernels (flmisr_general.cu, k_gen3_*): every integer phase in [-(R+1), mag-1+R] on
+        // both axes keeps each tile's LR windows and their clamp folds inside the staged halo
+        {
+            bool ok = gen3_smem(R, mag, K) <= (size_t)200 * 1024 && std::getenv("FLMISR_GEN2") == nullptr;
+            for (int i = 0; i < K; ++i)
+                ok = ok && gp.sy[i] >= -(R + 1) && gp.sy[i] <= mag - 1 + R && gp.sx[i] >= -(R + 1) &&
+                     gp.sx[i] <= mag - 1 + R;
+            gp.fused = ok ? 1 : 0;
+            gp.btvq = (c.btv_offsets == 0 && c.btv_window == 3) ? 3 : 0;
+            if (gp.fused) {   // hoisted constants of the fused kernels (as on the streaming path)
+                const double eps = c.l1_eps;
+                double npairs_g = 0.0;   // sum over the offset list of gamma_d (as fp32) x valid pairs
+                for (int o = 0; o < gp.noff; ++o)
+                    npairs_g += (double)gp.ogam[o] * (double)std::max(0, p->H - gp.offy[o]) *
+                                (double)std::max(0, p->W - std::abs(gp.offx[o]));
+                sp.aff_vg[NSLOT + 0] = c.p_norm == 1 ? -eps * (double)K * c.lr_h * c.lr_w : 0.0;
+                sp.aff_vg[NSLOT + 1] = -eps * npairs_g;
+                if (c.curv_mode != 1) {   // the FD mode's update pass is a flmisr_general.cu kernel
+                    sp.aff_uc[0] = c.p_norm == 1 ? eps * eps : 2.0;
+                    sp.aff_uc[1] = eps * eps;
+                }
+            }
+            gp.nblk3 = (int)gen3_blocks(p->W, p->H, gcap);
+        }
         gp.fd = c.curv_mode == 1;
         gp.sigma0 = c.scg_sigma0;
         const size_t gbytes = ntap * sizeof(float) + 2 * (size_t)nlr_px * sizeof(float) +

@@ -857,6 +857,7 @@ unsigned gen_blocks_hr(int W, int rows, int cap) {
 cudaError_t launch_gen_value_grad(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
                                   int phase, cudaStream_t s) {
     (void)bw;   // the general kernels walk the plan's BTV offset list (quadrant or Farsiu)
+    if (gp.fused) return launch_gen3_vg(pn, sp, gp, b, phase, s);
     const dim3 lb(LTX * LTY);
     if (pn == 2) { FL_GEN_R(k_gen2_residual, 2, lr_grid(gp), lb) } else { FL_GEN_R(k_gen2_residual, 1, lr_grid(gp), lb) }
     if (pn == 2) { FL_GEN_R(k_gen2_grad, 2, hr_grid(sp, gp), HNT) } else { FL_GEN_R(k_gen2_grad, 1, hr_grid(sp, gp), HNT) }
@@ -866,6 +867,7 @@ cudaError_t launch_gen_value_grad(int bw, int pn, const StencilParams& sp, const
 cudaError_t launch_gen_update_curv(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
                                    int phase, cudaStream_t s) {
     (void)bw;
+    if (gp.fused && !gp.fd) return launch_gen3_uc(pn, sp, gp, b, phase, s);
     const dim3 lb(LTX * LTY);
     if (pn == 2) k_gen2_update<2><<<hr_grid(sp, gp), HNT, 0, s>>>(sp, gp, b, phase);
     else k_gen2_update<1><<<hr_grid(sp, gp), HNT, 0, s>>>(sp, gp, b, phase);

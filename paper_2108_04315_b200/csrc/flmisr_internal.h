@@ -146,6 +146,9 @@ struct GenParams {
     int noff;                    // BTV offsets d = (offy, offx), offy >= 0 (quadrant or Farsiu set)
     int offy[GMAXOFF], offx[GMAXOFF];
     float ogam[GMAXOFF];         // gamma(d)
+    int fused;                   // 1: the fused tiled kernels k_gen3_* run the loop (phases in [-(R+1), mag-1+R])
+    int btvq;                    // BTV offsets are the quadrant of window btvq (compile-time offsets), 0: the list
+    int nblk3;                   // their CTAs
 };
 cudaError_t launch_gen_value_grad(int bw, int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b,
                                   int phase, cudaStream_t s);
@@ -157,6 +160,12 @@ cudaError_t launch_gen_interp(const StencilParams& sp, const GenParams& gp, floa
 unsigned gen_blocks(long long n);
 unsigned gen_blocks_lr(int k, int lr_h, int lr_w, int cap);   // CTAs of the tiled LR-pixel passes
 unsigned gen_blocks_hr(int W, int rows, int cap);             // CTAs of the tiled HR-pixel passes
+unsigned gen3_blocks(int W, int H, int cap);                  // CTAs of the fused general kernels
+size_t gen3_smem(int R, int mag, int k);                      // their dynamic shared memory (max of the two)
+cudaError_t launch_gen3_vg(int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b, int phase,
+                           cudaStream_t s);
+cudaError_t launch_gen3_uc(int pn, const StencilParams& sp, const GenParams& gp, const Buffers& b, int phase,
+                           cudaStream_t s);
 
 // Streaming-path column layout: each aligned group of 4 columns is stored as (c0, c2, c1, c3).
 __host__ __device__ __forceinline__ int phys_col(int c, int perm) {
