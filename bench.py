@@ -40,7 +40,7 @@ WORKLOADS = {
     "C4": "C4: K=9 LR 2048x2048 -> x3 SR 6144x6144 (37.7 MP HR), 20 SCG passes",
     "G3": "G3: K=4 LR 2048x2048 at quarter-pixel shifts (general-geometry path) -> x2 4096x4096, 20 SCG passes",
 }
-# general-geometry path (flmisr_general.cu): algorithmic bytes per HR pixel of the two-kernel phases
+# unfused general-geometry path (flmisr_general.cu): algorithmic bytes per HR pixel of the two-kernel phases
 # for K = mag^2 frames (LR pixels = HR pixels): residual x,p,y,w 16 + gradient w,x,p,r_old,r_new 20;
 # update x,p,r -> x,p 20 + data curvature x,p,y 12
 BYTES_GEN_VALUE_GRAD = 36
@@ -394,12 +394,14 @@ def run_flmisr(args):
     if uc["launches"]:   # per-phase kernels: the dominant launch is value+gradient
         vg_ms = vg["ms"] / max(vg["launches"], 1)
         uc_ms = uc["ms"] / max(uc["launches"], 1)
-        general = pl.fast_path == 0
-        bvg = BYTES_GEN_VALUE_GRAD if general else BYTES_VALUE_GRAD
-        buc = BYTES_GEN_UPDATE_CURV if general else BYTES_UPDATE_CURV
+        general = pl.fast_path in (0, 3)
+        # the fused general kernels (fast_path 3) move what the streaming kernels move (rho' stays on chip)
+        bvg = BYTES_GEN_VALUE_GRAD if pl.fast_path == 0 else BYTES_VALUE_GRAD
+        buc = BYTES_GEN_UPDATE_CURV if pl.fast_path == 0 else BYTES_UPDATE_CURV
         roof = {"bound": "hbm", "achieved": bvg * npx / (vg_ms / 1000.0) / 1e9, "peak": peak,
                 "unit": "GB/s", "traffic": None if general else (traffic or {}).get("value_grad"),
-                "kernel": "k_gen2_residual + k_gen2_grad" if general else "k_vg_stream",
+                "kernel": ("k_gen3_vg" if pl.fast_path == 3 else "k_gen2_residual + k_gen2_grad") if general
+                else "k_vg_stream",
                 "algorithmic_bytes_per_launch": bvg * npx, "avg_launch_ms": vg_ms,
                 "peak_source": peak_src}
         kernels = {"value_grad": {"avg_ms": vg_ms, "launches": vg["launches"],

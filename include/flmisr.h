@@ -170,8 +170,9 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
  * bytes to the other ranks, e.g. over the torch process group; S:288 coordinator role). */
 flmisr_status flmisr_nccl_unique_id(void* out128);
 
-/* HR geometry of a plan: H, W, owned rows [row_lo, row_hi); fast_path = 0 general-geometry kernels,
- * 1 tiled polyphase kernels, 2 streaming polyphase kernels; loop_kernel = 1 when the SCG loop runs as
+/* HR geometry of a plan: H, W, owned rows [row_lo, row_hi); fast_path = 0 general-geometry kernels
+ * (unfused), 1 tiled polyphase kernels, 2 streaming polyphase kernels, 3 fused general-geometry
+ * kernels (every integer phase in [-(R+1), mag-1+R]; FLMISR_GEN2=1 at plan time forces 0); loop_kernel = 1 when the SCG loop runs as
  * one persistent cooperative kernel (streaming path, world 1).  Any output may be NULL. */
 flmisr_status flmisr_plan_info(flmisr_plan_t plan, int32_t* H, int32_t* W, int32_t* row_lo, int32_t* row_hi,
                                int32_t* fast_path, int32_t* loop_kernel);

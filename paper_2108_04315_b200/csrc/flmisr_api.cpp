@@ -617,7 +617,7 @@ flmisr_status flmisr_plan_info(flmisr_plan_t p, int32_t* H, int32_t* W, int32_t*
     if (W) *W = p->W;
     if (row_lo) *row_lo = p->row_lo;
     if (row_hi) *row_hi = p->row_hi;
-    if (fast_path) *fast_path = p->fast ? (p->stream_path ? 2 : 1) : 0;
+    if (fast_path) *fast_path = p->fast ? (p->stream_path ? 2 : 1) : (p->gp.fused ? 3 : 0);
     return FLMISR_OK;
 }
 

@@ -34,15 +34,40 @@ CASES = {
     "single_frame": (30, 30, 2, synth.gaussian_psf(), np.array([[0.25, 0.0]]), 1, 0.05, 2),
     "mag3_psf5_p2": (17, 22, 3, synth.gaussian_psf(0.9, 5), np.round(_rng.uniform(0, 1, (7, 2)), 3), 2, 0.2, 3),
     "delta_w1": (21, 19, 2, synth.delta_psf(), np.array([[0, 0], [0.5, 0.5], [0.3, 0.1]]), 1, 0.05, 1),
+    # integer phases outside [-(R+1), mag-1+R]: always the unfused kernels
+    "far_shift": (26, 23, 2, synth.gaussian_psf(),
+                  np.array([[0, 0], [2.0, -1.5], [0.5, 0.5], [-1.0, 1.5], [1.5, 0.0], [0.0, -0.5]]), 1, 0.05, 3),
+    # mag 4: the fused gather's one-residue-class-per-thread form (at most one tap per axis and class)
+    "mag4_quarter": (12, 17, 4, synth.gaussian_psf(),
+                     np.array([[a / 4 + 0.05 * (b % 2), b / 4 + 0.04 * (a % 2)] for a in range(4) for b in range(4)]),
+                     1, 0.05, 3),
 }
+FUSABLE = {"far_shift": False}
+# f-trace tolerance of the full runs (default 1e-4).  These two geometries are less well conditioned:
+# a 1e-7 relative perturbation of y moves the oracle's own fp64 f trace by 4.4e-5 (far_shift) and
+# 9.8e-5 (mag4_quarter) -- the rho'' regime of DESIGN.md reading 23 -- so fp32 rounding is held to 1e-3
+# there; the final-image bar stays north_star's 1e-3.
+TRACE_RTOL = {"far_shift": 1e-3, "mag4_quarter": 1e-3}
 
 
-def make(orc, name, n_iter=20):
+@pytest.fixture(params=["fused", "unfused"])
+def impl(request, monkeypatch):
+    """The fused tiled kernels (flmisr_general3.cu) and the unfused ones (flmisr_general.cu,
+    FLMISR_GEN2=1 at plan time) on the same cases."""
+    if request.param == "unfused":
+        monkeypatch.setenv("FLMISR_GEN2", "1")
+    return request.param
+
+
+def make(orc, name, n_iter=20, impl=None):
     lr_h, lr_w, mag, psf, sh, pn, lam, w = CASES[name]
     k = len(sh)
     pl = flmisr.Plan(k=k, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=mag, p_norm=pn, lam=lam,
                      btv_window=w, n_iter=n_iter)
-    assert pl.fast_path == 0
+    if impl is None:
+        assert pl.fast_path in (0, 3)
+    else:
+        assert pl.fast_path == (3 if impl == "fused" and FUSABLE.get(name, True) else 0)
     pb = orc.Problem(k=k, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=mag, p_norm=pn, lam=lam, btv_window=w)
     return pl, pb
 
@@ -70,8 +95,8 @@ def test_adjoint(orc, name):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-def test_gradient_and_value(orc, name):
-    pl, pb = make(orc, name)
+def test_gradient_and_value(orc, name, impl):
+    pl, pb = make(orc, name, impl=impl)
     x = synth.random_fields((pb.H, pb.W), 3)
     y = synth.random_fields((pb.k, pb.lr_h, pb.lr_w), 4)
     out = torch.zeros((pb.H, pb.W), device="cuda")
@@ -85,8 +110,8 @@ def test_gradient_and_value(orc, name):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-def test_curvature(orc, name):
-    pl, pb = make(orc, name)
+def test_curvature(orc, name, impl):
+    pl, pb = make(orc, name, impl=impl)
     x = synth.random_fields((pb.H, pb.W), 5)
     y = synth.random_fields((pb.k, pb.lr_h, pb.lr_w), 6)
     p = synth.random_fields((pb.H, pb.W), 7, -1, 1)
@@ -128,16 +153,16 @@ def test_interpolation_fusion(orc, name):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-def test_reconstruct_matches_oracle(orc, name):
+def test_reconstruct_matches_oracle(orc, name, impl):
     lr_h, lr_w, mag, psf, sh, pn, lam, w = CASES[name]
     truth = synth.phantom(mag * lr_h, mag * lr_w, seed=61)
     y = synth.detector_stack(truth, mag, sh, 1 / 255, seed=61).astype(np.float32)
-    pl, pb = make(orc, name, n_iter=20)
+    pl, pb = make(orc, name, n_iter=20, impl=impl)
     hr, rep = pl.reconstruct(dev(y))
     xo, tr, st = orc.scg(pb, y.astype(np.float64), 20)
     assert rel(hr.cpu().numpy(), xo) <= 1e-3
     assert rep["accepted"] == st["accepted"]
-    np.testing.assert_allclose(rep["trace"][:, 1], tr[:, 1], rtol=1e-4)
+    np.testing.assert_allclose(rep["trace"][:, 1], tr[:, 1], rtol=TRACE_RTOL.get(name, 1e-4))
     np.testing.assert_array_equal(rep["trace"][:, 5], tr[:, 5])
 
 
@@ -155,7 +180,7 @@ def test_general_path_agrees_with_fast_path(orc, shape, monkeypatch):
         if force:
             monkeypatch.setenv("FLMISR_FORCE_GENERAL", "1")
         pl = flmisr.Plan(k=4, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=synth.gaussian_psf(), n_iter=20)
-        assert pl.fast_path == (0 if force else 2)
+        assert pl.fast_path == (3 if force else 2)
         hr, _ = pl.reconstruct(dev(y))
         outs.append(hr.cpu().numpy())
     xo, _, _ = orc.scg(pb, y.astype(np.float64), 20)
