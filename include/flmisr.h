@@ -166,6 +166,34 @@ flmisr_status flmisr_plan_virtual(const flmisr_config* cfg, flmisr_plan_t* out);
 flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const float* lr_stack, const float* x0,
                                          float* hr_out, flmisr_report* report);
 
+/*
+ * Row bands over peer memory (the inner-outer border exchange P:197 and the
+ * consensus sums P:195 of Alg. 1).  Each band's whole SCG loop is ONE persistent
+ * cooperative kernel; after every phase the bands meet through peer-mapped memory: each band stores
+ * its fp64 band sums into every rank's mailbox and bumps a per-sender flag word, every rank sums the
+ * world band sums in rank order (bit-identical consensus scalars everywhere), and the value+gradient
+ * pass stores the candidate r's eta boundary rows straight into the neighbours' halo buffers.
+ *
+ * flmisr_reconstruct_virtual_peer: the g bands plans[0..g-1] (flmisr_plan_virtual, ranks 0..g-1 of one
+ *   streaming-path configuration, same device; each virtual plan is sized for 1/g of the SMs) in ONE
+ *   cooperative launch with local pointers in place of the peer mappings.  Arguments, output and report
+ *   as flmisr_reconstruct_virtual.  FLMISR_ERR_CONFIG if the bands do not fit one cooperative wave.
+ * flmisr_peer_export: a world > 1 plan (flmisr_plan) writes FLMISR_PEER_BLOB_BYTES bytes to out (host):
+ *   CUDA IPC handles of its halo buffers and mailbox block.  The caller all-gathers the blobs of the
+ *   world ranks (e.g. over the torch process group) in rank order.
+ * flmisr_peer_connect: blobs = world x FLMISR_PEER_BLOB_BYTES bytes (host, rank order).  Maps every
+ *   peer's mailbox block and the neighbours' halo buffers (same node, NVLink / NVSwitch), after which
+ *   flmisr_reconstruct* on this plan runs the peer loop (the band gather to rank 0 stays on NCCL).
+ *   Every rank of the group must call flmisr_reconstruct* the same number of times with the same
+ *   n_iter.  Errors: FLMISR_ERR_CONFIG (not a streaming band plan, bad blobs, already connected),
+ *   FLMISR_ERR_CUDA (IPC mapping failed, e.g. GPUs without peer access).
+ */
+#define FLMISR_PEER_BLOB_BYTES 256
+flmisr_status flmisr_reconstruct_virtual_peer(flmisr_plan_t* plans, int32_t g, const float* lr_stack,
+                                              const float* x0, float* hr_out, flmisr_report* report);
+flmisr_status flmisr_peer_export(flmisr_plan_t plan, void* out);
+flmisr_status flmisr_peer_connect(flmisr_plan_t plan, const void* blobs);
+
 /* Fill out128 (128 bytes, host) with a fresh ncclUniqueId (rank 0 calls this and broadcasts the
  * bytes to the other ranks, e.g. over the torch process group; S:288 coordinator role). */
 flmisr_status flmisr_nccl_unique_id(void* out128);

@@ -135,7 +135,20 @@ struct flmisr_plan_s {
     int persist = 0;                        // 1: the SCG loop runs as one persistent cooperative kernel
     int prof_mode = 0;                      // layout of the profiling marks of the last call (0 per-kernel, 1 loop)
     flmisr_pipeline_s* pipe = nullptr;      // the pipeline driving this plan, if any
+    // row bands over peer memory (world > 1)
+    unsigned char* peer_mem = nullptr;      // arrival counter, epoch word, mailbox (peer_mem layout below)
+    int peer = 0;                           // 1: flmisr_peer_connect done, the SCG loop is k_scg_peer_loop
+    PeerLoop pl{};                          // its parameters (g = 1)
+    Buffers b_peer{};                       // b with the send rows pointing into the neighbours' halo buffers
+    std::vector<void*> ipc_open;            // peer mappings to close
 };
+
+// peer_mem layout: arrival counter (u64), epoch word (u32), mailbox [2][world][PEER_MAXCTAS][NSLOT] fp64
+constexpr int PEER_MAXCTAS = 256;
+size_t peer_mem_bytes(int world) { return 64 + (size_t)2 * world * PEER_MAXCTAS * NSLOT * sizeof(double); }
+unsigned long long* peer_cnt(unsigned char* m) { return reinterpret_cast<unsigned long long*>(m); }
+unsigned* peer_epoch(unsigned char* m) { return reinterpret_cast<unsigned*>(m + 8); }
+double* peer_mbox(unsigned char* m) { return reinterpret_cast<double*>(m + 64); }
 
 namespace {
 
@@ -349,6 +362,9 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             sp.nstrips = 1 + (p->W > SCOLS - SHALO ? (p->W - (SCOLS - SHALO) + SSTEP - 1) / SSTEP : 0);
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
+            // virtual bands share one device: each gets 1/world of the SMs (the peer-loop emulation runs
+            // all bands in one cooperative launch)
+            if (virt) nsm = std::max(1, nsm / world);
             const long long cap = (long long)nsm * SMINB * sp.wpb;   // one wave of resident warps
             const int rows = p->row_hi - p->row_lo;
             // Work items, one warp each, one wave.  Warps touching an image or band edge run the border
@@ -570,6 +586,10 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         const size_t hf = hb / sizeof(float);
         if (rank > 0) { b.send_top = hm; p->recv_top = hm + 2 * hf; b.halo_top = p->recv_top; }
         if (rank < world - 1) { b.send_bot = hm + hf; p->recv_bot = hm + 3 * hf; b.halo_bot = p->recv_bot; }
+        if (world > PMAX) return cleanup_fail(fail(FLMISR_ERR_CONFIG, "row bands: world <= 8"));
+        e = cudaMalloc(&p->peer_mem, peer_mem_bytes(world));
+        if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc peer mailbox"));
+        cudaMemset(p->peer_mem, 0, peer_mem_bytes(world));
         if (!virt) {
             NcclApi& api = nccl();
             if (!api.ok) return cleanup_fail(fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded"));
@@ -626,6 +646,8 @@ flmisr_status flmisr_destroy(flmisr_plan_t p) {
     if (p->pipe) flmisr_pipeline_destroy(p->pipe);   // drains it; the pipeline cannot outlive its plan
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->comm && nccl().ok) nccl().CommDestroy(p->comm);
+    for (void* m : p->ipc_open) cudaIpcCloseMemHandle(m);
+    if (p->peer_mem) cudaFree(p->peer_mem);
     if (p->halo_mem) cudaFree(p->halo_mem);
     if (p->gmem) cudaFree(p->gmem);
     if (p->gpart) cudaFree(p->gpart);
@@ -778,7 +800,13 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
         return FLMISR_OK;
     };
     bool looped = false;
-    if (p->persist) {   // one cooperative kernel for the init pass and all n_iter passes
+    if (p->peer) {   // row bands over peer memory: the whole loop of this band as one cooperative kernel
+        CUDA_TRY(launch_scg_peer_loop(p->bw, p->pn, p->sp, p->b_peer, p->pl, nullptr, s));
+        looped = true;
+        CUDA_TRY(mark());
+        p->prof_mode = 1;
+    }
+    if (p->persist && !looped) {   // one cooperative kernel for the init pass and all n_iter passes
         cudaError_t le = launch_scg_loop_stream(p->bw, p->pn, p->sp, p->b, s);
         if (le == cudaSuccess) {
             looped = true;
@@ -1003,6 +1031,161 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
         if (report->f_trace) std::memcpy(report->f_trace, plans[0]->trace_host, ntrace * sizeof(double));
     }
     if (hs.failed_stage) return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar");
+    return FLMISR_OK;
+}
+
+// PeerLoop of one band (g = 1) or of all bands of a virtual group (g = world, one device); mbox /
+// flags of rank q at the given (local or peer-mapped) peer_mem base
+static void peer_fill(PeerLoop& pl, int world, unsigned char* const* mem_of_rank) {
+    for (int q = 0; q < world; ++q) {
+        pl.mbox[q] = peer_mbox(mem_of_rank[q]);
+        pl.cnt[q] = peer_cnt(mem_of_rank[q]);
+    }
+}
+static int peer_ctas(const flmisr_plan_s* p) { return (p->sp.nitems + SWPB - 1) / SWPB; }
+
+// The g row bands of one reconstruction on ONE device, synchronised through the peer-loop protocol
+// (mailboxes, flags, halo rows stored into the neighbours' buffers) in one cooperative launch of
+// g x ctas CTAs -- the multi-GPU kernel with local pointers in place of the peer mappings.
+flmisr_status flmisr_reconstruct_virtual_peer(flmisr_plan_t* plans, int32_t g, const float* lr_stack,
+                                              const float* x0, float* hr_out, flmisr_report* report) {
+    if (!plans || g < 2 || g > PMAX) return fail(FLMISR_ERR_SHAPE, "virtual peer group needs 2 <= g <= 8 plans");
+    if (!lr_stack || !hr_out) return fail(FLMISR_ERR_SHAPE, "lr_stack and hr_out are required");
+    int ctas = 0;
+    for (int h = 0; h < g; ++h) {
+        flmisr_plan_s* q = plans[h];
+        if (!q || !q->virt || q->cfg.world != g || q->cfg.rank != h || q->H != plans[0]->H || q->W != plans[0]->W ||
+            q->cfg.n_iter != plans[0]->cfg.n_iter || q->cfg.device != plans[0]->cfg.device || !q->stream_path)
+            return fail(FLMISR_ERR_SHAPE, "plans must be flmisr_plan_virtual streaming bands 0..g-1 of one configuration");
+        ctas = std::max(ctas, peer_ctas(q));
+    }
+    CUDA_TRY(cudaSetDevice(plans[0]->cfg.device));
+    int nsm = 0, coop = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, plans[0]->cfg.device));
+    CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, plans[0]->cfg.device));
+    if (!coop || g * ctas > nsm || ctas > PEER_MAXCTAS)
+        return fail(FLMISR_ERR_CONFIG, "virtual peer group does not fit one cooperative wave");
+    cudaStream_t s = plans[0]->stream;
+    flmisr_status st;
+    for (int h = 0; h < g; ++h)
+        if ((st = enqueue_setup(plans[h], lr_stack, x0, s)) != FLMISR_OK) return st;
+    auto* pb = new PeerBands();   // ~6 KB: kernel-parameter space, not the host stack
+    std::vector<unsigned char*> mems(g);
+    PeerLoop pl{};
+    pl.g = g; pl.rank0 = 0; pl.world = g; pl.ctas = ctas;
+    for (int h = 0; h < g; ++h) {
+        pb->sp[h] = plans[h]->sp;
+        pb->b[h] = plans[h]->b;
+        pb->b[h].send_top = h > 0 ? plans[h - 1]->recv_bot : nullptr;       // straight into the neighbours' halos
+        pb->b[h].send_bot = h < g - 1 ? plans[h + 1]->recv_top : nullptr;
+        mems[h] = plans[h]->peer_mem;
+        pl.epoch_word[h] = peer_epoch(mems[h]);
+    }
+    peer_fill(pl, g, mems.data());
+    cudaError_t le = launch_scg_peer_loop(plans[0]->bw, plans[0]->pn, plans[0]->sp, plans[0]->b, pl, pb, s);
+    delete pb;
+    if (le != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("peer loop launch: ") + cudaGetErrorString(le));
+    for (int h = 0; h < g; ++h)
+        CUDA_TRY(launch_finalize(plans[h]->sp, plans[h]->b, hr_out, plans[h]->W, plans[h]->row_lo, plans[h]->row_hi, s));
+    const size_t ntrace = (size_t)(plans[0]->cfg.n_iter + 1) * 6;
+    for (int h = 0; h < g; ++h) {
+        CUDA_TRY(cudaMemcpyAsync(plans[h]->st_host, plans[h]->st, sizeof(ScgState), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(plans[h]->trace_host, plans[h]->b.trace, ntrace * sizeof(double), cudaMemcpyDeviceToHost,
+                                 s));
+    }
+    cudaError_t se = cudaStreamSynchronize(s);
+    if (se != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("virtual peer group: ") + cudaGetErrorString(se));
+    for (int h = 1; h < g; ++h)
+        if (std::memcmp(plans[h]->trace_host, plans[0]->trace_host, ntrace * sizeof(double)) != 0 ||
+            plans[h]->st_host->k != plans[0]->st_host->k)
+            return fail(FLMISR_ERR_NUMERIC, "virtual peer group: bands disagree on the consensus trace");
+    const ScgState& hs = *plans[0]->st_host;
+    if (report) {
+        report->iters_run = hs.k;
+        report->accepted = hs.accepted;
+        report->converged_at = hs.converged_at;
+        report->failed_stage = hs.failed_stage;
+        report->failed_iter = hs.failed_iter;
+        if (report->f_trace) std::memcpy(report->f_trace, plans[0]->trace_host, ntrace * sizeof(double));
+    }
+    if (hs.failed_stage) return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar");
+    return FLMISR_OK;
+}
+
+// What a rank publishes for its peers: IPC handles of its halo buffers and of its mailbox block, and
+// where its receive rows sit in the halo allocation.
+struct PeerBlob {
+    uint32_t magic, rank, world, ctas;
+    cudaIpcMemHandle_t halo, mbox;
+    uint64_t recv_top_off, recv_bot_off;
+};
+static_assert(sizeof(PeerBlob) <= FLMISR_PEER_BLOB_BYTES, "peer blob size");
+
+flmisr_status flmisr_peer_export(flmisr_plan_t p, void* out) {
+    if (!p || !out) return fail(FLMISR_ERR_SHAPE, "plan and out are required");
+    if (p->cfg.world < 2 || p->virt || !p->peer_mem) return fail(FLMISR_ERR_CONFIG, "peer export needs a band plan (world > 1)");
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    PeerBlob bl{};
+    bl.magic = 0x464c4d50u;   // "FLMP"
+    bl.rank = (uint32_t)p->cfg.rank;
+    bl.world = (uint32_t)p->cfg.world;
+    bl.ctas = (uint32_t)peer_ctas(p);
+    CUDA_TRY(cudaIpcGetMemHandle(&bl.halo, p->halo_mem));
+    CUDA_TRY(cudaIpcGetMemHandle(&bl.mbox, p->peer_mem));
+    bl.recv_top_off = p->recv_top ? (uint64_t)((char*)p->recv_top - (char*)p->halo_mem) : 0;
+    bl.recv_bot_off = p->recv_bot ? (uint64_t)((char*)p->recv_bot - (char*)p->halo_mem) : 0;
+    std::memset(out, 0, FLMISR_PEER_BLOB_BYTES);
+    std::memcpy(out, &bl, sizeof(bl));
+    return FLMISR_OK;
+}
+
+flmisr_status flmisr_peer_connect(flmisr_plan_t p, const void* blobs) {
+    if (!p || !blobs) return fail(FLMISR_ERR_SHAPE, "plan and blobs are required");
+    const int world = p->cfg.world, rank = p->cfg.rank;
+    if (world < 2 || p->virt || !p->peer_mem || !p->stream_path) return fail(FLMISR_ERR_CONFIG, "peer connect needs a streaming band plan (world > 1)");
+    if (p->peer) return fail(FLMISR_ERR_CONFIG, "plan already connected");
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    std::vector<unsigned char*> mems(world, nullptr);
+    std::vector<char*> halos(world, nullptr);
+    std::vector<PeerBlob> bl(world);
+    for (int q = 0; q < world; ++q) {
+        std::memcpy(&bl[q], (const char*)blobs + (size_t)q * FLMISR_PEER_BLOB_BYTES, sizeof(PeerBlob));
+        if (bl[q].magic != 0x464c4d50u || (int)bl[q].rank != q || (int)bl[q].world != world)
+            return fail(FLMISR_ERR_CONFIG, "peer blobs must be the world ranks' flmisr_peer_export outputs in rank order");
+    }
+    for (int q = 0; q < world; ++q) {
+        if (q == rank) {
+            mems[q] = p->peer_mem;
+            halos[q] = (char*)p->halo_mem;
+            continue;
+        }
+        void* m = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&m, bl[q].mbox, cudaIpcMemLazyEnablePeerAccess));
+        p->ipc_open.push_back(m);
+        mems[q] = (unsigned char*)m;
+        if (q == rank - 1 || q == rank + 1) {   // the neighbours' halo buffers receive our boundary rows
+            void* hmap = nullptr;
+            CUDA_TRY(cudaIpcOpenMemHandle(&hmap, bl[q].halo, cudaIpcMemLazyEnablePeerAccess));
+            p->ipc_open.push_back(hmap);
+            halos[q] = (char*)hmap;
+        }
+    }
+    PeerLoop& pl = p->pl;
+    pl = PeerLoop{};
+    pl.g = 1; pl.rank0 = rank; pl.world = world;
+    pl.ctas = 0;   // the same on every rank: the largest band's (smaller bands idle their extra CTAs)
+    for (int q = 0; q < world; ++q) pl.ctas = std::max(pl.ctas, (int)bl[q].ctas);
+    peer_fill(pl, world, mems.data());
+    pl.epoch_word[0] = peer_epoch(p->peer_mem);
+    p->b_peer = p->b;
+    p->b_peer.send_top = rank > 0 ? (float*)(halos[rank - 1] + bl[rank - 1].recv_bot_off) : nullptr;
+    p->b_peer.send_bot = rank < world - 1 ? (float*)(halos[rank + 1] + bl[rank + 1].recv_top_off) : nullptr;
+    int coop = 0, nsm = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, p->cfg.device));
+    CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->cfg.device));
+    if (!coop || pl.ctas > nsm || pl.ctas > PEER_MAXCTAS)
+        return fail(FLMISR_ERR_CONFIG, "peer loop needs a cooperative launch of one wave");
+    p->peer = 1;
     return FLMISR_OK;
 }
 

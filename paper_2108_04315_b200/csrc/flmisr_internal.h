@@ -97,6 +97,25 @@ struct Buffers {
     unsigned* gbar;              // grid-barrier arrival counter of the persistent loop kernel (zeroed per call)
 };
 
+// Row bands over peer memory (flmisr_stream.cu k_scg_peer_loop*).  Pointers
+// indexed by absolute rank q are the rank's memory as mapped on this device (CUDA IPC over NVLink;
+// plain device pointers when all bands share one device); those indexed by the launch-local band l
+// are this device's own.
+constexpr int PMAX = 8;                  // ranks of a peer group
+struct PeerLoop {
+    int g;                       // bands in this launch: 1 (one per GPU) or world (all on one device)
+    int rank0;                   // rank of band l = 0 of this launch
+    int world;
+    int ctas;                    // CTAs per band (identical on every rank)
+    double* mbox[PMAX];          // rank q's mailbox [2][world][ctas][NSLOT]: every CTA's partial sums
+    unsigned long long* cnt[PMAX];   // rank q's arrival counter (monotonic across calls)
+    unsigned* epoch_word[PMAX];  // band l: phases completed over all calls
+};
+struct PeerBands {               // g > 1 (one device): every band's parameters, kernel-parameter space
+    StencilParams sp[PMAX];
+    Buffers b[PMAX];
+};
+
 enum Phase : int { PH_ITER = 0, PH_INIT = 1, PH_DEBUG = 2 };
 
 // Launchers (flmisr_kernels.cu).  Return cudaSuccess or the launch error; dispatch on (kr, bw, pn).
@@ -112,6 +131,8 @@ cudaError_t launch_update_curv_stream(int bw, int pn, const StencilParams& sp, c
 cudaError_t launch_settle(const StencilParams& sp, const Buffers& b, cudaStream_t s);
 // the whole SCG loop (init pass + n_iter passes) as one cooperative persistent kernel (world == 1)
 cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, cudaStream_t s);
+cudaError_t launch_scg_peer_loop(int bw, int pn, const StencilParams& sp, const Buffers& b, const PeerLoop& pl,
+                                 const PeerBands* pb, cudaStream_t s);
 cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s);  // world > 1
 cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s);   // world > 1
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,

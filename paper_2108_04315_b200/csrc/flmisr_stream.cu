@@ -188,14 +188,16 @@ struct Geo {
     bool cv0, cv4;   // the lane's group / the right neighbour group lies inside the image
 };
 
-__device__ __forceinline__ Geo geometry(const StencilParams& sp) {
+// cta: this CTA's index among the CTAs that share the band's work items (blockIdx.x, or the CTA's
+// index within its band in the peer loop)
+__device__ __forceinline__ Geo geometry(const StencilParams& sp, int cta) {
     Geo g;
     // warp index through a lane-0 shuffle so the compiler sees it (and every row pointer and the
     // ring addresses derived from it) as warp-uniform: the bulk copies then take uniform-register
     // operands directly instead of a per-copy R2UR waterfall
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     g.lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * SWPB + warp;
+    const int gw = cta * SWPB + warp;
     g.live = gw < sp.nitems;
     // work item -> (strip, rows [r_lo, r_hi)); see StencilParams: border pieces (band edges, edge
     // strips) are seg_b rows, interior pieces seg_rows rows
@@ -663,7 +665,7 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp
     xcur = __shfl_sync(0xffffffffu, xcur, 0);
     rcur = __shfl_sync(0xffffffffu, rcur, 0);
     alpha = phase == PH_ITER ? __shfl_sync(0xffffffffu, alpha, 0) : 0.0f;
-    const Geo g = geometry(sp);
+    const Geo g = geometry(sp, blockIdx.x);
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
@@ -908,7 +910,7 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp
     rcur = __shfl_sync(0xffffffffu, rcur, 0);
     au = __shfl_sync(0xffffffffu, au, 0);
     be = __shfl_sync(0xffffffffu, be, 0);
-    const Geo g = geometry(sp);
+    const Geo g = geometry(sp, blockIdx.x);
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
@@ -1038,7 +1040,7 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_loop(const __grid_cons
                                                                 const __grid_constant__ Buffers b) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ ScgState S;
-    const Geo g = geometry(sp);
+    const Geo g = geometry(sp, blockIdx.x);
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     if (threadIdx.x == 0) S = *b.st;
@@ -1079,6 +1081,170 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_loop(const __grid_cons
         __syncthreads();
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *b.st = S;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Row bands over peer memory: the whole SCG loop of one band as one persistent kernel, the bands
+// synchronised per phase through peer-mapped memory.  After each phase EVERY
+// CTA of every band
+//   stores its fp64 partial sums into every rank's mailbox, slot [epoch & 1][rank][cta], then (one
+//     fence at system scope when the peers are other GPUs: its candidate r rows, stored straight into
+//     the neighbours' halo buffers, are ordered first) adds 1 to every rank's arrival counter;
+//   waits until its own rank's counter reaches (epoch + 1) x world x ctas (the counters only grow,
+//     across calls too, so no rank ever resets a word a peer writes);
+//   sums all world x ctas slots of its own mailbox in one fixed order -- the same consensus scalars,
+//     bit for bit, on every rank -- and runs the scalar logic (Alg. 1).
+// One hop per phase, as in the single-GPU loop kernel's grid barrier, with the band affine
+// corrections applied per slot owner.  One kernel per rank on a multi-GPU node (g = 1, peers =
+// CUDA-IPC mappings over NVLink); on one device all g bands run in ONE cooperative launch with local
+// pointers (the emulation the profiling guide prescribes for ranks that wait on one another).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p, bool sys) {
+    unsigned long long v;
+    if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// all threads of every CTA: consensus sums of this phase into tot
+__device__ void peer_sum(const StencilParams& sp, const PeerLoop& pl, int l, int j, int which,
+                         const double (&acc)[NSLOT], unsigned epoch, double (&tot)[NSLOT]) {
+    __shared__ double sred[32][NSLOT];
+    __shared__ double stot[NSLOT];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int C = pl.ctas, h = pl.rank0 + l, world = pl.world;
+    const bool sys = pl.g == 1;   // peers on other GPUs
+    const size_t par = (size_t)(epoch & 1) * world * C * NSLOT;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        const double v = warp_sum(acc[k]);
+        if (lane == 0) sred[warp][k] = v;
+    }
+    __syncthreads();
+    FL_TMARK(epoch, 0)
+    if (threadIdx.x == 0) {
+        // this CTA's slot with the band's affine correction spread over its slots (aff * v + off / C)
+        const double* aff = which == 0 ? sp.aff_vg : sp.aff_uc;
+        double v[NSLOT];
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += sred[w][k];
+            v[k] = t * aff[k] + (j == 0 ? aff[NSLOT + k] : 0.0);
+        }
+        const size_t o = par + ((size_t)h * C + j) * NSLOT;
+        for (int q = 0; q < world; ++q) {
+#pragma unroll
+            for (int k = 0; k < NSLOT; ++k) pl.mbox[q][o + k] = v[k];
+        }
+        if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int q = 0; q < world; ++q) {
+            if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(pl.cnt[q]) : "memory");
+            else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pl.cnt[q]) : "memory");
+        }
+        FL_TMARK(epoch, 1)
+        const unsigned long long target = (unsigned long long)(epoch + 1) * (unsigned long long)(world * C);
+        unsigned long long spins = 0;
+        while (ld_acquire_u64(pl.cnt[h], sys) < target)
+            if (++spins > (1ull << 32)) __trap();   // a lost rank or CTA: fail loudly instead of hanging
+    }
+    __syncthreads();
+    FL_TMARK(epoch, 2)
+    // fixed-order sum of the world x C slots: slot i = (rank, cta) by thread i % blockDim, then a fixed
+    // shuffle tree and cross-warp order
+    {
+        const double* mb = pl.mbox[h] + par;
+        double loc[NSLOT];
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) loc[k] = 0.0;
+        for (int i = threadIdx.x; i < world * C; i += blockDim.x)
+#pragma unroll
+            for (int k = 0; k < NSLOT; ++k) loc[k] += ld_relaxed_gpu(mb + (size_t)i * NSLOT + k);
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) {
+            const double v = warp_sum(loc[k]);
+            if (lane == 0) sred[warp][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < NSLOT) {
+            double v = 0.0;
+            for (int w = 0; w < nw; ++w) v += sred[w][threadIdx.x];
+            stot[threadIdx.x] = v;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) tot[k] = stot[k];
+    FL_TMARK(epoch, 3)
+    // the next phase reads peer-written halo rows through the bulk-copy (async) proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int BW, int PN>
+__device__ __forceinline__ void peer_loop_body(const StencilParams& sp, const Buffers& b, const PeerLoop& pl, int l,
+                                               int j, unsigned char* smem, ScgState& S) {
+    const Geo g = geometry(sp, j);
+    Ring ring;
+    ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
+    __shared__ unsigned s_e0;
+    if (threadIdx.x == 0) {
+        S = *b.st;
+        s_e0 = *pl.epoch_word[l];   // epochs of the earlier calls (written by the previous launch)
+    }
+    __syncthreads();
+    double* trace = j == 0 ? b.trace : nullptr;
+    uint32_t par = 0;
+    unsigned epoch = s_e0;
+    double acc[NSLOT], tot[NSLOT];
+    auto ui = [](int v) { return __shfl_sync(0xffffffffu, v, 0); };
+    auto uf = [](float v) { return __shfl_sync(0xffffffffu, v, 0); };
+    for (int pass = 0; !ui(S.done); ++pass) {
+        if (pass > 0) {
+            if (ui(S.success)) {
+                uc_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f), par, acc);
+                peer_sum(sp, pl, l, j, 1, acc, epoch++, tot);
+                if (threadIdx.x == 0) {
+                    S.xcur ^= 1;
+                    scg_after_curv(&S, tot);
+                }
+            } else if (threadIdx.x == 0) {
+                scg_pre_value(&S);
+            }
+            __syncthreads();
+            if (ui(S.done)) break;
+        }
+        vg_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par, acc);
+        peer_sum(sp, pl, l, j, 0, acc, epoch++, tot);
+        if (threadIdx.x == 0) scg_after_value(&S, tot, trace, pass > 0 ? PH_ITER : PH_INIT);
+        __syncthreads();
+    }
+    if (j == 0 && threadIdx.x == 0) {
+        *b.st = S;
+        *pl.epoch_word[l] = epoch;   // the next call's first epoch (identical on every rank)
+    }
+}
+
+// one band per launch (multi-GPU): parameters in the constant bank
+template <int BW, int PN>
+__global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_peer_loop(const __grid_constant__ StencilParams sp,
+                                                                     const __grid_constant__ Buffers b,
+                                                                     const __grid_constant__ PeerLoop pl) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ ScgState S;
+    peer_loop_body<BW, PN>(sp, b, pl, 0, blockIdx.x, smem, S);
+}
+
+// all bands in one cooperative launch (one device): band l = blockIdx.x / ctas; every band's
+// parameters in the constant bank (block-uniform index)
+template <int BW, int PN>
+__global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_peer_loop_multi(const __grid_constant__ PeerLoop pl,
+                                                                           const __grid_constant__ PeerBands pb) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ ScgState S;
+    const int l = __shfl_sync(0xffffffffu, (int)(blockIdx.x / pl.ctas), 0);
+    const int j = blockIdx.x - l * pl.ctas;
+    peer_loop_body<BW, PN>(pb.sp[l], pb.b[l], pl, l, j, smem, S);
 }
 
 bool pdl_enabled() {
@@ -1174,6 +1340,36 @@ cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, cons
     case BW_ * 10 + PN_: return launch_loop(k_scg_loop<BW_, PN_>, sp.nitems, sp, b, s);
         FL_LCASE(1, 1) FL_LCASE(1, 2) FL_LCASE(2, 1) FL_LCASE(2, 2) FL_LCASE(3, 1) FL_LCASE(3, 2)
 #undef FL_LCASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <typename K, typename... A>
+cudaError_t launch_coop(K kernel, int grid, cudaStream_t s, A... args) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(SWPB * 32);
+    cfg.dynamicSmemBytes = RING_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // co-residency: the barriers cannot deadlock
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+cudaError_t launch_scg_peer_loop(int bw, int pn, const StencilParams& sp, const Buffers& b, const PeerLoop& pl,
+                                 const PeerBands* pb, cudaStream_t s) {
+    switch (bw * 10 + pn) {
+#define FL_PCASE(BW_, PN_) \
+    case BW_ * 10 + PN_:   \
+        return pl.g == 1 ? launch_coop(k_scg_peer_loop<BW_, PN_>, pl.ctas, s, sp, b, pl) \
+                         : launch_coop(k_scg_peer_loop_multi<BW_, PN_>, pl.g * pl.ctas, s, pl, *pb);
+        FL_PCASE(1, 1) FL_PCASE(1, 2) FL_PCASE(2, 1) FL_PCASE(2, 2) FL_PCASE(3, 1) FL_PCASE(3, 2)
+#undef FL_PCASE
         default: return cudaErrorInvalidValue;
     }
 }

@@ -52,7 +52,9 @@ EXPORTS = ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_async", "flm
            "flmisr_profile", "flmisr_reconstruct_host", "flmisr_destroy", "flmisr_last_error",
            "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply", "flmisr_band",
            "flmisr_plan_virtual", "flmisr_reconstruct_virtual", "flmisr_pipeline_create",
-           "flmisr_pipeline_submit", "flmisr_pipeline_wait", "flmisr_pipeline_destroy")
+           "flmisr_pipeline_submit", "flmisr_pipeline_wait", "flmisr_pipeline_destroy",
+           "flmisr_reconstruct_virtual_peer", "flmisr_peer_export", "flmisr_peer_connect")
+PEER_BLOB_BYTES = 256   # FLMISR_PEER_BLOB_BYTES
 
 
 def _load():
@@ -75,6 +77,9 @@ def _load():
     lib.flmisr_band.argtypes = [C.c_int32] * 4 + [C.POINTER(C.c_int32)] * 2
     lib.flmisr_plan_virtual.argtypes = [C.POINTER(Config), C.POINTER(vp)]
     lib.flmisr_reconstruct_virtual.argtypes = [C.POINTER(vp), C.c_int32, vp, vp, vp, C.POINTER(Report)]
+    lib.flmisr_reconstruct_virtual_peer.argtypes = [C.POINTER(vp), C.c_int32, vp, vp, vp, C.POINTER(Report)]
+    lib.flmisr_peer_export.argtypes = [vp, vp]
+    lib.flmisr_peer_connect.argtypes = [vp, vp]
     lib.flmisr_pipeline_create.argtypes = [vp, C.c_int32, C.c_int32, C.c_float, C.POINTER(vp)]
     lib.flmisr_pipeline_submit.argtypes = [vp, vp, vp]
     lib.flmisr_pipeline_wait.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(Report)]
@@ -239,6 +244,44 @@ class Plan:
         sc = (C.c_double * 4)()
         _check(_lib.flmisr_debug_apply(self._h, op, _ptr(lr), _ptr(in0), _ptr(in1), _ptr(out), sc))
         return list(sc)
+
+
+def peer_connect(plan: "Plan", group=None) -> None:
+    """Row bands over peer memory (flmisr_peer_export / flmisr_peer_connect): every rank exports the
+    IPC handles of its halo buffers and mailbox block, the blobs are all-gathered over the torch
+    process group in rank order, and each rank maps its peers'.  Afterwards plan.reconstruct* runs
+    the band's whole SCG loop as one persistent kernel synchronised through peer memory."""
+    import torch.distributed as dist
+    blob = C.create_string_buffer(PEER_BLOB_BYTES)
+    _check(_lib.flmisr_peer_export(plan._h, C.cast(blob, C.c_void_p)))
+    blobs = gather_blobs(bytes(blob.raw), dist.get_world_size(group), group)
+    allb = C.create_string_buffer(b"".join(blobs), len(blobs) * PEER_BLOB_BYTES)
+    _check(_lib.flmisr_peer_connect(plan._h, C.cast(allb, C.c_void_p)))
+
+
+def gather_blobs(blob: bytes, world: int, group=None) -> list:
+    """All-gather one fixed-size byte blob per rank over the torch process group (rank order)."""
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, blob, group=group)
+    if any(not isinstance(b, bytes) or len(b) != len(blob) for b in out):
+        raise FlmisrError(-1, "peer blobs of unequal size")
+    return out
+
+
+def reconstruct_virtual_peer(plans, lr_stack, x0=None, out=None):
+    """flmisr_reconstruct_virtual_peer: the g bands (Plan(..., virtual=True, rank=h, world=g)) as the
+    peer-memory band loop, all in one cooperative launch on one device; returns (hr, report)."""
+    import torch
+    p0 = plans[0]
+    if out is None:
+        out = torch.empty((p0.H, p0.W), dtype=torch.float32, device=lr_stack.device)
+    arr = (C.c_void_p * len(plans))(*[p._h.value for p in plans])
+    trace = np.zeros((p0.n_iter + 1, 6))
+    rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
+    torch.cuda.current_stream(lr_stack.device).synchronize()
+    _check(_lib.flmisr_reconstruct_virtual_peer(arr, len(plans), _ptr(lr_stack), _ptr(x0), _ptr(out), C.byref(rep)))
+    return out, p0._report(rep, trace)
 
 
 def reconstruct_virtual(plans, lr_stack, x0=None, out=None):

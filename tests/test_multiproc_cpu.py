@@ -38,7 +38,11 @@ def _worker(rank, world, port, q):
         mine = {k: v for k, v in bands.items()}
         allb = [None] * world
         dist.all_gather_object(allb, mine)
-        q.put((rank, len(uid), all(i == ids[0] for i in ids), allb[0] == allb[1], bands))
+        # peer transport: every rank's fixed-size blob, gathered in rank order (flmisr_peer_connect input)
+        blob = bytes([rank]) * flmisr.PEER_BLOB_BYTES
+        blobs = flmisr.gather_blobs(blob, world)
+        peer_ok = blobs == [bytes([r]) * flmisr.PEER_BLOB_BYTES for r in range(world)]
+        q.put((rank, len(uid), all(i == ids[0] for i in ids), allb[0] == allb[1], bands, peer_ok))
     finally:
         dist.destroy_process_group()
 
@@ -56,8 +60,8 @@ def test_unique_id_broadcast_and_band_agreement():
         assert p.exitcode == 0
     res = [q.get() for _ in range(world)]
     from oracle import oracle
-    for rank, nid, same_id, same_bands, bands in res:
-        assert nid == 128 and same_id and same_bands
+    for rank, nid, same_id, same_bands, bands, peer_ok in res:
+        assert nid == 128 and same_id and same_bands and peer_ok
         for (H, mag, g), bb in bands.items():
             # bands tile [0, H) without gaps or overlap, boundaries are multiples of mag
             assert bb[0][0] == 0 and bb[-1][1] == H
