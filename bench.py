@@ -308,6 +308,8 @@ def run_flmisr(args):
         pl = flmisr.Plan(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, p_norm=1,
                          l1_eps=1e-3, lam=0.05, btv_alpha=0.4, btv_window=3, n_iter=n_iter, device=local,
                          rank=rank, world=world, nccl_id=nid)
+        if args.transport == "peer":   # the band loop over peer memory (CUDA IPC); gather stays on NCCL
+            flmisr.peer_connect(pl)
     else:             # replicas: every rank reconstructs its own projection
         pl = flmisr.Plan(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, p_norm=1,
                          l1_eps=1e-3, lam=0.05, btv_alpha=0.4, btv_window=3, n_iter=n_iter, device=local)
@@ -454,7 +456,8 @@ def run_flmisr(args):
                    "btv_alpha": 0.4, "btv_window": 3, "psf": "3x3 Gaussian sigma 0.5",
                    "l2": "flushed before every timed step (512 MiB device write)",
                    "parallelism": "single GPU" if world == 1 else
-                   (f"row bands x{world} (NCCL halo + allgather)" if partitioned else f"replicas x{world}")},
+                   ((f"row bands x{world} (peer-memory band loop)" if args.transport == "peer" else
+                     f"row bands x{world} (NCCL halo + allgather)") if partitioned else f"replicas x{world}")},
         "scg_iters_per_s": value * n_iter,
         "accepted_fraction": float(np.mean(accepted)) / n_iter if n_iter else None,
         "roofline": roof,
@@ -487,6 +490,9 @@ def main():
     ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned", "stream"],
                     help="N > 1: independent projections per rank (default) or row bands of one projection; "
                          "stream: C5 capture-reconstruct pipeline (host frames in, host images out)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="partitioned mode: NCCL halo send/recv + allgather per phase (default), or each band's "
+                         "whole loop as one kernel synchronised through CUDA-IPC peer memory")
     ap.add_argument("--partition", action="store_true", help="stream mode, N > 1: row bands instead of replicas")
     ap.add_argument("--u16", action="store_true", help="stream mode: 16-bit detector codes as input")
     ap.add_argument("--depth", type=int, default=3, help="stream mode: views in flight")
