@@ -28,6 +28,9 @@ namespace flmisr {
 namespace {
 
 constexpr int G3X = 64, G3Y = 32, G3T = 256, G3FC = 4;
+// resident CTAs per SM the fused kernels are compiled for (measured on G3: value+gradient 0.67 ms at 3
+// vs 0.72 at 4; update+curvature 0.32 at 3 vs 0.30 at 4)
+constexpr int G3MINB_VG = 3, G3MINB_UC = 4;
 constexpr int G3PPT = G3X * G3Y / G3T;   // 8 output pixels per thread: column t % 64, rows t / 64 + 4 k
 
 __device__ __forceinline__ int fdiv(int a, int m) { return a >= 0 ? a / m : -((-a + m - 1) / m); }
@@ -161,8 +164,20 @@ __device__ __forceinline__ float btv_curv(const StencilParams& sp, const GenPara
     return c;
 }
 
+// L2 prefetch (bulk-copy engine, no registers) of the row segment [c0, c1) of `rows` rows of A,
+// spread over the CTA's threads: the next tile's operands are in L2 when its staging loads issue
+__device__ __forceinline__ void l2_prefetch_rows(const float* A, size_t pitch, int r0, int nrows, int rlo, int rhi,
+                                                 int c0, int c1, int first_thread) {
+    const int t = (int)threadIdx.x - first_thread;
+    if (t < 0 || t >= nrows) return;
+    const int r = min(max(r0 + t, rlo), rhi);
+    const uintptr_t a = reinterpret_cast<uintptr_t>(A + (size_t)r * pitch + c0) & ~(uintptr_t)15;
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(A + (size_t)r * pitch + c1) + 15) & ~(uintptr_t)15;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
+
 template <int PN, int R, int MAG, int BQ>
-__global__ void __launch_bounds__(G3T, 3) k_gen3_vg(StencilParams sp, GenParams gp, Buffers b, int phase) {
+__global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, GenParams gp, Buffers b, int phase) {
     using T = G3<R, MAG>;
     constexpr int KD = T::KD, HX = T::H, XC = T::XC, WC = T::WC, NT = T::NT;
     extern __shared__ __align__(16) float g3s[];
@@ -198,6 +213,19 @@ __global__ void __launch_bounds__(G3T, 3) k_gen3_vg(StencilParams sp, GenParams 
         }
         __syncthreads();   // the previous tile's x' and windows are consumed
         g3_stage<R, MAG>(sp, X, P, alpha, ty0, tx0, xs);
+        {   // prefetch the next tile's x, p (tile + halo) and r_old rows into L2 while this one computes
+            const int tn = t + gridDim.x;
+            if (tn < ntx * nty) {
+                const int ny0 = (tn / ntx) * G3Y, nx0 = (tn % ntx) * G3X;
+                const int c0 = max(nx0 - HX, 0), c1 = min(nx0 + G3X + HX, sp.W);
+                const float* Xb = X - (size_t)sp.store_lo * sp.pitch;
+                const float* Pb = P - (size_t)sp.store_lo * sp.pitch;
+                const float* Rb = Ro - (size_t)sp.store_lo * sp.pitch;
+                l2_prefetch_rows(Xb, sp.pitch, ny0 - HX, T::XR, 0, sp.H - 1, c0, c1, 0);
+                l2_prefetch_rows(Pb, sp.pitch, ny0 - HX, T::XR, 0, sp.H - 1, c0, c1, 64);
+                l2_prefetch_rows(Rb, sp.pitch, ny0, G3Y, 0, sp.H - 1, nx0, min(nx0 + G3X, sp.W), 128);
+            }
+        }
         float g[G3PPT];
 #pragma unroll
         for (int k = 0; k < G3PPT; ++k) g[k] = 0.0f;
@@ -353,7 +381,7 @@ __global__ void __launch_bounds__(G3T, 3) k_gen3_vg(StencilParams sp, GenParams 
 }
 
 template <int PN, int R, int MAG, int BQ>
-__global__ void __launch_bounds__(G3T, 3) k_gen3_uc(StencilParams sp, GenParams gp, Buffers b, int phase) {
+__global__ void __launch_bounds__(G3T, G3MINB_UC) k_gen3_uc(StencilParams sp, GenParams gp, Buffers b, int phase) {
     using T = G3<R, MAG>;
     constexpr int KD = T::KD, HX = T::H, XC = T::XC;
     extern __shared__ __align__(16) float g3s[];
@@ -386,6 +414,17 @@ __global__ void __launch_bounds__(G3T, 3) k_gen3_uc(StencilParams sp, GenParams 
         __syncthreads();
         g3_stage<R, MAG>(sp, X, Pc, au, ty0, tx0, xs);
         g3_stage<R, MAG>(sp, Rc, Pc, be, ty0, tx0, ps);
+        {   // prefetch the next tile's x, p, r (tile + halo) into L2 while this one computes
+            const int tn = t + gridDim.x;
+            if (tn < ntx * nty) {
+                const int ny0 = (tn / ntx) * G3Y, nx0 = (tn % ntx) * G3X;
+                const int c0 = max(nx0 - HX, 0), c1 = min(nx0 + G3X + HX, sp.W);
+                const size_t so = (size_t)sp.store_lo * sp.pitch;
+                l2_prefetch_rows(X - so, sp.pitch, ny0 - HX, T::XR, 0, sp.H - 1, c0, c1, 0);
+                l2_prefetch_rows(Pc - so, sp.pitch, ny0 - HX, T::XR, 0, sp.H - 1, c0, c1, 64);
+                l2_prefetch_rows(Rc - so, sp.pitch, ny0 - HX, T::XR, 0, sp.H - 1, c0, c1, 128);
+            }
+        }
         __syncthreads();
         const bool inner = ty0 >= HX && ty0 + G3Y + HX <= sp.H && tx0 >= HX && tx0 + G3X + HX <= sp.W;
 #pragma unroll
