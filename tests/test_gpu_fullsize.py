@@ -77,3 +77,39 @@ def test_c3_reconstruction_properties(orc, c3):
     assert np.isfinite(h).all()
     J = orc.objective(pb, h, y.astype(np.float64))
     assert abs(J - f[-1]) <= 1e-5 * J
+
+
+@pytest.fixture(scope="module")
+def g3(orc):
+    """G3: C3's size at quarter-pixel shifts -- the fused general-geometry kernels bench.py --config G3
+    times (fast_path 3), against the oracle on the full image."""
+    c = synth.CONFIGS["G3"]
+    sh = np.asarray(c["shifts"], dtype=np.float64)
+    pl = flmisr.Plan(k=len(sh), lr_h=c["lr"], lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=c["mag"],
+                     n_iter=c["n_iter"])
+    pb = orc.Problem(k=len(sh), lr_h=c["lr"], lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=c["mag"])
+    assert pl.fast_path == 3
+    return pl, pb
+
+
+def test_g3_gradient_value_curvature_random_inputs(orc, g3):
+    """Per-operator bar at full size on the general path: gradient and value 1e-5 relative; the data
+    curvature adds the rho'' conditioning bound of reading 23 (as in tests/test_gpu_general.py)."""
+    from test_gpu_general import curv_rounding_bound
+    pl, pb = g3
+    y = synth.random_fields((pb.k, pl.lr_h, pl.lr_w), 82)
+    yd = torch.from_numpy(y).cuda()
+    xr = synth.random_fields((pl.H, pl.W), 83)
+    x0 = torch.from_numpy(xr).cuda()
+    x = xr.astype(np.float64)
+    r = torch.zeros_like(x0)
+    D, R, rr, _ = pl.debug(flmisr.OP_GRAD, lr=yd, in0=x0, out=r)
+    g = orc.grad(pb, x, y.astype(np.float64))
+    rn = r.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(rn + g) <= 1e-5 * np.linalg.norm(g)
+    Do, Ro = orc.value(pb, x, y.astype(np.float64))
+    assert abs(D - Do) <= 1e-5 * Do and abs(R - Ro) <= 1e-5 * Ro
+    p = synth.random_fields((pl.H, pl.W), 81, -1, 1)
+    delta, pp, mu, _ = pl.debug(flmisr.OP_CURV, lr=yd, in0=x0, in1=torch.from_numpy(p).cuda())
+    dref = orc.curv(pb, x, y.astype(np.float64), p.astype(np.float64))
+    assert abs(delta - dref) <= 1e-5 * abs(dref) + curv_rounding_bound(orc, pb, xr, y, p)
