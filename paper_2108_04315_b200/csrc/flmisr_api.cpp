@@ -382,15 +382,20 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             auto items = [&](int Si, int Sb) {
                 return (long long)sp.ni * nseg_int(Si, Sb) + (long long)sp.ne * ((rows + Sb - 1) / Sb);
             };
-            int S = 16;
+            // the shortest segments (S = 1 mod 3, >= S0) whose items fit one wave: every resident warp
+            // busy, each warp's serial row chain as short as possible (the phase time is ~ rows per
+            // warp x ~1.1 us at C3; a band of a g-GPU partition has few rows)
+            int S0 = 4;
+            if (const char* ev = std::getenv("FLMISR_SEG_MIN")) S0 = std::max(4, std::atoi(ev));
+            int S = to1mod3(S0);
             int Sb = to1mod3((int)(S / ratio));
             while (S < rows && items(S, Sb) > cap) {
                 S += 3;
                 Sb = to1mod3((int)(S / ratio));
             }
-            if (const char* ev = std::getenv("FLMISR_SEG_ROWS")) {   // tuning override (S = 1 mod 3)
-                const int v = std::atoi(ev);
-                if (v >= 4) { S = to1mod3(v); Sb = to1mod3((int)(S / ratio)); }
+            if (const char* ev = std::getenv("FLMISR_SEG_ROWS")) {   // tuning override (S = 1 mod 3), never
+                const int v = std::atoi(ev);                        // below the one-wave minimum
+                if (v >= 4 && to1mod3(v) > S) { S = to1mod3(v); Sb = to1mod3((int)(S / ratio)); }
             }
             S = std::min(S, rows + ((1 - rows % 3) + 3) % 3);     // smallest >= rows with S = 1 mod 3
             Sb = std::min(Sb, S);
