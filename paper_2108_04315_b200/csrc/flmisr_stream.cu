@@ -967,6 +967,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define FL_TMARK(ep, k)
 #endif
 
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // grid-wide sum of acc over all threads of all CTAs in a fixed order; result in tot (all threads)
 __device__ void grid_sum(const double (&acc)[NSLOT], double* part, unsigned* gbar, unsigned epoch,
                          double (&tot)[NSLOT]) {
@@ -994,9 +1000,11 @@ __device__ void grid_sum(const double (&acc)[NSLOT], double* part, unsigned* gba
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
         FL_TMARK(epoch, 1)
         const unsigned target = (epoch + 1) * (unsigned)G;
-        unsigned long long spins = 0;
+        unsigned spins = 0;
+        const unsigned long long tstart = now_ns();
         while (ld_acquire_u32(gbar) < target) {
-            if (++spins > (1ull << 31)) __trap();   // a lost CTA: fail loudly instead of hanging the device
+            // a lost CTA: fail loudly (after 10 s; a phase takes < 1 ms) instead of hanging the device
+            if ((++spins & 1023u) == 0 && now_ns() - tstart > 10000000000ull) __trap();
         }
         FL_TMARK(epoch, 2)
     }
@@ -1145,9 +1153,10 @@ __device__ void peer_sum(const StencilParams& sp, const PeerLoop& pl, int l, int
         }
         FL_TMARK(epoch, 1)
         const unsigned long long target = (unsigned long long)(epoch + 1) * (unsigned long long)(world * C);
-        unsigned long long spins = 0;
-        while (ld_acquire_u64(pl.cnt[h], sys) < target)
-            if (++spins > (1ull << 32)) __trap();   // a lost rank or CTA: fail loudly instead of hanging
+        unsigned spins = 0;
+        const unsigned long long tstart = now_ns();
+        while (ld_acquire_u64(pl.cnt[h], sys) < target)   // a lost rank or CTA: fail loudly after 60 s
+            if ((++spins & 1023u) == 0 && now_ns() - tstart > 60000000000ull) __trap();
     }
     __syncthreads();
     FL_TMARK(epoch, 2)
