@@ -41,6 +41,9 @@ CASES = {
     "mag4_quarter": (12, 17, 4, synth.gaussian_psf(),
                      np.array([[a / 4 + 0.05 * (b % 2), b / 4 + 0.04 * (a % 2)] for a in range(4) for b in range(4)]),
                      1, 0.05, 3),
+    # mag 1 (deblurring + sub-pixel registration, no zoom) and many frames (K = 12, 3 chunks of 4)
+    "mag1": (40, 52, 1, synth.gaussian_psf(), np.array([[0, 0], [0.5, 0.25], [-0.3, 0.6]]), 1, 0.05, 3),
+    "k12": (20, 26, 2, synth.gaussian_psf(), np.round(_rng.uniform(0, 1, (12, 2)), 3), 1, 0.05, 3),
 }
 FUSABLE = {"far_shift": False}
 # f-trace tolerance of the full runs (default 1e-4).  These two geometries are less well conditioned:
