@@ -39,7 +39,11 @@ WORKLOADS = {
     "C3": "C3: K=4 LR 2048x2048 -> x2 SR 4096x4096 (16.8 MP HR), 20 SCG passes",
     "C4": "C4: K=9 LR 2048x2048 -> x3 SR 6144x6144 (37.7 MP HR), 20 SCG passes",
     "G3": "G3: K=4 LR 2048x2048 at quarter-pixel shifts (general-geometry path) -> x2 4096x4096, 20 SCG passes",
+    "C6": "C6: K=4 LR 4096x4096 -> x2 SR 8192x8192 (67.1 MP HR), 20 SCG passes (the paper's largest case)",
 }
+# The paper's own single-GPU runtime for exactly this workload (BASELINE.md tab:runtime, P:435-437:
+# LR 2048^2 -> x2, 20 SCG iterations, 1x GTX 1080: 2.43 s) -- context on other hardware, not a target.
+PAPER_1GPU_S = {"C3": 2.43}
 # unfused general-geometry path (flmisr_general.cu): algorithmic bytes per HR pixel of the two-kernel phases
 # for K = mag^2 frames (LR pixels = HR pixels): residual x,p,y,w 16 + gradient w,x,p,r_old,r_new 20;
 # update x,p,r -> x,p 20 + data curvature x,p,y 12
@@ -451,7 +455,11 @@ def run_flmisr(args):
         "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if partitioned else "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "vs_baseline": (value * PAPER_1GPU_S[cfg] if world == 1 and cfg in PAPER_1GPU_S else None),
+        "vs_baseline_note": (f"value / (1 / {PAPER_1GPU_S[cfg]} s): the paper's own runtime for this workload on "
+                             "1x GTX 1080 (BASELINE.md tab:runtime) -- context, not a target"
+                             if world == 1 and cfg in PAPER_1GPU_S else None),
+        "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOADS[cfg], "n_iter": n_iter, "hr": [H, W], "p_norm": 1, "lambda": 0.05,
                    "btv_alpha": 0.4, "btv_window": 3, "psf": "3x3 Gaussian sigma 0.5",
                    "l2": "flushed before every timed step (512 MiB device write)",
@@ -485,7 +493,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="flmisr", choices=["flmisr", "reference"])
-    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4", "G3"])
+    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4", "C6", "G3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned", "stream"],
                     help="N > 1: independent projections per rank (default) or row bands of one projection; "

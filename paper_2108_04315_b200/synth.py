@@ -138,6 +138,8 @@ CONFIGS = {
     "C2": dict(lr=1024, mag=2, n_iter=50, seed=2109),
     "C3": dict(lr=2048, mag=2, n_iter=20, seed=2110),
     "C4": dict(lr=2048, mag=3, n_iter=20, seed=2111),
+    # the paper's largest tab:runtime workload: 4 LR 4096^2 -> x2 (67 MP HR), 20 iterations
+    "C6": dict(lr=4096, mag=2, n_iter=20, seed=2113),
     # general-geometry path at C3 size: K = 4 frames at quarter-pixel detector
     # positions (fractional HR phases, a different composed kernel per frame)
     "G3": dict(lr=2048, mag=2, n_iter=20, seed=2112,
