@@ -72,3 +72,17 @@ def test_band_too_small_names_minimum_height(fl):
         fl.Plan(**c)
     assert ei.value.status == fl.ERR_CONFIG
     assert "minimum HR height" in str(ei.value)
+
+
+def test_peer_entry_points_reject_bad_arguments_without_a_gpu(fl):
+    """The peer-memory band loop's entry points validate before touching a device."""
+    import ctypes as C
+    buf = C.create_string_buffer(fl.PEER_BLOB_BYTES)
+    assert fl._lib.flmisr_peer_export(None, C.cast(buf, C.c_void_p)) == -2          # FLMISR_ERR_SHAPE
+    assert "plan" in fl.last_error()
+    assert fl._lib.flmisr_peer_connect(None, C.cast(buf, C.c_void_p)) == -2
+    arr = (C.c_void_p * 1)(None)
+    assert fl._lib.flmisr_reconstruct_virtual_peer(arr, 1, None, None, None, None) == -2
+    assert "2 <= g <= 8" in fl.last_error()
+    arr9 = (C.c_void_p * 9)(*([None] * 9))
+    assert fl._lib.flmisr_reconstruct_virtual_peer(arr9, 9, None, None, None, None) == -2
