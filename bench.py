@@ -405,7 +405,7 @@ def run_flmisr(args):
         bvg = BYTES_GEN_VALUE_GRAD if pl.fast_path == 0 else BYTES_VALUE_GRAD
         buc = BYTES_GEN_UPDATE_CURV if pl.fast_path == 0 else BYTES_UPDATE_CURV
         roof = {"bound": "hbm", "achieved": bvg * npx / (vg_ms / 1000.0) / 1e9, "peak": peak,
-                "unit": "GB/s", "traffic": None if general else (traffic or {}).get("value_grad"),
+                "unit": "GB/s", "traffic": None if pl.fast_path == 0 else (traffic or {}).get("value_grad"),
                 "kernel": ("k_gen3_vg" if pl.fast_path == 3 else "k_gen2_residual + k_gen2_grad") if general
                 else "k_vg_stream",
                 "algorithmic_bytes_per_launch": bvg * npx, "avg_launch_ms": vg_ms,
