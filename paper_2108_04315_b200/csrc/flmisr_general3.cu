@@ -243,13 +243,29 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
                 load_taps<KD>(ts + i * KD * KD, tk);
                 const float* yi = gp.lr + (size_t)i * gp.lr_h * gp.lr_w;
                 float* wf = ws + f * T::WR * WC;
-                for (int e = tid; e < wr * wc; e += G3T) {
+                // this thread's window samples of y, all loads issued before the first use (fixed trip
+                // count: the window is at most WR x WC)
+                constexpr int NE = (T::WR * WC + G3T - 1) / G3T;
+                float yr[NE];
+#pragma unroll
+                for (int n = 0; n < NE; ++n) {
+                    const int e = tid + n * G3T;
+                    int ra, cb;
+                    split(e, wc, inv, ra, cb);
+                    const int a = alo + ra, bb = blo + cb;
+                    yr[n] = (e < wr * wc && a >= 0 && a < gp.lr_h && bb >= 0 && bb < gp.lr_w)
+                                ? __ldg(yi + (size_t)a * gp.lr_w + bb) : 0.0f;
+                }
+#pragma unroll
+                for (int n = 0; n < NE; ++n) {
+                    const int e = tid + n * G3T;
+                    if (e >= wr * wc) break;
                     int ra, cb;
                     split(e, wc, inv, ra, cb);
                     const int a = alo + ra, bb = blo + cb;
                     float d1 = 0.0f;
                     if (a >= 0 && a < gp.lr_h && bb >= 0 && bb < gp.lr_w) {
-                        const float yv = __ldg(yi + (size_t)a * gp.lr_w + bb);   // issued before the taps
+                        const float yv = yr[n];
                         const float ev = g3_fwd<R, MAG>(tk, xs, MAG * a + sy - R - (ty0 - HX), MAG * bb + sx - R - (tx0 - HX)) - yv;
                         float v;
                         if (PN == 2) {
@@ -360,8 +376,15 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
                 }
             }
         }
-        // BTV (valid pairs only) and the output
+        // BTV (valid pairs only) and the output; r_old of the 8 pixels loaded first (in flight
+        // during the BTV arithmetic)
         const bool inner = ty0 >= HX && ty0 + G3Y + HX <= sp.H && tx0 >= HX && tx0 + G3X + HX <= sp.W;
+        float rold[G3PPT];
+#pragma unroll
+        for (int k = 0; k < G3PPT; ++k) {
+            const int vy = vy0 + 4 * k;
+            rold[k] = (vy < sp.H && vx < sp.W) ? __ldg(Ro + (size_t)(vy - sp.store_lo) * sp.pitch + vx) : 0.0f;
+        }
 #pragma unroll
         for (int k = 0; k < G3PPT; ++k) {
             const int vy = vy0 + 4 * k;
@@ -373,7 +396,7 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
             const size_t o = (size_t)(vy - sp.store_lo) * sp.pitch + vx;
             Rn[o] = rn;
             acc[2] = fmaf(rn, rn, acc[2]);
-            acc[3] = fmaf(rn, __ldg(Ro + o), acc[3]);
+            acc[3] = fmaf(rn, rold[k], acc[3]);
         }
     }
     double accd[NSLOT] = {acc[0], acc[1], acc[2], acc[3]}, tot[NSLOT];
