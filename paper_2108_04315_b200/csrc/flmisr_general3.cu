@@ -41,7 +41,8 @@ template <int R, int MAG>
 struct G3 {
     static constexpr int KD = 2 * R + 2;                          // kappa offsets [-R, R+1]
     static constexpr int H = (2 * R + 1 > 2) ? 2 * R + 1 : 2;     // halo: forward + adjoint reach, BTV
-    static constexpr int XR = G3Y + 2 * H, XC = G3X + 2 * H;      // staged tile
+    static constexpr int CL = (H + 3) / 4 * 4;                    // column halo rounded to 16 B (float4 staging)
+    static constexpr int XR = G3Y + 2 * H, XC = G3X + 2 * CL;     // staged tile: rows ty0-H.., cols tx0-CL..
     static constexpr int WR = (G3Y + 2 * H + 2 * R) / MAG + 2;    // LR window bound (incl. border folds)
     static constexpr int WC = (G3X + 2 * H + 2 * R) / MAG + 2;
     static constexpr int NT = (KD + MAG - 1) / MAG;               // taps per axis in one residue class
@@ -57,8 +58,34 @@ template <int R, int MAG>
 __device__ __forceinline__ void g3_stage(const StencilParams& sp, const float* __restrict__ A,
                                          const float* __restrict__ B, float a, int ty0, int tx0, float* xs) {
     using T = G3<R, MAG>;
-    constexpr int RJ = (T::XR + 7) / 8, CQ = (T::XC + 31) / 32;
     const int w8 = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (tx0 - T::CL >= 0 && tx0 + G3X + T::CL <= sp.W) {
+        // interior columns: 16-byte loads (pitch and tx0 - CL are multiples of 4 floats), rows clamped
+        constexpr int C4 = T::XC / 4, N4 = T::XR * C4, J4 = (N4 + G3T - 1) / G3T;
+        float4 v4[J4];
+#pragma unroll
+        for (int j = 0; j < J4; ++j) {
+            const int e = threadIdx.x + j * G3T;
+            const int r = e / C4, c = (e - r * C4) * 4;
+            if (e < N4) {
+                const size_t o = (size_t)(clampi(ty0 - T::H + r, 0, sp.H - 1) - sp.store_lo) * sp.pitch + tx0 - T::CL + c;
+                const float4 xa = __ldg(reinterpret_cast<const float4*>(A + o));
+                if (B) {
+                    const float4 xb = __ldg(reinterpret_cast<const float4*>(B + o));
+                    v4[j] = make_float4(fmaf(a, xb.x, xa.x), fmaf(a, xb.y, xa.y), fmaf(a, xb.z, xa.z), fmaf(a, xb.w, xa.w));
+                } else {
+                    v4[j] = xa;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < J4; ++j) {
+            const int e = threadIdx.x + j * G3T;
+            if (e < N4) reinterpret_cast<float4*>(xs)[e] = v4[j];   // XC % 4 == 0: row-major float4 index
+        }
+        return;
+    }
+    constexpr int RJ = (T::XR + 7) / 8, CQ = (T::XC + 31) / 32;
     float v[RJ][CQ];
 #pragma unroll
     for (int j = 0; j < RJ; ++j) {
@@ -67,7 +94,7 @@ __device__ __forceinline__ void g3_stage(const StencilParams& sp, const float* _
 #pragma unroll
         for (int q = 0; q < CQ; ++q) {
             const int c = lane + 32 * q;
-            const size_t o = ro + clampi(tx0 - T::H + c, 0, sp.W - 1);
+            const size_t o = ro + clampi(tx0 - T::CL + c, 0, sp.W - 1);
             v[j][q] = (r < T::XR && c < T::XC) ? fmaf(a, __ldg(B + o), __ldg(A + o)) : 0.0f;
         }
     }
@@ -179,7 +206,7 @@ __device__ __forceinline__ void l2_prefetch_rows(const float* A, size_t pitch, i
 template <int PN, int R, int MAG, int BQ>
 __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, GenParams gp, Buffers b, int phase) {
     using T = G3<R, MAG>;
-    constexpr int KD = T::KD, HX = T::H, XC = T::XC, WC = T::WC, NT = T::NT;
+    constexpr int KD = T::KD, HX = T::H, CL = T::CL, XC = T::XC, WC = T::WC, NT = T::NT;
     extern __shared__ __align__(16) float g3s[];
     float* xs = g3s;                                   // XR x XC staged x'
     float* ws = xs + T::XR * XC;                       // FC x WR x WC rho' windows
@@ -266,7 +293,7 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
                     float d1 = 0.0f;
                     if (a >= 0 && a < gp.lr_h && bb >= 0 && bb < gp.lr_w) {
                         const float yv = yr[n];
-                        const float ev = g3_fwd<R, MAG>(tk, xs, MAG * a + sy - R - (ty0 - HX), MAG * bb + sx - R - (tx0 - HX)) - yv;
+                        const float ev = g3_fwd<R, MAG>(tk, xs, MAG * a + sy - R - (ty0 - HX), MAG * bb + sx - R - (tx0 - CL)) - yv;
                         float v;
                         if (PN == 2) {
                             v = ev * ev;
@@ -390,8 +417,8 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
             const int vy = vy0 + 4 * k;
             if (vy >= sp.H || vx >= sp.W) continue;
             float gb = 0.0f;
-            if (inner) btv_grad<BQ, true>(sp, gp, xs, XC, ry + 4 * k + HX, cx + HX, vy, vx, gb, acc[1]);
-            else btv_grad<BQ, false>(sp, gp, xs, XC, ry + 4 * k + HX, cx + HX, vy, vx, gb, acc[1]);
+            if (inner) btv_grad<BQ, true>(sp, gp, xs, XC, ry + 4 * k + HX, cx + CL, vy, vx, gb, acc[1]);
+            else btv_grad<BQ, false>(sp, gp, xs, XC, ry + 4 * k + HX, cx + CL, vy, vx, gb, acc[1]);
             const float rn = -fmaf(sp.lam, gb, g[k]);
             const size_t o = (size_t)(vy - sp.store_lo) * sp.pitch + vx;
             Rn[o] = rn;
@@ -406,7 +433,7 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
 template <int PN, int R, int MAG, int BQ>
 __global__ void __launch_bounds__(G3T, G3MINB_UC) k_gen3_uc(StencilParams sp, GenParams gp, Buffers b, int phase) {
     using T = G3<R, MAG>;
-    constexpr int KD = T::KD, HX = T::H, XC = T::XC;
+    constexpr int KD = T::KD, HX = T::H, CL = T::CL, XC = T::XC;
     extern __shared__ __align__(16) float g3s[];
     float* xs = g3s;                 // new x on the tile + halo
     float* ps = xs + T::XR * XC;     // new p
@@ -454,7 +481,7 @@ __global__ void __launch_bounds__(G3T, G3MINB_UC) k_gen3_uc(StencilParams sp, Ge
         for (int k = 0; k < G3PPT; ++k) {
             const int uy = ty0 + ry + 4 * k, ux = tx0 + cx;
             if (uy >= sp.H || ux >= sp.W) continue;
-            const int ly = ry + 4 * k + HX, lx = cx + HX;
+            const int ly = ry + 4 * k + HX, lx = cx + CL;
             const float xn = xs[ly * XC + lx], pn = ps[ly * XC + lx];
             const size_t o = (size_t)(uy - sp.store_lo) * sp.pitch + ux;
             Xn[o] = xn;
@@ -483,7 +510,7 @@ __global__ void __launch_bounds__(G3T, G3MINB_UC) k_gen3_uc(StencilParams sp, Ge
                 split(e, wc, inv, ra, cb);
                 const int a = alo + ra, bb = blo + cb;
                 const float yv = __ldg(yi + (size_t)a * gp.lr_w + bb);
-                const int r0 = MAG * a + sy - R - (ty0 - HX), c0 = MAG * bb + sx - R - (tx0 - HX);
+                const int r0 = MAG * a + sy - R - (ty0 - HX), c0 = MAG * bb + sx - R - (tx0 - CL);
                 const float ev = g3_fwd<R, MAG>(tk, xs, r0, c0) - yv;
                 const float ap = g3_fwd<R, MAG>(tk, ps, r0, c0);
                 if (PN == 2) {   // rho'' = 2: the affine factor
