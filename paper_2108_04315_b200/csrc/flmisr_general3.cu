@@ -29,8 +29,15 @@ namespace {
 
 constexpr int G3X = 64, G3Y = 32, G3T = 256, G3FC = 4;
 // resident CTAs per SM the fused kernels are compiled for (measured on G3: value+gradient 0.67 ms at 3
-// vs 0.72 at 4; update+curvature 0.32 at 3 vs 0.30 at 4)
-constexpr int G3MINB_VG = 3, G3MINB_UC = 4;
+// vs 0.72 at 4, and G3 53.8 proj/s at 3 vs 50.7 at 2 (profiles/r01_g3_minblocks_ab.txt); update+curvature
+// 0.32 at 3 vs 0.30 at 4)
+#ifndef FLMISR_G3MINB_VG
+#define FLMISR_G3MINB_VG 3
+#endif
+#ifndef FLMISR_G3MINB_UC
+#define FLMISR_G3MINB_UC 4
+#endif
+constexpr int G3MINB_VG = FLMISR_G3MINB_VG, G3MINB_UC = FLMISR_G3MINB_UC;   // tuning builds override
 constexpr int G3PPT = G3X * G3Y / G3T;   // 8 output pixels per thread: column t % 64, rows t / 64 + 4 k
 
 __device__ __forceinline__ int fdiv(int a, int m) { return a >= 0 ? a / m : -((-a + m - 1) / m); }
