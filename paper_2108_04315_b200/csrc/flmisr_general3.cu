@@ -42,6 +42,15 @@ constexpr int G3PPT = G3X * G3Y / G3T;   // 8 output pixels per thread: column t
 
 __device__ __forceinline__ int fdiv(int a, int m) { return a >= 0 ? a / m : -((-a + m - 1) / m); }
 __device__ __forceinline__ int cdiv(int a, int m) { return -fdiv(-a, m); }
+// floor / ceil division by the compile-time magnification: an arithmetic shift when MAG is a power of two
+__host__ __device__ constexpr int ilog2c(int m) { return m <= 1 ? 0 : 1 + ilog2c(m / 2); }
+template <int M>
+__device__ __forceinline__ int fdivc(int a) {
+    if constexpr ((M & (M - 1)) == 0) return a >> ilog2c(M);
+    else return fdiv(a, M);
+}
+template <int M>
+__device__ __forceinline__ int cdivc(int a) { return -fdivc<M>(-a); }
 __device__ __forceinline__ int pmod(int a, int m) { return ((a % m) + m) % m; }
 
 template <int R, int MAG>
@@ -269,8 +278,8 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
 #pragma unroll 1
             for (int f = 0; f < G3FC && i0 + f < gp.k; ++f) {
                 const int i = i0 + f, sy = gp.sy[i], sx = gp.sx[i];
-                const int alo = cdiv(vylo - sy - R - 1, MAG), ahi = fdiv(vyhi - sy + R, MAG);
-                const int blo = cdiv(vxlo - sx - R - 1, MAG), bhi = fdiv(vxhi - sx + R, MAG);
+                const int alo = cdivc<MAG>(vylo - sy - R - 1), ahi = fdivc<MAG>(vyhi - sy + R);
+                const int blo = cdivc<MAG>(vxlo - sx - R - 1), bhi = fdivc<MAG>(vxhi - sx + R);
                 const int wr = ahi - alo + 1, wc = bhi - blo + 1;
                 const float inv = 1.0f / (float)wc;
                 float tk[KD * KD];
@@ -321,7 +330,7 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
 #pragma unroll 1
             for (int f = 0; f < G3FC && i0 + f < gp.k; ++f) {
                 const int i = i0 + f, sy = gp.sy[i], sx = gp.sx[i];
-                const int alo = cdiv(vylo - sy - R - 1, MAG), blo = cdiv(vxlo - sx - R - 1, MAG);
+                const int alo = cdivc<MAG>(vylo - sy - R - 1), blo = cdivc<MAG>(vxlo - sx - R - 1);
                 const float* ti = ts + i * KD * KD;
                 const float* wf = ws + f * T::WR * WC;
                 const int uy = vy0 - sy, ux = vx - sx;   // frame-relative HR coordinates
@@ -385,7 +394,7 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
                     float gk = 0.0f;
                     for (int f = 0; f < G3FC && i0 + f < gp.k; ++f) {
                         const int i = i0 + f, sy = gp.sy[i], sx = gp.sx[i];
-                        const int alo = cdiv(vylo - sy - R - 1, MAG), blo = cdiv(vxlo - sx - R - 1, MAG);
+                        const int alo = cdivc<MAG>(vylo - sy - R - 1), blo = cdivc<MAG>(vxlo - sx - R - 1);
                         const float* ti = ts + i * KD * KD;
                         const float* wf = ws + f * T::WR * WC;
                         const int ylo = vy == 0 ? gp.fy_lo : vy, yhi = vy == sp.H - 1 ? gp.fy_hi : vy;
@@ -396,11 +405,11 @@ __global__ void __launch_bounds__(G3T, G3MINB_VG) k_gen3_vg(StencilParams sp, Ge
                                 for (int Pp = 0; Pp < KD; ++Pp) {
                                     const int ny = yy - sy - (Pp - R);
                                     if (pmod(ny, MAG)) continue;
-                                    const int a = fdiv(ny, MAG);
+                                    const int a = fdivc<MAG>(ny);
                                     for (int Qq = 0; Qq < KD; ++Qq) {
                                         const int nx = xx - sx - (Qq - R);
                                         if (pmod(nx, MAG)) continue;
-                                        const int bb = fdiv(nx, MAG);
+                                        const int bb = fdivc<MAG>(nx);
                                         all = fmaf(ti[Pp * KD + Qq], wf[(a - alo) * WC + bb - blo], all);
                                     }
                                 }
@@ -502,10 +511,10 @@ __global__ void __launch_bounds__(G3T, G3MINB_UC) k_gen3_uc(StencilParams sp, Ge
 #pragma unroll 1
         for (int i = 0; i < gp.k; ++i) {
             const int sy = gp.sy[i], sx = gp.sx[i];
-            const int alo = ty0 == 0 ? 0 : max(0, cdiv(ty0 - sy, MAG));
-            const int ahi = ty0 + G3Y >= sp.H ? gp.lr_h - 1 : min(gp.lr_h - 1, fdiv(ty0 + G3Y - 1 - sy, MAG));
-            const int blo = tx0 == 0 ? 0 : max(0, cdiv(tx0 - sx, MAG));
-            const int bhi = tx0 + G3X >= sp.W ? gp.lr_w - 1 : min(gp.lr_w - 1, fdiv(tx0 + G3X - 1 - sx, MAG));
+            const int alo = ty0 == 0 ? 0 : max(0, cdivc<MAG>(ty0 - sy));
+            const int ahi = ty0 + G3Y >= sp.H ? gp.lr_h - 1 : min(gp.lr_h - 1, fdivc<MAG>(ty0 + G3Y - 1 - sy));
+            const int blo = tx0 == 0 ? 0 : max(0, cdivc<MAG>(tx0 - sx));
+            const int bhi = tx0 + G3X >= sp.W ? gp.lr_w - 1 : min(gp.lr_w - 1, fdivc<MAG>(tx0 + G3X - 1 - sx));
             const int wr = ahi - alo + 1, wc = bhi - blo + 1;
             if (wr <= 0 || wc <= 0) continue;
             const float inv = 1.0f / (float)wc;
