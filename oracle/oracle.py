@@ -18,7 +18,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "flmisr_oracle.c")
-_LIB = os.path.join(_HERE, "libflmisr_oracle.so")
+# ORACLE_LIB: an alternative build of this source (tools/mutate_oracle.py points it at mutants)
+_LIB = os.environ.get("ORACLE_LIB", os.path.join(_HERE, "libflmisr_oracle.so"))
 
 
 def build(force: bool = False) -> str:
