@@ -71,6 +71,9 @@ typedef struct {
     int32_t scg_rules;   /* bit mask: 1 = PR+ restart (beta <- max(beta, 0)); 2 = Netlab scale
                             rules (delta = curv + lam |p|^2 each pass; lam x4 at Delta < 0.25, x1/2 at
                             Delta > 0.75, bounded to [1e-15, 1e100]); 0 = Moller literal (reading 11) */
+    int32_t x0_mode;     /* initial estimate when flmisr_reconstruct* gets x0 == NULL: 0 = bilinear
+                            upsample of frame 0 (reading 14); 1 = multi-image interpolation
+                            fusion (reading 24: the flmisr_interp_fuse image)                */
 } flmisr_config;
 
 typedef struct {
@@ -112,6 +115,23 @@ flmisr_status flmisr_plan(const flmisr_config* cfg, flmisr_plan_t* out);
  */
 flmisr_status flmisr_reconstruct(flmisr_plan_t plan, const float* lr_stack, const float* x0, float* hr_out,
                                  void* cuda_stream, flmisr_report* report);
+
+/*
+ * flmisr_interp_fuse: the paper's non-iterative baseline, multi-image interpolation fusion ("we
+ * inserted the pixel values of the LR images into the corresponding integer location in the HR grid";
+ * tab:runtime's "Multi-image interp." row; reading 24): every LR pixel of a frame with an
+ * integer HR phase is written at its HR site mag*(a,b) + s_i (the first such frame in index order wins);
+ * HR sites no frame covers keep the bilinear upsample of frame 0 (reading 14).  On a polyphase-complete
+ * stack every HR site holds exactly one LR pixel.
+ *   lr_stack  device pointer, k x lr_h x lr_w fp32 (caller-owned, read only)
+ *   hr_out    device pointer, H x W fp32 row-major (caller-owned, written)
+ *   cuda_stream  cudaStream_t the kernels are enqueued on (0 = the plan's stream); asynchronous
+ *             (no host synchronisation).  Uses the plan's scratch buffers: do not overlap it with a
+ *             reconstruction on the same plan.
+ * Errors: FLMISR_ERR_SHAPE on NULL pointers, FLMISR_ERR_CONFIG for a band plan (world > 1),
+ * FLMISR_ERR_CUDA on a launch failure.
+ */
+flmisr_status flmisr_interp_fuse(flmisr_plan_t plan, const float* lr_stack, float* hr_out, void* cuda_stream);
 
 /*
  * flmisr_reconstruct_async / flmisr_finish: the two halves of flmisr_reconstruct.  _async enqueues the
@@ -179,14 +199,19 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
  *   cooperative launch with local pointers in place of the peer mappings.  Arguments, output and report
  *   as flmisr_reconstruct_virtual.  FLMISR_ERR_CONFIG if the bands do not fit one cooperative wave.
  * flmisr_peer_export: a world > 1 plan (flmisr_plan) writes FLMISR_PEER_BLOB_BYTES bytes to out (host):
- *   CUDA IPC handles of its halo buffers and mailbox block.  The caller all-gathers the blobs of the
+ *   CUDA IPC handles of its halo buffers and mailbox block, its geometry (H, W, n_iter, halo, pitch), a
+ *   digest of its configuration and its device's PCI bus id.  The caller all-gathers the blobs of the
  *   world ranks (e.g. over the torch process group) in rank order.
  * flmisr_peer_connect: blobs = world x FLMISR_PEER_BLOB_BYTES bytes (host, rank order).  Maps every
  *   peer's mailbox block and the neighbours' halo buffers (same node, NVLink / NVSwitch), after which
  *   flmisr_reconstruct* on this plan runs the peer loop (the band gather to rank 0 stays on NCCL).
  *   Every rank of the group must call flmisr_reconstruct* the same number of times with the same
- *   n_iter.  Errors: FLMISR_ERR_CONFIG (not a streaming band plan, bad blobs, already connected),
- *   FLMISR_ERR_CUDA (IPC mapping failed, e.g. GPUs without peer access).
+ *   n_iter.  Errors: FLMISR_ERR_CONFIG (not a streaming band plan, bad blobs, already connected, a
+ *   peer that planned a different problem, a peer device without peer access or native peer
+ *   atomics), FLMISR_ERR_CUDA (IPC mapping failed).  On any error the plan stays on the NCCL
+ *   transport and remains usable.  Status: EXPERIMENTAL on real multi-GPU nodes -- the kernel code
+ *   is parity-tested in the single-device emulation (flmisr_reconstruct_virtual_peer); the IPC /
+ *   system-scope path has not run on more than one GPU in this repository's test environment.
  */
 #define FLMISR_PEER_BLOB_BYTES 256
 flmisr_status flmisr_reconstruct_virtual_peer(flmisr_plan_t* plans, int32_t g, const float* lr_stack,

@@ -20,35 +20,67 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
+STAMP = LIB + ".stamp"
+
+
+def _flags_key() -> str:
+    """The compile configuration a library was built with: tuning DEFS, arch and compiler.  A library
+    built with other flags (e.g. a tuning build written to the default path) is stale."""
+    import hashlib
+    return hashlib.sha256(repr((DEFS, ARCH, NVCC)).encode()).hexdigest()
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(STAMP) as f:
+            if f.read().strip() != _flags_key():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS + [__file__])
 
 
+OBJDIR = os.path.join(ROOT, "build", "obj")   # git-ignored object cache (incremental rebuilds)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
+    os.makedirs(OBJDIR, exist_ok=True)
+    key = _flags_key()[:12]
+    hdr_t = max(os.path.getmtime(h) for h in HEADERS + [__file__])
     objs, cmds = [], []
     for src in SOURCES:
-        obj = os.path.join(CSRC, os.path.basename(src) + "." + os.path.basename(LIB) + ".o")
+        obj = os.path.join(OBJDIR, f"{os.path.basename(src)}.{os.path.basename(LIB)}.{key}.o")
+        objs.append(obj)
+        # reuse an object built with the same flags after its source and every header last changed
+        if not force and not verbose and os.path.exists(obj) and \
+                os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
+            continue
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", *DEFS,
-               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", src, "-o", obj]
+               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c", src, "-o", obj + ".tmp"]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
-        cmds.append(cmd)
-        objs.append(obj)
+        cmds.append((cmd, obj))
+
+    def run(c):
+        subprocess.check_call(c[0])
+        os.replace(c[1] + ".tmp", c[1])
+
     # the translation units are independent: compile them concurrently
     from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
-        for _ in ex.map(subprocess.check_call, cmds):
-            pass
+    if cmds:
+        with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+            for _ in ex.map(run, cmds):
+                pass
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
+    with open(STAMP, "w") as f:
+        f.write(_flags_key() + "\n")
     return LIB
 
 

@@ -197,6 +197,8 @@ flmisr_status validate(const flmisr_config* c, bool virt) {
         return fail(FLMISR_ERR_CONFIG, "btv_alpha must be in (0, 1) (P:138, S:183)");
     if (c->btv_window < 1 || c->btv_window > MAXBW) return fail(FLMISR_ERR_CONFIG, "btv_window must be in [1, 3]");
     if (c->n_iter < 0) return fail(FLMISR_ERR_CONFIG, "n_iter must be >= 0");
+    if (c->x0_mode != 0 && c->x0_mode != 1)
+        return fail(FLMISR_ERR_CONFIG, "x0_mode must be 0 (bilinear frame 0) or 1 (interpolation fusion)");
     if (!(c->scg_lambda0 > 0.0) || !std::isfinite(c->scg_lambda0))
         return fail(FLMISR_ERR_CONFIG, "scg_lambda0 must be > 0 (S:362)");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(FLMISR_ERR_CONFIG, "need 0 <= rank < world");
@@ -692,6 +694,15 @@ flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float
     bool p_zeroed = false;
     if (x0) {
         CUDA_TRY(launch_hr_copy(x0 + (size_t)p->store_lo * p->W, p->W, 0, b.X[0], p->pitch, p->sp.perm, srows, p->W, s));
+    } else if (p->cfg.x0_mode == 1 && p->fast) {
+        // interpolation fusion on a polyphase-complete stack is the ingested Y itself (every HR site
+        // holds one LR pixel), band + halo rows, in the same buffer layout
+        CUDA_TRY(cudaMemcpyAsync(b.X[0], b.Y, p->hr_bytes, cudaMemcpyDeviceToDevice, s));
+    } else if (p->cfg.x0_mode == 1) {
+        // general path (world 1, natural layout): bilinear estimate, then the integer-phase frames'
+        // pixels on their sites from the plan's LR copy
+        CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s));
+        CUDA_TRY(launch_gen_interp(p->sp, p->gp, b.X[0], p->pitch, s));
     } else {   // the permuted-layout x0 kernel writes p0 = 0 in the same pass
         CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s, b.P[0]));
         p_zeroed = init_x0_zeroes_p(p->ip);
@@ -1119,12 +1130,34 @@ flmisr_status flmisr_reconstruct_virtual_peer(flmisr_plan_t* plans, int32_t g, c
 
 // What a rank publishes for its peers: IPC handles of its halo buffers and of its mailbox block, and
 // where its receive rows sit in the halo allocation.
+// The geometry fields and the configuration digest let every rank reject a peer that planned a
+// different problem (it would wait on barrier epochs that never come); the PCI bus id lets it check
+// that the peer device supports native peer atomics (the system-scope arrival counters).
 struct PeerBlob {
     uint32_t magic, rank, world, ctas;
     cudaIpcMemHandle_t halo, mbox;
     uint64_t recv_top_off, recv_bot_off;
+    uint32_t H, W, n_iter, eta, pitch, pad;
+    uint64_t cfg_digest;
+    char pci[32];
 };
 static_assert(sizeof(PeerBlob) <= FLMISR_PEER_BLOB_BYTES, "peer blob size");
+
+// FNV-1a over every numeric configuration field that shapes the SCG trajectory
+static uint64_t cfg_digest(const flmisr_config& c) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* d, size_t n) {
+        for (size_t i = 0; i < n; ++i) { h ^= ((const unsigned char*)d)[i]; h *= 1099511628211ull; }
+    };
+    const int32_t iv[] = {c.k, c.lr_h, c.lr_w, c.psf_h, c.psf_w, c.mag, c.p_norm, c.btv_window, c.n_iter,
+                          c.btv_offsets, c.curv_mode, c.scg_rules, c.x0_mode};
+    const double dv[] = {c.l1_eps, c.lambda, c.btv_alpha, c.scg_sigma0, c.scg_lambda0};
+    mix(iv, sizeof(iv));
+    mix(dv, sizeof(dv));
+    mix(c.shifts, sizeof(double) * 2 * (size_t)c.k);
+    mix(c.psf, sizeof(double) * (size_t)c.psf_h * c.psf_w);
+    return h;
+}
 
 flmisr_status flmisr_peer_export(flmisr_plan_t p, void* out) {
     if (!p || !out) return fail(FLMISR_ERR_SHAPE, "plan and out are required");
@@ -1139,6 +1172,10 @@ flmisr_status flmisr_peer_export(flmisr_plan_t p, void* out) {
     CUDA_TRY(cudaIpcGetMemHandle(&bl.mbox, p->peer_mem));
     bl.recv_top_off = p->recv_top ? (uint64_t)((char*)p->recv_top - (char*)p->halo_mem) : 0;
     bl.recv_bot_off = p->recv_bot ? (uint64_t)((char*)p->recv_bot - (char*)p->halo_mem) : 0;
+    bl.H = (uint32_t)p->H; bl.W = (uint32_t)p->W; bl.n_iter = (uint32_t)p->cfg.n_iter;
+    bl.eta = (uint32_t)p->eta; bl.pitch = (uint32_t)p->pitch;
+    bl.cfg_digest = cfg_digest(p->cfg);
+    CUDA_TRY(cudaDeviceGetPCIBusId(bl.pci, (int)sizeof(bl.pci), p->cfg.device));
     std::memset(out, 0, FLMISR_PEER_BLOB_BYTES);
     std::memcpy(out, &bl, sizeof(bl));
     return FLMISR_OK;
@@ -1157,6 +1194,26 @@ flmisr_status flmisr_peer_connect(flmisr_plan_t p, const void* blobs) {
         std::memcpy(&bl[q], (const char*)blobs + (size_t)q * FLMISR_PEER_BLOB_BYTES, sizeof(PeerBlob));
         if (bl[q].magic != 0x464c4d50u || (int)bl[q].rank != q || (int)bl[q].world != world)
             return fail(FLMISR_ERR_CONFIG, "peer blobs must be the world ranks' flmisr_peer_export outputs in rank order");
+        if ((int)bl[q].H != p->H || (int)bl[q].W != p->W || (int)bl[q].n_iter != p->cfg.n_iter ||
+            (int)bl[q].eta != p->eta || (int)bl[q].pitch != p->pitch || bl[q].cfg_digest != cfg_digest(p->cfg))
+            return fail(FLMISR_ERR_CONFIG, "peer rank " + std::to_string(q) +
+                                               " planned a different problem (geometry, n_iter or parameters differ)");
+    }
+    // the arrival counters are system-scope atomics on peer memory: every peer device must be
+    // reachable with native peer atomics (NVLink); a peer whose PCI id this process cannot resolve
+    // (not visible here) is accepted on the IPC mapping alone
+    for (int q = 0; q < world; ++q) {
+        if (q == rank) continue;
+        int pd = -1;
+        bl[q].pci[sizeof(bl[q].pci) - 1] = 0;
+        if (cudaDeviceGetByPCIBusId(&pd, bl[q].pci) != cudaSuccess) { cudaGetLastError(); continue; }
+        if (pd == p->cfg.device) return fail(FLMISR_ERR_CONFIG, "two ranks share one device");
+        int acc = 0, atom = 0;
+        CUDA_TRY(cudaDeviceGetP2PAttribute(&acc, cudaDevP2PAttrAccessSupported, p->cfg.device, pd));
+        CUDA_TRY(cudaDeviceGetP2PAttribute(&atom, cudaDevP2PAttrNativeAtomicSupported, p->cfg.device, pd));
+        if (!acc || !atom)
+            return fail(FLMISR_ERR_CONFIG, "peer device " + std::string(bl[q].pci) +
+                                               " lacks peer access or native peer atomics; use the NCCL transport");
     }
     for (int q = 0; q < world; ++q) {
         if (q == rank) {
@@ -1231,6 +1288,31 @@ flmisr_status flmisr_reconstruct_host(flmisr_plan_t p, const float* lr_host, flo
     st = flmisr_finish(p, report);
     if (hr_host && root && !direct) std::memcpy(hr_host, p->pin_out, nhr * sizeof(float));
     return st;
+}
+
+flmisr_status flmisr_interp_fuse(flmisr_plan_t p, const float* lr, float* out, void* cuda_stream) {
+    if (!p) return fail(FLMISR_ERR_SHAPE, "plan is NULL");
+    if (!lr || !out) return fail(FLMISR_ERR_SHAPE, "lr_stack and hr_out are required");
+    if (p->cfg.world != 1) return fail(FLMISR_ERR_CONFIG, "flmisr_interp_fuse needs a world == 1 plan");
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->stream;
+    const Buffers& b = p->b;
+    IngestParams ip0 = p->ip;
+    ip0.perm = 0;
+    if (p->fast) {   // polyphase-complete: every HR site holds exactly one LR pixel
+        CUDA_TRY(launch_ingest(ip0, lr, b.R[0], s));
+        CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, p->H, p->W, s));
+    } else {         // bilinear estimate everywhere, then the integer-phase frames' pixels on their sites
+        CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(p->gp.lr), lr,
+                                 (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(launch_init_x0(ip0, lr, b.R[0], s));
+        CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, p->H, p->W, s));
+        StencilParams sp0 = p->sp;
+        sp0.perm = 0;
+        CUDA_TRY(launch_gen_interp(sp0, p->gp, out, p->W, s));
+    }
+    return FLMISR_OK;
 }
 
 flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, const float* in0, const float* in1,

@@ -154,12 +154,17 @@ __device__ __forceinline__ const float* rrowp(const Buffers& b, const float* R, 
     return rowp(R, sp, row);
 }
 
+// Direct (non-ring) loads of the two warm-up rows of a segment.  Plain coherent loads, not
+// ld.global.nc: in the persistent loop kernels these rows were written earlier in the SAME launch by
+// other CTAs (x/p of the neighbouring segment) or by peer GPUs (r halo rows), and the non-coherent
+// path is only defined for data that is read-only for the whole kernel.  The grid barrier's acquire
+// orders them (PTX memory model: weak loads after an acquire observe the released stores).
 template <bool BORDER>
 __device__ __forceinline__ float4 ld4(const float* rp, int col, int W) {
-    if (!BORDER || col + 3 < W) return __ldg(reinterpret_cast<const float4*>(rp + col));
+    if (!BORDER || col + 3 < W) return *reinterpret_cast<const float4*>(rp + col);
     // right image border (W % 4 == 0): a group is either inside or wholly outside -> replicate col W-1
     // (column W-1 is the c3 slot of the last group, at the same physical place)
-    float v = __ldg(rp + (W - 1));
+    float v = rp[W - 1];
     return make_float4(v, v, v, v);
 }
 

@@ -39,6 +39,7 @@ class Config(C.Structure):
         ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("device", C.c_int32),
         ("btv_offsets", C.c_int32), ("curv_mode", C.c_int32), ("scg_rules", C.c_int32),
+        ("x0_mode", C.c_int32),
     ]
 
 
@@ -53,7 +54,7 @@ EXPORTS = ("flmisr_plan", "flmisr_reconstruct", "flmisr_reconstruct_async", "flm
            "flmisr_nccl_unique_id", "flmisr_plan_info", "flmisr_debug_apply", "flmisr_band",
            "flmisr_plan_virtual", "flmisr_reconstruct_virtual", "flmisr_pipeline_create",
            "flmisr_pipeline_submit", "flmisr_pipeline_wait", "flmisr_pipeline_destroy",
-           "flmisr_reconstruct_virtual_peer", "flmisr_peer_export", "flmisr_peer_connect")
+           "flmisr_reconstruct_virtual_peer", "flmisr_peer_export", "flmisr_peer_connect", "flmisr_interp_fuse")
 PEER_BLOB_BYTES = 256   # FLMISR_PEER_BLOB_BYTES
 
 
@@ -84,6 +85,7 @@ def _load():
     lib.flmisr_pipeline_submit.argtypes = [vp, vp, vp]
     lib.flmisr_pipeline_wait.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(Report)]
     lib.flmisr_pipeline_destroy.argtypes = [vp]
+    lib.flmisr_interp_fuse.argtypes = [vp, vp, vp, vp]
     for f in EXPORTS:
         if f == "flmisr_last_error":
             continue
@@ -137,14 +139,33 @@ def _stream_handle(stream, device):
     return C.c_void_p(h if h else 1)
 
 
-def _ptr(t):
+def _ptr(t, numel=None, device=None, what="buffer", dtype="float32"):
+    """Pointer of a contiguous torch tensor or numpy array.  numel: the element count the C ABI will
+    read or write; device: the CUDA ordinal a device tensor must live on (None: a host array is
+    expected).  A wrong dtype, device, size or layout raises ValueError before any C call."""
     if t is None:
         return None
     if hasattr(t, "data_ptr"):
         if not t.is_contiguous():
-            raise ValueError("tensor must be contiguous")
+            raise ValueError(f"{what}: tensor must be contiguous")
+        if str(t.dtype) != f"torch.{dtype}":
+            raise ValueError(f"{what}: dtype {t.dtype}, expected {dtype}")
+        if device is not None and (t.device.type != "cuda" or t.device.index != device):
+            raise ValueError(f"{what}: tensor on {t.device}, expected cuda:{device}")
+        if device is None and t.device.type != "cpu":
+            raise ValueError(f"{what}: tensor on {t.device}, expected a host tensor")
+        if numel is not None and t.numel() != numel:
+            raise ValueError(f"{what}: {t.numel()} elements, expected {numel}")
         return C.c_void_p(t.data_ptr())
     if isinstance(t, np.ndarray):
+        if device is not None:
+            raise ValueError(f"{what}: numpy array given where a cuda:{device} tensor is expected")
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{what}: array must be C-contiguous")
+        if t.dtype != np.dtype(dtype):
+            raise ValueError(f"{what}: dtype {t.dtype}, expected {dtype}")
+        if numel is not None and t.size != numel:
+            raise ValueError(f"{what}: {t.size} elements, expected {numel}")
         return t.ctypes.data_as(C.c_void_p)
     raise TypeError(type(t))
 
@@ -155,7 +176,7 @@ class Plan:
     def __init__(self, k, lr_h, lr_w, shifts, psf, mag=2, p_norm=1, l1_eps=1e-3, lam=0.05,
                  btv_alpha=0.4, btv_window=3, n_iter=20, scg_sigma0=1e-4, scg_lambda0=1e-6,
                  rank=0, world=1, nccl_id: bytes | None = None, device=0, virtual=False,
-                 btv_offsets=0, scg_rules=0, curv_mode=0):
+                 btv_offsets=0, scg_rules=0, curv_mode=0, x0_mode=0):
         self.shifts = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(k, 2))
         self.psf = np.ascontiguousarray(np.asarray(psf, dtype=np.float64))
         self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
@@ -163,7 +184,7 @@ class Plan:
                      self.psf.ctypes.data_as(C.POINTER(C.c_double)), self.psf.shape[0], self.psf.shape[1],
                      mag, p_norm, l1_eps, lam, btv_alpha, btv_window, n_iter, scg_sigma0, scg_lambda0,
                      rank, world, C.cast(self._id, C.c_void_p) if self._id is not None else None, device,
-                     btv_offsets, curv_mode, scg_rules)
+                     btv_offsets, curv_mode, scg_rules, x0_mode)
         self.k, self.lr_h, self.lr_w, self.mag, self.n_iter = k, lr_h, lr_w, mag, n_iter
         self.rank, self.world, self.device = rank, world, device
         self._pipes = weakref.WeakSet()   # pipelines driving this plan (destroyed first)
@@ -197,6 +218,22 @@ class Plan:
                     failed_stage=rep.failed_stage, failed_iter=rep.failed_iter,
                     trace=trace[: rep.iters_run + 1].copy())
 
+    # argument checks of the device entry points (include/flmisr.h: full LR frames in, x0 H x W,
+    # hr_out H x W on rank 0 / the owned band elsewhere, fp32, on the plan's device)
+    def _out_numel(self):
+        return self.H * self.W if self.rank == 0 or self.world == 1 else (self.row_hi - self.row_lo) * self.W
+
+    def _lr_ptr(self, t):
+        return _ptr(t, self.k * self.lr_h * self.lr_w, self.device, "lr_stack")
+
+    def _hr_ptr(self, t, what):
+        return _ptr(t, self.H * self.W, self.device, what)
+
+    def _out_ptr(self, t):
+        if t is not None and t.numel() == self.H * self.W:
+            return _ptr(t, self.H * self.W, self.device, "hr_out")
+        return _ptr(t, self._out_numel(), self.device, "hr_out")
+
     def reconstruct(self, lr_stack, x0=None, out=None, stream=None, raise_numeric=True):
         """flmisr_reconstruct on device tensors: lr_stack (k, lr_h, lr_w) fp32 CUDA; returns (hr, report)."""
         import torch
@@ -205,15 +242,26 @@ class Plan:
         trace = np.zeros((self.n_iter + 1, 6))
         rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
         s = _stream_handle(stream, lr_stack.device)
-        st = _lib.flmisr_reconstruct(self._h, _ptr(lr_stack), _ptr(x0), _ptr(out), s, C.byref(rep))
+        st = _lib.flmisr_reconstruct(self._h, self._lr_ptr(lr_stack), self._hr_ptr(x0, "x0"),
+                                     self._out_ptr(out), s, C.byref(rep))
         if st != OK and (raise_numeric or st != ERR_NUMERIC):
             _check(st)
         return out, self._report(rep, trace)
 
+    def interp_fuse(self, lr_stack, out=None, stream=None):
+        """flmisr_interp_fuse: the multi-image interpolation fusion image (asynchronous on `stream`)."""
+        import torch
+        if out is None:
+            out = torch.empty((self.H, self.W), dtype=torch.float32, device=lr_stack.device)
+        _check(_lib.flmisr_interp_fuse(self._h, self._lr_ptr(lr_stack), self._hr_ptr(out, "hr_out"),
+                                       _stream_handle(stream, lr_stack.device)))
+        return out
+
     def reconstruct_async(self, lr_stack, out, x0=None, stream=None):
         """flmisr_reconstruct_async: enqueue only; pair with finish()."""
         s = _stream_handle(stream, lr_stack.device)
-        _check(_lib.flmisr_reconstruct_async(self._h, _ptr(lr_stack), _ptr(x0), _ptr(out), s))
+        _check(_lib.flmisr_reconstruct_async(self._h, self._lr_ptr(lr_stack), self._hr_ptr(x0, "x0"),
+                                             self._out_ptr(out), s))
 
     def finish(self, raise_numeric=True):
         trace = np.zeros((self.n_iter + 1, 6))
@@ -237,12 +285,15 @@ class Plan:
             out = np.empty((self.H, self.W), dtype=np.float32)
         trace = np.zeros((self.n_iter + 1, 6))
         rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
-        _check(_lib.flmisr_reconstruct_host(self._h, _ptr(lr), _ptr(out), C.byref(rep)))
+        _check(_lib.flmisr_reconstruct_host(self._h, _ptr(lr, self.k * self.lr_h * self.lr_w, what="lr_stack"),
+                                            _ptr(out, self._out_numel(), what="hr_out"), C.byref(rep)))
         return out, self._report(rep, trace)
 
     def debug(self, op: int, lr=None, in0=None, in1=None, out=None):
         sc = (C.c_double * 4)()
-        _check(_lib.flmisr_debug_apply(self._h, op, _ptr(lr), _ptr(in0), _ptr(in1), _ptr(out), sc))
+        d = self.device
+        _check(_lib.flmisr_debug_apply(self._h, op, _ptr(lr, self.k * self.lr_h * self.lr_w, d, "lr"),
+                                       _ptr(in0, None, d, "in0"), _ptr(in1, None, d, "in1"), _ptr(out, None, d, "out"), sc))
         return list(sc)
 
 
@@ -253,8 +304,15 @@ def peer_connect(plan: "Plan", group=None) -> None:
     the band's whole SCG loop as one persistent kernel synchronised through peer memory."""
     import torch.distributed as dist
     blob = C.create_string_buffer(PEER_BLOB_BYTES)
-    _check(_lib.flmisr_peer_export(plan._h, C.cast(blob, C.c_void_p)))
-    blobs = gather_blobs(bytes(blob.raw), dist.get_world_size(group), group)
+    st = _lib.flmisr_peer_export(plan._h, C.cast(blob, C.c_void_p))
+    err = None if st == OK else (st, last_error())
+    # every rank takes part in the gather even if its export failed (an all-zero blob), so no rank is
+    # left waiting in the collective; then every rank sees the same failure
+    blobs = gather_blobs(bytes(blob.raw) if err is None else bytes(PEER_BLOB_BYTES), dist.get_world_size(group), group)
+    if err is not None:
+        raise FlmisrError(*err)
+    if any(b == bytes(PEER_BLOB_BYTES) for b in blobs):
+        raise FlmisrError(ERR_CONFIG, "peer export failed on another rank")
     allb = C.create_string_buffer(b"".join(blobs), len(blobs) * PEER_BLOB_BYTES)
     _check(_lib.flmisr_peer_connect(plan._h, C.cast(allb, C.c_void_p)))
 
@@ -280,7 +338,8 @@ def reconstruct_virtual_peer(plans, lr_stack, x0=None, out=None):
     trace = np.zeros((p0.n_iter + 1, 6))
     rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
     torch.cuda.current_stream(lr_stack.device).synchronize()
-    _check(_lib.flmisr_reconstruct_virtual_peer(arr, len(plans), _ptr(lr_stack), _ptr(x0), _ptr(out), C.byref(rep)))
+    _check(_lib.flmisr_reconstruct_virtual_peer(arr, len(plans), p0._lr_ptr(lr_stack), p0._hr_ptr(x0, "x0"),
+                                                p0._hr_ptr(out, "hr_out"), C.byref(rep)))
     return out, p0._report(rep, trace)
 
 
@@ -295,7 +354,8 @@ def reconstruct_virtual(plans, lr_stack, x0=None, out=None):
     trace = np.zeros((p0.n_iter + 1, 6))
     rep = Report(0, 0, 0, 0, 0, trace.ctypes.data_as(C.POINTER(C.c_double)))
     torch.cuda.current_stream(lr_stack.device).synchronize()
-    _check(_lib.flmisr_reconstruct_virtual(arr, len(plans), _ptr(lr_stack), _ptr(x0), _ptr(out), C.byref(rep)))
+    _check(_lib.flmisr_reconstruct_virtual(arr, len(plans), p0._lr_ptr(lr_stack), p0._hr_ptr(x0, "x0"),
+                                           p0._hr_ptr(out, "hr_out"), C.byref(rep)))
     return out, p0._report(rep, trace)
 
 
@@ -307,6 +367,7 @@ class Pipeline:
     def __init__(self, plan: Plan, depth: int = 2, input_u16: bool = False, u16_scale: float = 1.0 / 65535.0):
         self.plan = plan
         self.depth = depth
+        self._in_dtype = "uint16" if input_u16 else "float32"
         self._h = C.c_void_p()
         _check(_lib.flmisr_pipeline_create(plan._h, depth, int(input_u16), u16_scale, C.byref(self._h)))
         plan._pipes.add(self)
@@ -315,7 +376,9 @@ class Pipeline:
 
     def submit(self, lr_host, hr_host=None):
         slot = self._n % self.depth
-        _check(_lib.flmisr_pipeline_submit(self._h, _ptr(lr_host), _ptr(hr_host)))
+        p = self.plan
+        _check(_lib.flmisr_pipeline_submit(self._h, _ptr(lr_host, p.k * p.lr_h * p.lr_w, None, "lr_host", self._in_dtype),
+                                           _ptr(hr_host, p.H * p.W, None, "hr_host")))
         self._keep[slot] = (lr_host, hr_host)
         self._n += 1
 

@@ -126,6 +126,75 @@ def make_stack(lr: int, mag: int, seed: int, sigma_n: float = 1.0 / 255.0, lr_w:
     return y, sh, truth
 
 
+def box_aperture_psf(mag: int) -> np.ndarray:
+    """The detector aperture detector_stack integrates over, as a centred odd PSF on the HR grid
+    (reading 1: a box aperture, when wanted, is part of the PSF argument): outer(b, b) with
+    b = [1/2, 1, ..., 1, 1/2] / mag for even mag (mag + 1 taps), ones(mag) / mag for odd mag."""
+    b = np.ones(mag) / mag if mag % 2 else np.concatenate([[0.5], np.ones(mag - 1), [0.5]]) / mag
+    return np.outer(b, b)
+
+
+# ---- "natural-like" ground truths for the SR-vs-interpolation quality protocol (tab:natural,
+# P:388-395; SPEC AC6 S:533 "natural/synthetic images <= 1024^2").  Values in [0.05, 0.95].
+def dead_leaves(n: int, seed: int, rmin: float = 2.0, rmax: float = 80.0, count: int = 6000) -> np.ndarray:
+    """Occluding discs with power-law radii (density ~ r^-3) and uniform grey levels: the classic
+    scale-invariant model of natural-image statistics (edges at every scale and orientation)."""
+    rng = np.random.default_rng(seed)
+    img = np.full((n, n), np.nan)
+    u = rng.uniform(size=count)
+    rad = (rmin ** -2 - u * (rmin ** -2 - rmax ** -2)) ** -0.5
+    for k in range(count):
+        cy, cx = rng.uniform(-rmax, n + rmax, 2)
+        g = rng.uniform(0.05, 0.95)
+        r = rad[k]
+        y0, y1 = int(max(0, cy - r)), int(min(n, cy + r + 1))
+        x0, x1 = int(max(0, cx - r)), int(min(n, cx + r + 1))
+        if y0 >= y1 or x0 >= x1:
+            continue
+        yy, xx = np.mgrid[y0:y1, x0:x1]
+        sub = img[y0:y1, x0:x1]
+        m = ((yy - cy) ** 2 + (xx - cx) ** 2 <= r * r) & np.isnan(sub)
+        sub[m] = g
+    img[np.isnan(img)] = 0.5
+    return img
+
+
+def pink_noise(n: int, seed: int, beta: float = 1.0) -> np.ndarray:
+    """Gaussian texture with a 1/f^beta amplitude spectrum (natural images: beta ~ 1)."""
+    rng = np.random.default_rng(seed)
+    f = np.fft.fftfreq(n)
+    r = np.hypot(f[None, :], f[:, None])
+    r[0, 0] = 1.0
+    spec = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / r ** beta
+    spec[0, 0] = 0.0
+    img = np.real(np.fft.ifft2(spec))
+    img = (img - img.min()) / (img.max() - img.min())
+    return 0.05 + 0.9 * img
+
+
+def resolution_chart(n: int, seed: int) -> np.ndarray:
+    """Siemens star (36 cycles), bar groups of periods 16 .. 2 HR px (the QRM bar pattern)
+    and random small rectangles (text-like detail) on a grey background."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.mgrid[0:n, 0:n].astype(np.float64)
+    img = np.full((n, n), 0.5)
+    cy = cx = 0.3 * n
+    th = np.arctan2(yy - cy, xx - cx)
+    rr = np.hypot(yy - cy, xx - cx)
+    inside = rr < 0.25 * n
+    img[inside] = ((np.sin(36 * th) > 0) * 0.7 + 0.15)[inside]
+    x = int(0.6 * n)
+    for i, per in enumerate([16, 12, 8, 6, 4, 3, 2]):
+        y0 = int(0.05 * n + i * 0.13 * n)
+        band = ((np.arange(int(0.35 * n)) // (per / 2)) % 2) * 0.7 + 0.15
+        img[y0:y0 + int(0.1 * n), x:x + len(band)] = band[None, :]
+    for _ in range(int(0.16 * n)):
+        y0, x0 = rng.integers(int(0.6 * n), n - 10), rng.integers(0, int(0.55 * n))
+        h, w = rng.integers(2, 9, 2)
+        img[y0:y0 + h, x0:x0 + w] = rng.uniform(0.05, 0.95)
+    return img
+
+
 def random_fields(shape, seed: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:
     """Uniform O(1) fp32 test field (per-operator parity inputs)."""
     rng = np.random.default_rng(seed)
