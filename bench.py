@@ -42,7 +42,7 @@ WORKLOADS = {
     "C2": "C2: K=4 LR 1024x1024 -> x2 SR 2048x2048 (4.2 MP HR), 50 SCG passes",
     "C3": "C3: K=4 LR 2048x2048 -> x2 SR 4096x4096 (16.8 MP HR), 20 SCG passes",
     "C4": "C4: K=9 LR 2048x2048 -> x3 SR 6144x6144 (37.7 MP HR), 20 SCG passes",
-    "G3": "G3: K=4 LR 2048x2048 at quarter-pixel shifts (general-geometry path) -> x2 4096x4096, 20 SCG passes",
+    "G3": "G3: K=4 LR 2048x2048 at quarter-pixel shifts (a composed kernel per frame; per-phase streaming path) -> x2 4096x4096, 20 SCG passes",
     "C6": "C6: K=4 LR 4096x4096 -> x2 SR 8192x8192 (67.1 MP HR), 20 SCG passes (the paper's largest case)",
 }
 # The paper's own single-GPU runtime for exactly this workload (BASELINE.md tab:runtime, P:435-437:
@@ -576,7 +576,7 @@ def run_flmisr(args):
     else:                # one cooperative kernel runs the whole loop (one GPU, or a band of the peer loop)
         loop_bytes = (BYTES_VALUE_GRAD * n_vg + BYTES_UPDATE_CURV * n_uc) * npx_rank
         loop_ms = vg["ms"] / max(vg["launches"], 1)
-        kname = "k_scg_peer_loop" if transport == "peer" else "k_scg_loop"
+        kname = "k_scg_peer_loop" if transport == "peer" else ("k_scg_loop4" if pl.fast_path == 4 else "k_scg_loop")
         roof = {"bound": "hbm", "achieved": loop_bytes / (loop_ms / 1000.0) / 1e9, "peak": peak, "unit": "GB/s",
                 "traffic": (traffic or {}).get("scg_loop"), "kernel": kname,
                 "algorithmic_bytes_per_launch": loop_bytes, "avg_launch_ms": loop_ms, "peak_source": peak_src}

@@ -13,9 +13,10 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("FLMISR_LIB", os.path.join(HERE, "libflmisr.so"))
 DEFS = os.environ.get("FLMISR_DEFS", "").split()   # e.g. "-DFLMISR_SWPB=4 -DFLMISR_SMINB=4" (tuning builds)
-SOURCES = [os.path.join(CSRC, f) for f in ("flmisr_kernels.cu", "flmisr_stream.cu", "flmisr_general.cu", "flmisr_general3.cu",
-                                                          "flmisr_api.cpp")]
-HEADERS = [os.path.join(CSRC, "flmisr_internal.h"), os.path.join(CSRC, "flmisr_common.cuh"), os.path.join(ROOT, "include", "flmisr.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("flmisr_kernels.cu", "flmisr_stream.cu", "flmisr_stream4.cu",
+                                          "flmisr_general.cu", "flmisr_general3.cu", "flmisr_api.cpp")]
+HEADERS = [os.path.join(CSRC, "flmisr_internal.h"), os.path.join(CSRC, "flmisr_common.cuh"),
+           os.path.join(CSRC, "flmisr_stream_common.cuh"), os.path.join(ROOT, "include", "flmisr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

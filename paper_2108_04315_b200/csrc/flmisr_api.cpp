@@ -101,6 +101,9 @@ struct flmisr_plan_s {
     int row_lo = 0, row_hi = 0, store_lo = 0, store_hi = 0;
     int fast = 0;
     int stream_path = 0;   // 1: register-streaming kernels (flmisr_stream.cu), 0: tiled kernels
+    int pc = 0;            // 1: per-phase streaming kernels (flmisr_stream4.cu): complete phases, kappa per frame
+    int all_int = 0;       // 1: every frame's HR shift mag * shift_i is integral
+    PcTaps pct{};          // their taps per phase class
     int virt = 0;          // 1: band of an in-process virtual group (flmisr_reconstruct_virtual), no NCCL
     float* halo_mem = nullptr;   // send/recv halo rows (world > 1)
     StencilParams sp{};
@@ -223,6 +226,8 @@ extern "C" {
 
 const char* flmisr_last_error(void) { return g_last_error.c_str(); }
 
+static int world_of(const flmisr_config& c) { return c.world; }
+
 static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, bool virt) {
     if (!out) return fail(FLMISR_ERR_CONFIG, "out is NULL");
     *out = nullptr;
@@ -252,6 +257,24 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         else frame_of_phase[ph] = i;
     }
     if (std::getenv("FLMISR_FORCE_GENERAL") || c.btv_offsets == 1 || c.curv_mode == 1) fast = false;
+    // per-phase path (flmisr_stream4.cu): x2 with K = 4 frames whose integer phases tile [0,2)^2 but whose
+    // composed kernels differ (sub-pixel remainders per frame), PSF <= 3x3, one GPU: the polyphase Y with a
+    // 4x4 kernel per phase class runs on streaming kernels instead of the general path
+    bool pc = false;
+    if (!fast && mag == 2 && K == 4 && std::max(c.psf_h, c.psf_w) <= 3 && c.world == 1 && !virt &&
+        c.btv_offsets == 0 && c.curv_mode == 0 && (c.lr_w % 2) == 0 && c.lr_w >= 4 && c.lr_h >= 4 &&
+        !std::getenv("FLMISR_FORCE_GENERAL") && !std::getenv("FLMISR_NO_PC")) {
+        int seen[4] = {-1, -1, -1, -1};
+        pc = true;
+        for (int i = 0; i < K && pc; ++i) {
+            if (sy[i] < 0 || sy[i] > 1 || sx[i] < 0 || sx[i] > 1 || seen[sy[i] * 2 + sx[i]] >= 0) pc = false;
+            else seen[sy[i] * 2 + sx[i]] = i;
+        }
+        if (pc) {
+            for (int ph = 0; ph < 4; ++ph) frame_of_phase[ph] = seen[ph];
+            fast = true;
+        }
+    }
     if (!fast && c.world > 1)
         return fail(FLMISR_ERR_CONFIG,
                     "row-band partitioning (world > 1) needs the polyphase fast path (K = mag^2 frames with distinct "
@@ -259,7 +282,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
                     "one GPU per projection");
     if (!fast && K > GMAXK) return fail(FLMISR_ERR_CONFIG, "the general-geometry path supports k <= 64 frames");
     const bool frac = (fy0 != 0.0 || fx0 != 0.0);
-    const int kr = fast ? (frac ? R + 1 : R) : R + 1;
+    const int kr = pc ? R + 1 : (fast ? (frac ? R + 1 : R) : R + 1);
     if (fast && kr > MAXKR) return fail(FLMISR_ERR_CONFIG, "kappa radius exceeds 3");
     if (c.world > 1 && !virt && !nccl().ok) return fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded");
 
@@ -271,6 +294,27 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     p->cfg.psf = p->psf.data();
     p->cfg.nccl_unique_id = nullptr;
     p->fast = fast ? 1 : 0;
+    p->pc = pc ? 1 : 0;
+    p->all_int = 1;
+    for (int i = 0; i < 2 * K; ++i)
+        if (mag * c.shifts[i] != std::floor(mag * c.shifts[i])) p->all_int = 0;
+    if (c.x0_mode == 1 && world_of(c) > 1 && !p->all_int) {
+        delete p;
+        return fail(FLMISR_ERR_CONFIG, "x0_mode = 1 with fractional HR shifts needs world == 1");
+    }
+    if (pc) {   // kappa of each phase class, offsets [-R, R+1] placed in the 4x4 window [-1, 2]
+        for (int ph = 0; ph < 4; ++ph) {
+            std::vector<double> kap;
+            int syi, sxi;
+            double fy, fx;
+            composed_taps(c, frame_of_phase[ph], kap, syi, sxi, fy, fx);
+            const int KD = 2 * R + 2;
+            for (int j = 0; j < 16; ++j) p->pct.k[ph][j] = 0.0f;
+            for (int P = -R; P <= R + 1; ++P)
+                for (int Q = -R; Q <= R + 1; ++Q)
+                    p->pct.k[ph][(P + 1) * 4 + (Q + 1)] = (float)kap[(size_t)(P + R) * KD + (Q + R)];
+        }
+    }
     p->virt = virt ? 1 : 0;
     p->no_graph = std::getenv("FLMISR_NO_GRAPH") != nullptr;
     p->H = mag * c.lr_h;
@@ -356,12 +400,14 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 3; ++j) err = std::max(err, std::fabs(K3[i * 3 + j] - a3[i] * b3[j]));
         const bool separable = kr <= 1 && err <= 1e-12 * std::fabs(K3[pm]);
-        p->stream_path = fast && separable && (p->W % 4 == 0) && p->W >= 8 && p->H >= 4 &&
-                         std::getenv("FLMISR_FORCE_TILED") == nullptr;
+        p->stream_path = (fast && separable && (p->W % 4 == 0) && p->W >= 8 && p->H >= 4 &&
+                          std::getenv("FLMISR_FORCE_TILED") == nullptr) || pc;
         if (p->stream_path) {
             for (int i = 0; i < 3; ++i) { sp.ka[i] = (float)a3[i]; sp.kb[i] = (float)b3[i]; }
             sp.wpb = SWPB;
-            sp.nstrips = 1 + (p->W > SCOLS - SHALO ? (p->W - (SCOLS - SHALO) + SSTEP - 1) / SSTEP : 0);
+            // strips of SCOLS columns stepping by SSTEP (common kappa) or PC_SSTEP (per-phase kernels)
+            const int halo = pc ? (SCOLS - PC_SSTEP) / 2 : SHALO, step = SCOLS - 2 * halo;
+            sp.nstrips = 1 + (p->W > SCOLS - halo ? (p->W - (SCOLS - halo) + step - 1) / step : 0);
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device);
             // virtual bands share one device: each gets 1/world of the SMs (the peer-loop emulation runs
@@ -377,7 +423,12 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             if (const char* ev = std::getenv("FLMISR_EDGE_RATIO")) ratio = std::max(1.0, std::atof(ev));
             sp.ne = sp.nstrips >= 2 ? 2 : 1;
             sp.ni = sp.nstrips - sp.ne;
-            auto to1mod3 = [](int v) { v = std::max(v, 4); return v + ((1 - v % 3) + 3) % 3; };
+            // segment lengths: 1 mod 3 for the common-kappa kernels (row loop unrolled by 3), multiples of 4
+            // for the per-phase kernels (unrolled by 4; every segment starts on an even row)
+            auto to1mod3 = [pc](int v) {
+                v = std::max(v, 4);
+                return pc ? (v + 3) / 4 * 4 : v + ((1 - v % 3) + 3) % 3;
+            };
             auto nseg_int = [&](int Si, int Sb) {   // pieces of one interior strip
                 return rows <= 2 * Sb ? (rows + Sb - 1) / Sb : 2 + (rows - 2 * Sb + Si - 1) / Si;
             };
@@ -392,14 +443,14 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             int S = to1mod3(S0);
             int Sb = to1mod3((int)(S / ratio));
             while (S < rows && items(S, Sb) > cap) {
-                S += 3;
+                S += pc ? 4 : 3;
                 Sb = to1mod3((int)(S / ratio));
             }
             if (const char* ev = std::getenv("FLMISR_SEG_ROWS")) {   // tuning override (S = 1 mod 3), never
                 const int v = std::atoi(ev);                        // below the one-wave minimum
                 if (v >= 4 && to1mod3(v) > S) { S = to1mod3(v); Sb = to1mod3((int)(S / ratio)); }
             }
-            S = std::min(S, rows + ((1 - rows % 3) + 3) % 3);     // smallest >= rows with S = 1 mod 3
+            S = std::min(S, pc ? to1mod3(rows) : rows + ((1 - rows % 3) + 3) % 3);   // smallest admissible >= rows
             Sb = std::min(Sb, S);
             sp.seg_rows = S;
             sp.seg_b = Sb;
@@ -438,7 +489,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     ip.perm = sp.perm = p->stream_path;
     // streaming kernels on one GPU: per-CTA slots are reduced by every CTA of the next kernel instead of
     // by the last CTA of the producing one (no serial last-CTA tail)
-    sp.deferred = p->stream_path && c.world == 1 && std::getenv("FLMISR_NO_DEFER") == nullptr;
+    sp.deferred = p->stream_path && !pc && c.world == 1 && std::getenv("FLMISR_NO_DEFER") == nullptr;
 
     // ---- device memory ----
     auto cleanup_fail = [&](flmisr_status st) { flmisr_destroy(p); return st; };
@@ -644,7 +695,7 @@ flmisr_status flmisr_plan_info(flmisr_plan_t p, int32_t* H, int32_t* W, int32_t*
     if (W) *W = p->W;
     if (row_lo) *row_lo = p->row_lo;
     if (row_hi) *row_hi = p->row_hi;
-    if (fast_path) *fast_path = p->fast ? (p->stream_path ? 2 : 1) : (p->gp.fused ? 3 : 0);
+    if (fast_path) *fast_path = p->pc ? 4 : p->fast ? (p->stream_path ? 2 : 1) : (p->gp.fused ? 3 : 0);
     return FLMISR_OK;
 }
 
@@ -680,6 +731,30 @@ flmisr_status flmisr_destroy(flmisr_plan_t p) {
 
 namespace {
 
+// Multi-image interpolation fusion (reading 24) into dst (rows [0, H), pitch dpitch, layout dperm)
+// for a world == 1 plan: the bilinear frame-0 estimate, then every integer-phase frame's LR pixels on
+// their HR sites (first frame in index order wins), staged in the natural-layout scratch buffer.
+flmisr_status enqueue_interp(flmisr_plan_s* p, const float* lr, float* dst, int dpitch, int dperm, float* scratch,
+                             cudaStream_t s) {
+    IngestParams ip0 = p->ip;
+    ip0.perm = 0;
+    StencilParams sp0 = p->sp;
+    sp0.perm = 0;
+    GenParams gi{};
+    gi.k = p->cfg.k; gi.lr_h = p->cfg.lr_h; gi.lr_w = p->cfg.lr_w; gi.mag = p->cfg.mag;
+    gi.lr = lr;
+    for (int i = 0; i < p->cfg.k && i < GMAXK; ++i) {
+        const double ty = p->cfg.mag * p->cfg.shifts[2 * i], tx = p->cfg.mag * p->cfg.shifts[2 * i + 1];
+        gi.sy[i] = (int)std::floor(ty);
+        gi.sx[i] = (int)std::floor(tx);
+        gi.integer_phase[i] = ty == std::floor(ty) && tx == std::floor(tx);
+    }
+    CUDA_TRY(launch_init_x0(ip0, lr, scratch, s));
+    CUDA_TRY(launch_gen_interp(sp0, gi, scratch, p->pitch, s));
+    CUDA_TRY(launch_hr_copy(scratch, p->pitch, 0, dst, dpitch, dperm, p->H, p->W, s));
+    return FLMISR_OK;
+}
+
 // a1 polyphase ingest, a2 initial estimate (or the caller's x0), p0 = 0, r_old = 0, SCG state.
 flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float* x0, cudaStream_t s) {
     const Buffers& b = p->b;
@@ -694,15 +769,13 @@ flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float
     bool p_zeroed = false;
     if (x0) {
         CUDA_TRY(launch_hr_copy(x0 + (size_t)p->store_lo * p->W, p->W, 0, b.X[0], p->pitch, p->sp.perm, srows, p->W, s));
-    } else if (p->cfg.x0_mode == 1 && p->fast) {
-        // interpolation fusion on a polyphase-complete stack is the ingested Y itself (every HR site
-        // holds one LR pixel), band + halo rows, in the same buffer layout
+    } else if (p->cfg.x0_mode == 1 && p->fast && p->all_int) {
+        // interpolation fusion on a polyphase-complete stack of integer phases is the ingested Y itself
+        // (every HR site holds one LR pixel), band + halo rows, in the same buffer layout
         CUDA_TRY(cudaMemcpyAsync(b.X[0], b.Y, p->hr_bytes, cudaMemcpyDeviceToDevice, s));
-    } else if (p->cfg.x0_mode == 1) {
-        // general path (world 1, natural layout): bilinear estimate, then the integer-phase frames'
-        // pixels on their sites from the plan's LR copy
-        CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s));
-        CUDA_TRY(launch_gen_interp(p->sp, p->gp, b.X[0], p->pitch, s));
+    } else if (p->cfg.x0_mode == 1) {   // world 1 (plan check): staged through R[1], unused until the first pass
+        flmisr_status st = enqueue_interp(p, lr_stack, b.X[0], p->pitch, p->sp.perm, b.R[1], s);
+        if (st != FLMISR_OK) return st;
     } else {   // the permuted-layout x0 kernel writes p0 = 0 in the same pass
         CUDA_TRY(launch_init_x0(p->ip, lr_stack, b.X[0], s, b.P[0]));
         p_zeroed = init_x0_zeroes_p(p->ip);
@@ -720,12 +793,14 @@ flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float
 // the inner-outer border exchange of the r candidate.
 cudaError_t launch_vg(flmisr_plan_s* p, int phase, cudaStream_t s) {
     if (!p->fast) return launch_gen_value_grad(p->bw, p->pn, p->sp, p->gp, p->b, phase, s);
+    if (p->pc) return launch_pc_vg(p->bw, p->pn, p->sp, p->b, p->pct, phase, s);
     return p->stream_path ? launch_value_grad_stream(p->bw, p->pn, p->sp, p->b, phase, s)
                           : launch_value_grad(p->kr, p->bw, p->pn, p->sp, p->b, phase, s);
 }
 
 cudaError_t launch_uc(flmisr_plan_s* p, int phase, cudaStream_t s) {
     if (!p->fast) return launch_gen_update_curv(p->bw, p->pn, p->sp, p->gp, p->b, phase, s);
+    if (p->pc) return launch_pc_uc(p->bw, p->pn, p->sp, p->b, p->pct, phase, s);
     return p->stream_path ? launch_update_curv_stream(p->bw, p->pn, p->sp, p->b, phase, s)
                           : launch_update_curv(p->kr, p->bw, p->pn, p->sp, p->b, phase, s);
 }
@@ -823,7 +898,8 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
         p->prof_mode = 1;
     }
     if (p->persist && !looped) {   // one cooperative kernel for the init pass and all n_iter passes
-        cudaError_t le = launch_scg_loop_stream(p->bw, p->pn, p->sp, p->b, s);
+        cudaError_t le = p->pc ? launch_pc_loop(p->bw, p->pn, p->sp, p->b, p->pct, s)
+                               : launch_scg_loop_stream(p->bw, p->pn, p->sp, p->b, s);
         if (le == cudaSuccess) {
             looped = true;
             CUDA_TRY(mark());   // ev2: end of the loop kernel
@@ -1299,20 +1375,12 @@ flmisr_status flmisr_interp_fuse(flmisr_plan_t p, const float* lr, float* out, v
     const Buffers& b = p->b;
     IngestParams ip0 = p->ip;
     ip0.perm = 0;
-    if (p->fast) {   // polyphase-complete: every HR site holds exactly one LR pixel
+    if (p->fast && p->all_int) {   // polyphase-complete, integer phases: every HR site holds one LR pixel
         CUDA_TRY(launch_ingest(ip0, lr, b.R[0], s));
         CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, p->H, p->W, s));
-    } else {         // bilinear estimate everywhere, then the integer-phase frames' pixels on their sites
-        CUDA_TRY(cudaMemcpyAsync(const_cast<float*>(p->gp.lr), lr,
-                                 (size_t)p->cfg.k * p->cfg.lr_h * p->cfg.lr_w * sizeof(float),
-                                 cudaMemcpyDeviceToDevice, s));
-        CUDA_TRY(launch_init_x0(ip0, lr, b.R[0], s));
-        CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, p->H, p->W, s));
-        StencilParams sp0 = p->sp;
-        sp0.perm = 0;
-        CUDA_TRY(launch_gen_interp(sp0, p->gp, out, p->W, s));
+        return FLMISR_OK;
     }
-    return FLMISR_OK;
+    return enqueue_interp(p, lr, out, p->W, 0, b.R[0], s);
 }
 
 flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, const float* in0, const float* in1,
@@ -1350,6 +1418,9 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
             CUDA_TRY(launch_hr_copy(in0, p->W, 0, b.X[0], p->pitch, 0, H, p->W, s));
             if (gen) {
                 CUDA_TRY(launch_gen_forward(sp0, p->gp, b.X[0], out, s));
+            } else if (p->pc) {
+                CUDA_TRY(launch_pc_forward_debug(sp0, p->pct, b.X[0], b.R[0], s));
+                CUDA_TRY(launch_egest(ip0, b.R[0], out, s));
             } else {
                 CUDA_TRY(launch_forward_debug(p->kr, sp0, b.X[0], b.R[0], s));
                 CUDA_TRY(launch_egest(ip0, b.R[0], out, s));
@@ -1360,6 +1431,9 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
             if (gen) {
                 CUDA_TRY(cudaMemcpyAsync(p->gp.w, in0, lr_bytes, cudaMemcpyDeviceToDevice, s));
                 CUDA_TRY(launch_gen_adjoint(sp0, p->gp, p->gp.w, b.R[1], s));
+            } else if (p->pc) {
+                CUDA_TRY(launch_ingest(ip0, in0, b.R[0], s));
+                CUDA_TRY(launch_pc_adjoint_debug(sp0, p->pct, b.R[0], b.R[1], s));
             } else {
                 CUDA_TRY(launch_ingest(ip0, in0, b.R[0], s));
                 CUDA_TRY(launch_adjoint_debug(p->kr, sp0, b.R[0], b.R[1], s));
@@ -1386,14 +1460,12 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
             break;
         case FLMISR_OP_INTERP:
             if (!lr || !out) return fail(FLMISR_ERR_SHAPE, "INTERP needs lr and out");
-            if (gen) {   // bilinear estimate everywhere, then the integer-phase frames' pixels on their sites
-                CUDA_TRY(put_lr(lr));
-                CUDA_TRY(launch_init_x0(ip0, lr, b.R[0], s));
-                CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, H, p->W, s));
-                CUDA_TRY(launch_gen_interp(sp0, p->gp, out, p->W, s));
-            } else {     // polyphase-complete stack: every HR site holds exactly one LR pixel
+            if (p->fast && p->all_int) {   // polyphase-complete, integer phases: one LR pixel per HR site
                 CUDA_TRY(launch_ingest(ip0, lr, b.R[0], s));
                 CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, H, p->W, s));
+            } else {   // bilinear estimate everywhere, then the integer-phase frames' pixels on their sites
+                flmisr_status ist = enqueue_interp(p, lr, out, p->W, 0, b.R[0], s);
+                if (ist != FLMISR_OK) return ist;
             }
             break;
         case FLMISR_OP_X0:

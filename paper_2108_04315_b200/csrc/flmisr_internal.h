@@ -80,6 +80,13 @@ constexpr int SCOLS = 128;
 constexpr int SHALO = 2;
 constexpr int SSTEP = SCOLS - 2 * SHALO;
 
+// Per-phase streaming path (flmisr_stream4.cu): K = 4 frames at x2 with complete integer phases and a
+// composed kernel per frame; strips overlap by 4 columns per side.
+constexpr int PC_SSTEP = SCOLS - 8;
+struct PcTaps {
+    float k[4][16];              // kappa of phase class 2 (u mod 2) + (v mod 2) at [(P+1)*4 + (Q+1)], P, Q in [-1, 2]
+};
+
 struct Buffers {
     const float* Y;              // polyphase-interleaved LR stack on the HR grid (storage base)
     float* X[2];                 // x ping-pong
@@ -133,6 +140,13 @@ cudaError_t launch_settle(const StencilParams& sp, const Buffers& b, cudaStream_
 cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, cudaStream_t s);
 cudaError_t launch_scg_peer_loop(int bw, int pn, const StencilParams& sp, const Buffers& b, const PeerLoop& pl,
                                  const PeerBands* pb, cudaStream_t s);
+cudaError_t launch_pc_vg(int bw, int pn, const StencilParams& sp, const Buffers& b, const PcTaps& T, int phase,
+                         cudaStream_t s);
+cudaError_t launch_pc_uc(int bw, int pn, const StencilParams& sp, const Buffers& b, const PcTaps& T, int phase,
+                         cudaStream_t s);
+cudaError_t launch_pc_loop(int bw, int pn, const StencilParams& sp, const Buffers& b, const PcTaps& T, cudaStream_t s);
+cudaError_t launch_pc_forward_debug(const StencilParams& sp, const PcTaps& T, const float* x, float* z, cudaStream_t s);
+cudaError_t launch_pc_adjoint_debug(const StencilParams& sp, const PcTaps& T, const float* w, float* g, cudaStream_t s);
 cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s);  // world > 1
 cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s);   // world > 1
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,

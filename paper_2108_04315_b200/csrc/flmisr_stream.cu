@@ -31,239 +31,13 @@
 
 #include "flmisr_common.cuh"
 #include "flmisr_internal.h"
+#include "flmisr_stream_common.cuh"
 
 namespace flmisr {
 namespace {
 
 
-// ---- packed fp32x2 helpers (PTX f32x2 -> SASS FFMA2 / FADD2 / FMUL2 on sm_100a) ----
-__device__ __forceinline__ float2 F2(float a, float b) { return make_float2(a, b); }
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}\n"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    return d;
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}\n"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return d;
-}
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}\n"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return d;
-}
-__device__ __forceinline__ float2 fma2s(float s, float2 b, float2 c) { return fma2(F2(s, s), b, c); }
-__device__ __forceinline__ float2 mul2s(float s, float2 b) { return mul2(F2(s, s), b); }
-__device__ __forceinline__ float2 rsq2(float2 q) { return F2(rsq(q.x), rsq(q.y)); }
-__device__ __forceinline__ float2 lo2(const float4& v) { return F2(v.x, v.y); }   // (c0, c2)
-__device__ __forceinline__ float2 hi2(const float4& v) { return F2(v.z, v.w); }   // (c1, c3)
-
-// ---- per-warp TMA ring: cp.async.bulk (1D bulk copy engine) row segments -> shared memory ----
-constexpr int NST = 3;            // stages per warp (== the row-loop unroll)
-constexpr int NARR = 4;           // rows per stage (4 arrays)
-constexpr int RING_FLOATS = NST * NARR * SCOLS;
-// ring data + mbarriers, rounded to 128 B so every warp's ring (bulk-copy destination, 16-byte
-// shared-memory vector reads) stays aligned
-constexpr size_t RING_BYTES_PER_WARP = ((size_t)RING_FLOATS * 4 + NST * 8 + 127) / 128 * 128;
-constexpr size_t RING_SMEM = SWPB * RING_BYTES_PER_WARP;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint32_t bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
-    return ok != 0;
-}
-
-struct Ring {
-    const float* ptr;   // this warp's ring (generic pointer into shared memory)
-    uint32_t data;      // shared address of this warp's ring
-    uint32_t bars;      // shared address of its NST mbarriers
-    __device__ __forceinline__ void init(unsigned char* smem, int warp, int lane) {
-        unsigned char* base = smem + (size_t)warp * RING_BYTES_PER_WARP;
-        ptr = reinterpret_cast<const float*>(base);
-        data = smem_u32(base);
-        bars = smem_u32(base + (size_t)RING_FLOATS * 4);
-        if (lane == 0) {
-            for (int s = 0; s < NST; ++s) mbar_init(bars + 8 * s);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncwarp();
-    }
-    // whole (converged) warp: one elected lane arms stage s and issues its four 512-byte row copies;
-    // the addresses are warp-uniform, so no per-lane branch or register-to-uniform waterfall
-    __device__ __forceinline__ void issue(int s, const float* a0, const float* a1, const float* a2,
-                                          const float* a3) const {
-        const uint32_t bar = bars + 8 * s;
-        const uint32_t d = data + (uint32_t)(s * NARR * SCOLS * 4);
-        asm volatile(
-            "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\t"
-            "@P mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
-            "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], 512, [%0];\n\t"
-            "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%5], 512, [%0];\n\t"
-            "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%6], [%7], 512, [%0];\n\t"
-            "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%8], [%9], 512, [%0];\n\t}"
-            ::"r"(bar), "r"(NARR * SCOLS * 4), "r"(d), "l"(a0), "r"(d + SCOLS * 4), "l"(a1), "r"(d + 2 * SCOLS * 4),
-              "l"(a2), "r"(d + 3 * SCOLS * 4), "l"(a3)
-            : "memory");
-    }
-    __device__ __forceinline__ void wait(int s, uint32_t parity) const {
-        while (!mbar_try(bars + 8 * s, parity)) {
-        }
-    }
-    __device__ __forceinline__ float4 get(int s, int a, int lane) const {
-        return *reinterpret_cast<const float4*>(ptr + (s * NARR + a) * SCOLS + 4 * lane);
-    }
-    // all lanes: the stage's rows are consumed; order the generic-proxy reads before the async
-    // proxy refills the stage
-    __device__ __forceinline__ void release() const {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-    }
-};
-
-__device__ __forceinline__ const float* rowp(const float* base, const StencilParams& sp, int row) {
-    int r = min(max(row, sp.store_lo), sp.store_hi - 1);
-    return base + (size_t)(r - sp.store_lo) * sp.pitch;
-}
-
-// r rows for the update kernel: rows outside the owned band come from the received halo buffers
-// (inner-outer border exchange) when this rank has a neighbour on that side.
-__device__ __forceinline__ const float* rrowp(const Buffers& b, const float* R, const StencilParams& sp, int row) {
-    if (row < sp.row_lo && b.halo_top) {
-        int k = min(max(row - (sp.row_lo - b.eta), 0), b.eta - 1);
-        return b.halo_top + (size_t)k * sp.pitch;
-    }
-    if (row >= sp.row_hi && b.halo_bot) {
-        int k = min(max(row - sp.row_hi, 0), b.eta - 1);
-        return b.halo_bot + (size_t)k * sp.pitch;
-    }
-    return rowp(R, sp, row);
-}
-
-// Direct (non-ring) loads of the two warm-up rows of a segment.  Plain coherent loads, not
-// ld.global.nc: in the persistent loop kernels these rows were written earlier in the SAME launch by
-// other CTAs (x/p of the neighbouring segment) or by peer GPUs (r halo rows), and the non-coherent
-// path is only defined for data that is read-only for the whole kernel.  The grid barrier's acquire
-// orders them (PTX memory model: weak loads after an acquire observe the released stores).
-template <bool BORDER>
-__device__ __forceinline__ float4 ld4(const float* rp, int col, int W) {
-    if (!BORDER || col + 3 < W) return *reinterpret_cast<const float4*>(rp + col);
-    // right image border (W % 4 == 0): a group is either inside or wholly outside -> replicate col W-1
-    // (column W-1 is the c3 slot of the last group, at the same physical place)
-    float v = rp[W - 1];
-    return make_float4(v, v, v, v);
-}
-
-// store a lane's 4 columns given as the pairs A = (c0, c2), B = (c1, c3) in the permuted layout;
-// partial lanes (strip overlap) write only the output half (.x: c0,c1 / .y: c2,c3)
-__device__ __forceinline__ void stp(float* rp, float2 A, float2 B, bool olo, bool ohi) {
-    if (olo && ohi) {
-        *reinterpret_cast<float4*>(rp) = make_float4(A.x, A.y, B.x, B.y);
-    } else {
-        if (olo) { rp[0] = A.x; rp[2] = B.x; }
-        if (ohi) { rp[1] = A.y; rp[3] = B.y; }
-    }
-}
-
-struct Geo {
-    int lane, cbase, col0, r_lo, r_hi, w_lo, w_hi, llast;
-    bool strip0, live, border, rstrip;
-    bool olo, ohi;   // columns (c0, c1) / (c2, c3) of this lane are output columns of the strip
-    bool cv0, cv4;   // the lane's group / the right neighbour group lies inside the image
-};
-
-// cta: this CTA's index among the CTAs that share the band's work items (blockIdx.x, or the CTA's
-// index within its band in the peer loop)
-__device__ __forceinline__ Geo geometry(const StencilParams& sp, int cta) {
-    Geo g;
-    // warp index through a lane-0 shuffle so the compiler sees it (and every row pointer and the
-    // ring addresses derived from it) as warp-uniform: the bulk copies then take uniform-register
-    // operands directly instead of a per-copy R2UR waterfall
-    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-    g.lane = threadIdx.x & 31;
-    const int gw = cta * SWPB + warp;
-    g.live = gw < sp.nitems;
-    // work item -> (strip, rows [r_lo, r_hi)); see StencilParams: border pieces (band edges, edge
-    // strips) are seg_b rows, interior pieces seg_rows rows
-    int strip = 0, seg = 0, nseg = 1;
-    g.r_lo = g.r_hi = sp.row_lo;
-    if (g.live && gw < sp.n_int) {            // interior strip 1 .. ni: seg_b | seg_rows ... | seg_b
-        strip = 1 + gw % sp.ni;
-        seg = gw / sp.ni;
-        nseg = sp.nseg_i;
-        if (seg == 0) {
-            g.r_hi = min(sp.row_lo + sp.seg_b, sp.row_hi);
-        } else if (seg == nseg - 1) {
-            g.r_lo = max(sp.row_hi - sp.seg_b, sp.row_lo + sp.seg_b);
-            g.r_hi = sp.row_hi;
-        } else {
-            g.r_lo = sp.row_lo + sp.seg_b + (seg - 1) * sp.seg_rows;
-            g.r_hi = min(g.r_lo + sp.seg_rows, sp.row_hi - sp.seg_b);
-        }
-    } else if (g.live) {                      // edge strip 0 / nstrips-1: seg_b rows each
-        const int e = gw - sp.n_int;
-        strip = (sp.ne == 1 || (e & 1) == 0) ? 0 : sp.nstrips - 1;
-        seg = e / sp.ne;
-        nseg = sp.nseg_b;
-        g.r_lo = sp.row_lo + seg * sp.seg_b;
-        g.r_hi = min(g.r_lo + sp.seg_b, sp.row_hi);
-    }
-    g.cbase = strip * SSTEP;
-    g.col0 = g.cbase + 4 * g.lane;
-    g.strip0 = strip == 0;
-    const int oc_lo = g.strip0 ? 0 : g.cbase + SHALO;
-    const int oc_hi = (strip == sp.nstrips - 1) ? sp.W : min(g.cbase + SCOLS - SHALO, sp.W);
-    // strip bounds are at even offsets and W % 4 == 0, so (c0, c1) and (c2, c3) share their masks
-    g.olo = g.live && g.col0 >= oc_lo && g.col0 + 1 < oc_hi;
-    g.ohi = g.live && g.col0 + 2 >= oc_lo && g.col0 + 3 < oc_hi;
-    g.cv0 = g.col0 < sp.W;
-    g.cv4 = g.col0 + 4 < sp.W;
-    g.rstrip = g.cbase + SCOLS > sp.W;
-    g.llast = min(max((sp.W - 1 - g.cbase) >> 2, 0), 31);
-    if (!g.live) g.r_hi = g.r_lo;
-    // rows whose new x/p this segment writes: owned rows, plus the band's halo rows for the first /
-    // last segment of a band with a neighbour on that side (bit-identical to the neighbour's owned
-    // rows: same inputs, same fp32 operations)
-    g.w_lo = g.r_lo;
-    g.w_hi = g.r_hi;
-    if (g.live && seg == 0 && sp.row_lo > 0) g.w_lo = sp.store_lo;
-    if (g.live && seg == nseg - 1 && sp.row_hi < sp.H) g.w_hi = sp.store_hi;
-    // interior warps: no image border, every row they touch (r_lo - 2 .. r_hi + 2) is an owned row of
-    // the band, so they need no clamps, no halo buffers and no masks beyond the strip's output columns
-    g.border = g.strip0 || g.rstrip || g.r_lo < sp.row_lo + 3 || g.r_hi > sp.row_hi - 3;
-#ifdef FLMISR_ALL_BORDER   // tuning build: every warp takes the border instantiation
-    g.border = true;
-#endif
-    return g;
-}
-
-__device__ __forceinline__ float shup(float v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-__device__ __forceinline__ float shdn(float v) { return __shfl_down_sync(0xffffffffu, v, 1); }
-__device__ __forceinline__ float msum(float2 a, const Geo& g) { return (g.olo ? a.x : 0.f) + (g.ohi ? a.y : 0.f); }
-
-// right-border strip: lanes past the image take the replicated column W-1 (clamp, reading 4)
-template <bool BORDER>
-__device__ __forceinline__ float4 fixr(float4 v, const Geo& g) {
-    if (BORDER && g.rstrip) {
-        const float r = __shfl_sync(0xffffffffu, v.w, g.llast);
-        if (!g.cv0) v = make_float4(r, r, r, r);
-    }
-    return v;
-}
+// (shared helpers, the ring, warp geometry, the grid barrier: flmisr_stream_common.cuh)
 
 // ------------------------------------------------------------------------------------------------
 // value + gradient at x' = x + alpha p (Alg. 1 lines 14-19), streaming.
@@ -519,13 +293,6 @@ struct VG {
     }
 };
 
-// Programmatic dependent launch: the streaming kernels are launched with programmatic stream
-// serialization, so the next kernel's CTAs may be scheduled onto SMs this grid has already left;
-// every kernel waits for its predecessor's completion (and memory flush) before touching any data.
-__device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-}
 
 
 // ---- deferred reduction (sp.deferred): producers publish per-CTA slots, consumers settle them ----
@@ -945,101 +712,6 @@ __global__ void k_settle(StencilParams sp, Buffers b) {
 // shared-memory copy of the state (bit-identical in all CTAs), so no CTA waits on a serial last-CTA
 // reduction or on kernel teardown and relaunch.  CTA 0 writes the trace and the final state.
 // ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-#ifdef FLMISR_TIMING
-// diagnostic build only: per (phase, CTA): CTA work end, arrival, release, scalars done (globaltimer ns)
-__device__ unsigned long long g_loop_time[64 * 256 * 4];
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define FL_TMARK(ep, k) \
-    if (threadIdx.x == 0 && (ep) < 64 && blockIdx.x < 256) g_loop_time[((ep) * 256 + blockIdx.x) * 4 + (k)] = gtimer();
-#else
-#define FL_TMARK(ep, k)
-#endif
-
-__device__ __forceinline__ unsigned long long now_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-// grid-wide sum of acc over all threads of all CTAs in a fixed order; result in tot (all threads)
-__device__ void grid_sum(const double (&acc)[NSLOT], double* part, unsigned* gbar, unsigned epoch,
-                         double (&tot)[NSLOT]) {
-    __shared__ double sred[32][NSLOT];
-    __shared__ double stot[NSLOT];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int G = gridDim.x;
-    double* slot = part + (size_t)(epoch & 1) * NSLOT * G;   // double-buffered by phase parity
-#pragma unroll
-    for (int k = 0; k < NSLOT; ++k) {
-        const double v = warp_sum(acc[k]);
-        if (lane == 0) sred[warp][k] = v;
-    }
-    __syncthreads();
-    FL_TMARK(epoch, 0)
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < NSLOT; ++k) {
-            double v = 0.0;
-            for (int w = 0; w < nw; ++w) v += sred[w][k];
-            slot[(size_t)k * G + blockIdx.x] = v;
-        }
-        // release-reduction: this CTA's phase output (ordered before it by the barrier above,
-        // cumulativity) and its slots become visible to any CTA that acquires the count
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
-        FL_TMARK(epoch, 1)
-        const unsigned target = (epoch + 1) * (unsigned)G;
-        unsigned spins = 0;
-        const unsigned long long tstart = now_ns();
-        while (ld_acquire_u32(gbar) < target) {
-            // a lost CTA: fail loudly (after 10 s; a phase takes < 1 ms) instead of hanging the device
-            if ((++spins & 1023u) == 0 && now_ns() - tstart > 10000000000ull) __trap();
-        }
-        FL_TMARK(epoch, 2)
-    }
-    __syncthreads();
-    // every CTA: slot j of CTA j by thread j, fixed shuffle tree, fixed cross-warp order
-    double loc[NSLOT];
-#pragma unroll
-    for (int k = 0; k < NSLOT; ++k) loc[k] = 0.0;
-    for (int j = threadIdx.x; j < G; j += blockDim.x) {
-#pragma unroll
-        for (int k = 0; k < NSLOT; ++k) loc[k] += ld_relaxed_gpu(slot + (size_t)k * G + j);
-    }
-#pragma unroll
-    for (int k = 0; k < NSLOT; ++k) {
-        const double v = warp_sum(loc[k]);
-        if (lane == 0) sred[warp][k] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < NSLOT) {
-        double v = 0.0;
-        for (int w = 0; w < nw; ++w) v += sred[w][threadIdx.x];
-        stot[threadIdx.x] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < NSLOT; ++k) tot[k] = stot[k];
-    FL_TMARK(epoch, 3)
-    // the next phase reads other CTAs' generic-proxy stores through the bulk-copy (async) proxy
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-template <int WHICH>
-__device__ __forceinline__ void affine(const StencilParams& sp, double (&t)[NSLOT]) {
-    const double* aff = WHICH == 0 ? sp.aff_vg : sp.aff_uc;
-#pragma unroll
-    for (int k = 0; k < NSLOT; ++k) t[k] = t[k] * aff[k] + aff[NSLOT + k];
-}
 
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_loop(const __grid_constant__ StencilParams sp,

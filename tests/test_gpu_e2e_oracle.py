@@ -33,7 +33,7 @@ def rel(a, b):
 
 def _config(orc, name):
     c = synth.CONFIGS[name]
-    y, sh, _ = synth.make_stack(c["lr"], c["mag"], seed=c["seed"])
+    y, sh, _ = synth.make_stack(c["lr"], c["mag"], seed=c["seed"], shifts=c.get("shifts"))
     pb = orc.Problem(k=len(sh), lr_h=c["lr"], lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=c["mag"])
     xo, tr, st = orc.scg(pb, y.astype(np.float64), c["n_iter"])
     assert st["rc"] == 0
@@ -103,6 +103,18 @@ def test_c2_final_image_vs_oracle(orc):
         assert pl.fast_path == 2 and pl.loop_kernel
         hr, rep = pl.reconstruct(torch.from_numpy(ref["y"]).cuda())
         _check_against_oracle("C2 1 GPU", hr, rep, ref)
+
+
+def test_g3_final_image_vs_oracle(orc):
+    """G3 (C3's size, quarter-pixel detector positions: a composed kernel per frame) on the per-phase
+    streaming loop kernel bench.py --config G3 times, against orc.scg on the same stack."""
+    ref = _config(orc, "G3")
+    c = ref["c"]
+    with flmisr.Plan(k=4, lr_h=c["lr"], lr_w=c["lr"], shifts=ref["sh"], psf=synth.gaussian_psf(), mag=c["mag"],
+                     n_iter=c["n_iter"]) as pl:
+        assert pl.fast_path == 4 and pl.loop_kernel
+        hr, rep = pl.reconstruct(torch.from_numpy(ref["y"]).cuda())
+        _check_against_oracle("G3 1 GPU (per-phase kernels)", hr, rep, ref)
 
 
 def test_c1_converged_solution(orc):

@@ -79,17 +79,25 @@ def test_c3_reconstruction_properties(orc, c3):
     assert abs(J - f[-1]) <= 1e-5 * J
 
 
-@pytest.fixture(scope="module")
-def g3(orc):
-    """G3: C3's size at quarter-pixel shifts -- the fused general-geometry kernels bench.py --config G3
-    times (fast_path 3), against the oracle on the full image."""
+@pytest.fixture(scope="module", params=["per_phase", "fused_general"])
+def g3(orc, request):
+    """G3: C3's size at quarter-pixel shifts, against the oracle on the full image, on the per-phase
+    streaming kernels bench.py --config G3 times (fast_path 4) and on the fused general-geometry
+    kernels (FLMISR_NO_PC=1, fast_path 3)."""
+    import os
     c = synth.CONFIGS["G3"]
     sh = np.asarray(c["shifts"], dtype=np.float64)
-    pl = flmisr.Plan(k=len(sh), lr_h=c["lr"], lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=c["mag"],
-                     n_iter=c["n_iter"])
+    if request.param == "fused_general":
+        os.environ["FLMISR_NO_PC"] = "1"
+    try:
+        pl = flmisr.Plan(k=len(sh), lr_h=c["lr"], lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=c["mag"],
+                         n_iter=c["n_iter"])
+    finally:
+        os.environ.pop("FLMISR_NO_PC", None)
     pb = orc.Problem(k=len(sh), lr_h=c["lr"], lr_w=c["lr"], shifts=sh, psf=synth.gaussian_psf(), mag=c["mag"])
-    assert pl.fast_path == 3
-    return pl, pb
+    assert pl.fast_path == (4 if request.param == "per_phase" else 3)
+    yield pl, pb
+    pl.destroy()
 
 
 def test_g3_gradient_value_curvature_random_inputs(orc, g3):

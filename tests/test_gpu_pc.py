@@ -1,0 +1,164 @@
+"""Per-phase streaming path (flmisr_stream4.cu, fast_path 4) vs the fp64 oracle, through the C ABI.
+
+Polyphase-complete x2 stacks whose four frames carry different composed kernels kappa_i = h (*)
+bilinear(phi_i) (reading 19): quarter-pixel detector positions (G3's pattern), permuted frame order,
+a delta PSF (2x2 kappa), a non-separable PSF, p = 2, BTV windows 1..3, single and multiple 128-column
+strips with ragged tails.  Bars (north_star): per-operator relative L2 <= 1e-5 (and per-pixel max-abs
+on well-conditioned inputs), final image after 20 SCG passes <= 1e-3 with the same accept sequence."""
+import numpy as np
+import pytest
+
+from paper_2108_04315_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2108_04315_b200 import flmisr  # noqa: E402
+
+G3SH = np.array([[0.0, 0.0], [0.25, 0.5], [0.5, 0.25], [0.75, 0.75]])
+NONSEP = np.array([[0.02, 0.10, 0.05], [0.08, 0.40, 0.12], [0.03, 0.11, 0.09]])
+NONSEP = NONSEP / NONSEP.sum()
+CASES = {
+    # name: (lr_h, lr_w, psf, shifts, p_norm, lam, w)
+    "g3_one_strip": (40, 48, synth.gaussian_psf(), G3SH, 1, 0.05, 3),
+    "g3_strips": (75, 300, synth.gaussian_psf(), G3SH, 1, 0.05, 3),
+    "ragged": (37, 50, synth.gaussian_psf(), G3SH, 1, 0.05, 3),
+    "perm_order": (33, 62, synth.gaussian_psf(), np.array([[0.6, 0.5], [0.0, 0.2], [0.5, 0.05], [0.1, 0.6]]), 1, 0.05, 3),
+    "p2_w2": (30, 66, synth.gaussian_psf(0.7), G3SH, 2, 0.2, 2),
+    "delta_w1": (24, 36, synth.delta_psf(), G3SH, 1, 0.05, 1),
+    "nonsep": (41, 70, NONSEP, G3SH, 1, 0.05, 3),
+}
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def make(orc, name, n_iter=20):
+    lr_h, lr_w, psf, sh, pn, lam, w = CASES[name]
+    pl = flmisr.Plan(k=4, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=2, p_norm=pn, lam=lam, btv_window=w,
+                     n_iter=n_iter)
+    assert pl.fast_path == 4, pl.fast_path
+    pb = orc.Problem(k=4, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=2, p_norm=pn, lam=lam, btv_window=w)
+    return pl, pb
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_forward_adjoint(orc, name):
+    pl, pb = make(orc, name)
+    x = synth.random_fields((pb.H, pb.W), 1)
+    out = torch.zeros((4, pb.lr_h, pb.lr_w), device="cuda")
+    pl.debug(flmisr.OP_FORWARD, in0=dev(x), out=out)
+    ref = orc.forward(pb, x.astype(np.float64))
+    assert rel(out.cpu().numpy(), ref) <= 1e-5
+    w = synth.random_fields((4, pb.lr_h, pb.lr_w), 2, -1, 1)
+    outa = torch.zeros((pb.H, pb.W), device="cuda")
+    pl.debug(flmisr.OP_ADJOINT, in0=dev(w), out=outa)
+    assert rel(outa.cpu().numpy(), orc.adjoint(pb, w.astype(np.float64))) <= 1e-5
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_gradient_value_curvature_random(orc, name):
+    """The hot-loop kernels themselves (k_vg4 / k_uc4) on O(1) random fields."""
+    pl, pb = make(orc, name)
+    x = synth.random_fields((pb.H, pb.W), 3)
+    y = synth.random_fields((4, pb.lr_h, pb.lr_w), 4)
+    p = synth.random_fields((pb.H, pb.W), 7, -1, 1)
+    out = torch.zeros((pb.H, pb.W), device="cuda")
+    D, R, rr, _ = pl.debug(flmisr.OP_GRAD, lr=dev(y), in0=dev(x), out=out)
+    g = orc.grad(pb, x.astype(np.float64), y.astype(np.float64))
+    assert rel(out.cpu().numpy(), -g) <= 1e-5
+    Dr, Rr = orc.value(pb, x.astype(np.float64), y.astype(np.float64))
+    assert abs(D - Dr) <= 1e-5 * abs(Dr)
+    assert abs(R - Rr) <= 1e-5 * abs(Rr) + 1e-12
+    assert abs(rr - np.vdot(g, g)) <= 1e-5 * np.vdot(g, g)
+    delta, pp, mu, _ = pl.debug(flmisr.OP_CURV, lr=dev(y), in0=dev(x), in1=dev(p))
+    ref = orc.curv(pb, x.astype(np.float64), y.astype(np.float64), p.astype(np.float64))
+    from test_gpu_general import curv_rounding_bound
+    assert abs(delta - ref) <= 1e-5 * abs(ref) + curv_rounding_bound(orc, pb, x, y, p)
+    p64 = p.astype(np.float64)
+    assert abs(pp - np.vdot(p64, p64)) <= 1e-6 * np.vdot(p64, p64)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_pixelwise_well_conditioned(orc, name):
+    """Every pixel (image border rows/columns included) on inputs with |e| >= 20 eps; curvature at the
+    plain 1e-5 bar."""
+    pl, pb = make(orc, name)
+    from test_gpu_pixelwise import _inputs
+    x, y, p = _inputs(orc, pb, 21)
+    out = torch.zeros((pb.H, pb.W), device="cuda")
+    pl.debug(flmisr.OP_GRAD, lr=dev(y), in0=dev(x), out=out)
+    g = -orc.grad(pb, x.astype(np.float64), y.astype(np.float64))
+    err = np.abs(out.cpu().numpy().astype(np.float64) - g)
+    assert err.max() <= 1e-5 * np.abs(g).max(), np.unravel_index(np.argmax(err), err.shape)
+    delta, _, _, _ = pl.debug(flmisr.OP_CURV, lr=dev(y), in0=dev(x), in1=dev(p))
+    ref = orc.curv(pb, x.astype(np.float64), y.astype(np.float64), p.astype(np.float64))
+    assert abs(delta - ref) <= 1e-5 * abs(ref)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_reconstruct_matches_oracle(orc, name):
+    lr_h, lr_w, psf, sh, pn, lam, w = CASES[name]
+    truth = synth.phantom(2 * lr_h, 2 * lr_w, seed=91)
+    y = synth.detector_stack(truth, 2, sh, 1 / 255, seed=91).astype(np.float32)
+    pl, pb = make(orc, name, n_iter=20)
+    assert pl.loop_kernel   # the persistent loop kernel (k_scg_loop4)
+    hr, rep = pl.reconstruct(dev(y))
+    xo, tr, st = orc.scg(pb, y.astype(np.float64), 20)
+    assert rel(hr.cpu().numpy(), xo) <= 1e-3
+    assert rep["accepted"] == st["accepted"]
+    np.testing.assert_array_equal(rep["trace"][:, 5], tr[:, 5])
+    # f-trace bar: 1e-4, or 3x the oracle's own sensitivity to a 1e-7 relative perturbation of y when the
+    # problem is worse conditioned (delta_w1 has no BTV term: the pure Charbonnier-L1 objective moves its
+    # fp64 trace by 5e-3 under that perturbation -- DESIGN.md reading 23's rho'' regime)
+    y1 = y.astype(np.float64) * (1 + 1e-7 * np.random.default_rng(0).standard_normal(y.shape))
+    _, tr1, _ = orc.scg(pb, y1, 20)
+    sens = float(np.max(np.abs(tr1[:, 1] - tr[:, 1]) / np.abs(tr[:, 1])))
+    np.testing.assert_allclose(rep["trace"][:, 1], tr[:, 1], rtol=max(1e-4, 3 * sens))
+
+
+def test_per_phase_kernels_equal_loop(orc, monkeypatch):
+    """FLMISR_NO_PERSIST=1 (per-phase k_vg4 / k_uc4 in a CUDA graph) reproduces the loop kernel."""
+    lr_h, lr_w, psf, sh, pn, lam, w = CASES["g3_strips"]
+    y = synth.detector_stack(synth.phantom(2 * lr_h, 2 * lr_w, seed=92), 2, sh, 1 / 255, seed=92).astype(np.float32)
+    pl, _ = make(orc, "g3_strips", n_iter=15)
+    a, ra = pl.reconstruct(dev(y))
+    monkeypatch.setenv("FLMISR_NO_PERSIST", "1")
+    pk, _ = make(orc, "g3_strips", n_iter=15)
+    assert not pk.loop_kernel
+    b, rb = pk.reconstruct(dev(y))
+    np.testing.assert_array_equal(ra["trace"][:, 5], rb["trace"][:, 5])
+    np.testing.assert_allclose(ra["trace"][:, 1], rb["trace"][:, 1], rtol=1e-6)
+    assert rel(a.cpu().numpy(), b.cpu().numpy().astype(np.float64)) <= 1e-5
+
+
+def test_general_path_agrees(orc, monkeypatch):
+    """FLMISR_NO_PC=1 routes the same stack to the fused general kernels (fast_path 3): same result."""
+    lr_h, lr_w, psf, sh, pn, lam, w = CASES["g3_strips"]
+    y = synth.detector_stack(synth.phantom(2 * lr_h, 2 * lr_w, seed=93), 2, sh, 1 / 255, seed=93).astype(np.float32)
+    pl, _ = make(orc, "g3_strips")
+    a, ra = pl.reconstruct(dev(y))
+    monkeypatch.setenv("FLMISR_NO_PC", "1")
+    pg = flmisr.Plan(k=4, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=2, n_iter=20)
+    assert pg.fast_path == 3
+    b, rb = pg.reconstruct(dev(y))
+    np.testing.assert_array_equal(ra["trace"][:, 5], rb["trace"][:, 5])
+    assert rel(a.cpu().numpy(), b.cpu().numpy().astype(np.float64)) <= 1e-4
+
+
+def test_interp_and_x0_mode_fractional(orc):
+    """Interpolation fusion with fractional frames inserts only the integer-phase frame (reading 24)."""
+    lr_h, lr_w, psf, sh, pn, lam, w = CASES["perm_order"]
+    y = synth.random_fields((4, lr_h, lr_w), 94)
+    pl, pb = make(orc, "perm_order")
+    got = pl.interp_fuse(dev(y)).cpu().numpy()
+    np.testing.assert_allclose(got, orc.interp_fuse(pb, y.astype(np.float64)), rtol=0, atol=2e-6)
