@@ -404,7 +404,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
                           std::getenv("FLMISR_FORCE_TILED") == nullptr) || pc;
         if (p->stream_path) {
             for (int i = 0; i < 3; ++i) { sp.ka[i] = (float)a3[i]; sp.kb[i] = (float)b3[i]; }
-            sp.wpb = SWPB;
+            sp.wpb = pc ? PC_WPB : SWPB;
             // strips of SCOLS columns stepping by SSTEP (common kappa) or PC_SSTEP (per-phase kernels)
             const int halo = pc ? (SCOLS - PC_SSTEP) / 2 : SHALO, step = SCOLS - 2 * halo;
             sp.nstrips = 1 + (p->W > SCOLS - halo ? (p->W - (SCOLS - halo) + step - 1) / step : 0);
@@ -413,7 +413,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             // virtual bands share one device: each gets 1/world of the SMs (the peer-loop emulation runs
             // all bands in one cooperative launch)
             if (virt) nsm = std::max(1, nsm / world);
-            const long long cap = (long long)nsm * SMINB * sp.wpb;   // one wave of resident warps
+            const long long cap = (long long)nsm * (pc ? 1 : SMINB) * sp.wpb;   // one wave of resident warps
             const int rows = p->row_hi - p->row_lo;
             // Work items, one warp each, one wave.  Warps touching an image or band edge run the border
             // instantiation, ~1.4x slower per row (per-warp timing), so border pieces

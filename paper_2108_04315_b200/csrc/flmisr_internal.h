@@ -83,6 +83,10 @@ constexpr int SSTEP = SCOLS - 2 * SHALO;
 // Per-phase streaming path (flmisr_stream4.cu): K = 4 frames at x2 with complete integer phases and a
 // composed kernel per frame; strips overlap by 4 columns per side.
 constexpr int PC_SSTEP = SCOLS - 8;
+#ifndef FLMISR_PC_WPB
+#define FLMISR_PC_WPB 12
+#endif
+constexpr int PC_WPB = FLMISR_PC_WPB;    // warps per CTA of the per-phase kernels (one CTA per SM)
 struct PcTaps {
     float k[4][16];              // kappa of phase class 2 (u mod 2) + (v mod 2) at [(P+1)*4 + (Q+1)], P, Q in [-1, 2]
 };

@@ -32,7 +32,7 @@ namespace {
 constexpr int NS4 = 4;   // ring stages == row-loop unroll == x' window rows == pending rows
 constexpr int H4 = 4;    // strip column overlap per side
 using Ring4 = RingT<NS4>;
-constexpr size_t RING4_SMEM = RingDims<NS4>::SMEM;
+constexpr size_t RING4_SMEM = RingDims<NS4, PC_WPB>::SMEM;
 static_assert(SCOLS - 2 * H4 == PC_SSTEP, "per-phase strip step");
 
 // tap of phase class cls = 2 rho + gamma at offset (P, Q), P, Q in [-1, 2] (compile-time indices:
@@ -47,8 +47,10 @@ static_assert(SCOLS - 2 * H4 == PC_SSTEP, "per-phase strip step");
 // ------------------------------------------------------------------------------------------------
 template <int BW, int PN, bool BORDER>
 struct VG4 {
-    float2 XA[4], XB[4];            // x' pairs of the window rows (slot = (row - t0) & 3)
-    float XM[4], X4[4], X5[4];      // x' at c-1 (left lane's c3), c4, c5 (right lane's c0, c1)
+    // x' pairs of the window rows (slot = (row - t0) & 3), each formed once per row: M1 = (c-1, c1)
+    // (c-1 = the left lane's c3), A = (c0, c2), B = (c1, c3), D = (c2, c4), E = (c3, c5) (c4, c5 = the
+    // right lane's c0, c1): every kappa offset Q in [-1, 2] of both pixel pairs is one register pair
+    float2 XM1[4], XA[4], XB[4], XD[4], XE[4];
     float2 GA[4], GB[4], GD[4], GE[4];   // pending r at (c0,c2), (c1,c3), (c2,c4), (c3,c5)
     float2 accd, vb[4], rr, rro;    // .x: columns c0+c1, .y: columns c2+c3
     const float *ix, *ip, *iy, *ir; // interior warps: next rows to stage (strip start column)
@@ -84,13 +86,14 @@ struct VG4 {
     __device__ __forceinline__ void set_x(int s, const float4& xv, const float4& pv) {
         XA[s] = fma2s(alpha, lo2(pv), lo2(xv));
         XB[s] = fma2s(alpha, hi2(pv), hi2(xv));
-        XM[s] = shup(XB[s].y);
-        X4[s] = shdn(XA[s].x);
-        X5[s] = shdn(XB[s].x);
+        float xm1 = shup(XB[s].y), x4 = shdn(XA[s].x), x5 = shdn(XB[s].x);
         if (BORDER) {
-            if (g.strip0 && g.lane == 0) XM[s] = XA[s].x;                 // clamp at column 0
-            if (!g.cv4) { X4[s] = XB[s].y; X5[s] = XB[s].y; }            // clamp at column W-1
+            if (g.strip0 && g.lane == 0) xm1 = XA[s].x;                  // clamp at column 0
+            if (!g.cv4) { x4 = XB[s].y; x5 = XB[s].y; }                  // clamp at column W-1
         }
+        XM1[s] = F2(xm1, XB[s].x);
+        XD[s] = F2(XA[s].y, x4);
+        XE[s] = F2(XB[s].y, x5);
     }
 
     template <int PH>
@@ -111,22 +114,19 @@ struct VG4 {
         // B: w(t+1) = -rho'(z - Y) (as rho'(Y - z)), data value, gathered adjoint into rows t..t+3
         {
             const int tw = t + 1;
-            const float2 M1[4] = {F2(XM[s0], XB[s0].x), F2(XM[s1], XB[s1].x), F2(XM[s2], XB[s2].x), F2(XM[s3], XB[s3].x)};
-            const float2 D[4] = {F2(XA[s0].y, X4[s0]), F2(XA[s1].y, X4[s1]), F2(XA[s2].y, X4[s2]), F2(XA[s3].y, X4[s3])};
-            const float2 E[4] = {F2(XB[s0].y, X5[s0]), F2(XB[s1].y, X5[s1]), F2(XB[s2].y, X5[s2]), F2(XB[s3].y, X5[s3])};
-            const float2 A[4] = {XA[s0], XA[s1], XA[s2], XA[s3]};
-            const float2 B[4] = {XB[s0], XB[s1], XB[s2], XB[s3]};
             float2 zA = F2(0.f, 0.f), zB = zA;
+            const int sl[4] = {s0, s1, s2, s3};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {   // window row j = offset P = j - 1
-                zA = fma2s(TK(cA, j - 1, -1), M1[j], zA);
-                zA = fma2s(TK(cA, j - 1, 0), A[j], zA);
-                zA = fma2s(TK(cA, j - 1, 1), B[j], zA);
-                zA = fma2s(TK(cA, j - 1, 2), D[j], zA);
-                zB = fma2s(TK(cB, j - 1, -1), A[j], zB);
-                zB = fma2s(TK(cB, j - 1, 0), B[j], zB);
-                zB = fma2s(TK(cB, j - 1, 1), D[j], zB);
-                zB = fma2s(TK(cB, j - 1, 2), E[j], zB);
+                const int q = sl[j];
+                zA = fma2s(TK(cA, j - 1, -1), XM1[q], zA);
+                zA = fma2s(TK(cA, j - 1, 0), XA[q], zA);
+                zA = fma2s(TK(cA, j - 1, 1), XB[q], zA);
+                zA = fma2s(TK(cA, j - 1, 2), XD[q], zA);
+                zB = fma2s(TK(cB, j - 1, -1), XA[q], zB);
+                zB = fma2s(TK(cB, j - 1, 0), XB[q], zB);
+                zB = fma2s(TK(cB, j - 1, 1), XD[q], zB);
+                zB = fma2s(TK(cB, j - 1, 2), XE[q], zB);
             }
             const bool orow = tw >= g.r_lo && tw < g.r_hi;
             const float2 eA = sub2(lo2(fy), zA), eB = sub2(hi2(fy), zB);   // Y - z = -e
@@ -158,19 +158,33 @@ struct VG4 {
             // target row t+1+P gets sum_Q kappa_{c(u)}(P,Q) w(u), u = v - (P,Q):
             //   v in A: Q=-1 u=(c1,c3) class B, Q=0 A, Q=1 (c-1,c1) class B, Q=2 (c-2,c0) class A
             //   v in B: Q=-1 u=(c2,c4) class A, Q=0 B, Q=1 A, Q=2 (c-1,c1) class B
-            float2 cAa[4], cBa[4];
+            if (!BORDER) {
+                // interior: straight into the pending rows t..t+3
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float2 a = mul2s(TK(cB, j - 1, -1), wB);
-                a = fma2s(TK(cA, j - 1, 0), wA, a);
-                a = fma2s(TK(cB, j - 1, 1), wM1, a);
-                cAa[j] = fma2s(TK(cA, j - 1, 2), wM2, a);
-                float2 c = mul2s(TK(cA, j - 1, -1), wD);
-                c = fma2s(TK(cB, j - 1, 0), wB, c);
-                c = fma2s(TK(cA, j - 1, 1), wA, c);
-                cBa[j] = fma2s(TK(cB, j - 1, 2), wM1, c);
-            }
-            if (BORDER) {
+                for (int j = 0; j < 4; ++j) {
+                    const int q = sl[j];
+                    GA[q] = fma2s(TK(cB, j - 1, -1), wB, GA[q]);
+                    GA[q] = fma2s(TK(cA, j - 1, 0), wA, GA[q]);
+                    GA[q] = fma2s(TK(cB, j - 1, 1), wM1, GA[q]);
+                    GA[q] = fma2s(TK(cA, j - 1, 2), wM2, GA[q]);
+                    GB[q] = fma2s(TK(cA, j - 1, -1), wD, GB[q]);
+                    GB[q] = fma2s(TK(cB, j - 1, 0), wB, GB[q]);
+                    GB[q] = fma2s(TK(cA, j - 1, 1), wA, GB[q]);
+                    GB[q] = fma2s(TK(cB, j - 1, 2), wM1, GB[q]);
+                }
+            } else {
+                float2 cAa[4], cBa[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float2 a = mul2s(TK(cB, j - 1, -1), wB);
+                    a = fma2s(TK(cA, j - 1, 0), wA, a);
+                    a = fma2s(TK(cB, j - 1, 1), wM1, a);
+                    cAa[j] = fma2s(TK(cA, j - 1, 2), wM2, a);
+                    float2 c = mul2s(TK(cA, j - 1, -1), wD);
+                    c = fma2s(TK(cB, j - 1, 0), wB, c);
+                    c = fma2s(TK(cA, j - 1, 1), wA, c);
+                    cBa[j] = fma2s(TK(cB, j - 1, 2), wM1, c);
+                }
                 // columns: the clamped forward reads fold back onto the edge pixels (adjoint of clamp):
                 // v = 0 also takes u = 0 at Q = -1; v = W-1 (c3 of the last in-image group) takes
                 // u = W-1 at Q = 1, 2 and u = W-2 at Q = 2
@@ -195,11 +209,12 @@ struct VG4 {
                     cAa[2] = add2(cAa[2], cAa[3]); cBa[2] = add2(cBa[2], cBa[3]);
                     cAa[3] = cBa[3] = F2(0.f, 0.f);
                 }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    GA[sl[j]] = add2(GA[sl[j]], cAa[j]);
+                    GB[sl[j]] = add2(GB[sl[j]], cBa[j]);
+                }
             }
-            GA[s0] = add2(GA[s0], cAa[0]); GB[s0] = add2(GB[s0], cBa[0]);
-            GA[s1] = add2(GA[s1], cAa[1]); GB[s1] = add2(GB[s1], cBa[1]);
-            GA[s2] = add2(GA[s2], cAa[2]); GB[s2] = add2(GB[s2], cBa[2]);
-            GA[s3] = add2(GA[s3], cAa[3]); GB[s3] = add2(GB[s3], cBa[3]);
         }
 
         // D: BTV pairs (t, t+d) evaluated once; lambda gamma psi' to both endpoints (Eq. prior,
@@ -215,9 +230,8 @@ struct VG4 {
                     if (dy == 0 && dx == 0) continue;
                     const float lg = sp.lgc[dx + dy - 1];
                     const int cls = dx + dy - 1;
-                    const float2 Dq = F2(XA[sq].y, X4[sq]), Eq = F2(XB[sq].y, X5[sq]);
-                    const float2 pA = dx == 0 ? XA[sq] : (dx == 1 ? XB[sq] : Dq);
-                    const float2 pB = dx == 0 ? XB[sq] : (dx == 1 ? Dq : Eq);
+                    const float2 pA = dx == 0 ? XA[sq] : (dx == 1 ? XB[sq] : XD[sq]);
+                    const float2 pB = dx == 0 ? XB[sq] : (dx == 1 ? XD[sq] : XE[sq]);
                     const float2 dA = sub2(XA[s0], pA), dB = sub2(XB[s0], pB);
                     const float2 qA = fma2(dA, dA, e2), qB = fma2(dB, dB, e2);
                     const float2 rA = rsq2(qA), rB = rsq2(qB);
@@ -553,7 +567,7 @@ __device__ __forceinline__ void uc4_phase(const StencilParams& sp, const Buffers
 
 // ---- per-phase kernels (debug entries and the non-persistent fallback; last-CTA reduction) ----
 template <int BW, int PN>
-__global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg4(const __grid_constant__ StencilParams sp,
+__global__ void __launch_bounds__(PC_WPB * 32, 1) k_vg4(const __grid_constant__ StencilParams sp,
                                                            const __grid_constant__ Buffers b,
                                                            const __grid_constant__ PcTaps T, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -562,7 +576,7 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg4(const __grid_constant_
     const int xcur = __shfl_sync(0xffffffffu, st->xcur, 0);
     const int rcur = __shfl_sync(0xffffffffu, st->rcur, 0);
     const float alpha = phase == PH_ITER ? __shfl_sync(0xffffffffu, st->alpha_f, 0) : 0.0f;
-    const Geo g = geometry<H4>(sp, blockIdx.x);
+    const Geo g = geometry<H4, PC_WPB>(sp, blockIdx.x);
     Ring4 ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT], tot[NSLOT];
@@ -572,7 +586,7 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg4(const __grid_constant_
 }
 
 template <int BW, int PN>
-__global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc4(const __grid_constant__ StencilParams sp,
+__global__ void __launch_bounds__(PC_WPB * 32, 1) k_uc4(const __grid_constant__ StencilParams sp,
                                                            const __grid_constant__ Buffers b,
                                                            const __grid_constant__ PcTaps T, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -588,7 +602,7 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc4(const __grid_constant_
     const int rcur = __shfl_sync(0xffffffffu, st->rcur, 0);
     const float au = phase == PH_DEBUG ? 0.0f : __shfl_sync(0xffffffffu, st->alpha_upd_f, 0);
     const float be = phase == PH_DEBUG ? 0.0f : __shfl_sync(0xffffffffu, st->beta_f, 0);
-    const Geo g = geometry<H4>(sp, blockIdx.x);
+    const Geo g = geometry<H4, PC_WPB>(sp, blockIdx.x);
     Ring4 ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT], tot[NSLOT];
@@ -602,12 +616,12 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc4(const __grid_constant_
 
 // ---- the whole SCG loop as one persistent cooperative kernel (as k_scg_loop, flmisr_stream.cu) ----
 template <int BW, int PN>
-__global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_loop4(const __grid_constant__ StencilParams sp,
+__global__ void __launch_bounds__(PC_WPB * 32, 1) k_scg_loop4(const __grid_constant__ StencilParams sp,
                                                                  const __grid_constant__ Buffers b,
                                                                  const __grid_constant__ PcTaps T) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ ScgState S;
-    const Geo g = geometry<H4>(sp, blockIdx.x);
+    const Geo g = geometry<H4, PC_WPB>(sp, blockIdx.x);
     Ring4 ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     if (threadIdx.x == 0) S = *b.st;
@@ -700,8 +714,8 @@ cudaError_t launch4(K kernel, bool coop, int nw, cudaStream_t s, A... args) {
     cudaError_t e = set_smem(kernel);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((nw + SWPB - 1) / SWPB);
-    cfg.blockDim = dim3(SWPB * 32);
+    cfg.gridDim = dim3((nw + PC_WPB - 1) / PC_WPB);
+    cfg.blockDim = dim3(PC_WPB * 32);
     cfg.dynamicSmemBytes = RING4_SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

@@ -58,11 +58,11 @@ __device__ __forceinline__ float2 hi2(const float4& v) { return F2(v.z, v.w); } 
 constexpr int NARR = 4;           // rows per stage (4 arrays)
 // ring data + mbarriers of NS stages, rounded to 128 B so every warp's ring (bulk-copy destination,
 // 16-byte shared-memory vector reads) stays aligned
-template <int NS>
+template <int NS, int WPB = SWPB>
 struct RingDims {
     static constexpr int FLOATS = NS * NARR * SCOLS;
     static constexpr size_t BYTES_PER_WARP = ((size_t)FLOATS * 4 + NS * 8 + 127) / 128 * 128;
-    static constexpr size_t SMEM = SWPB * BYTES_PER_WARP;
+    static constexpr size_t SMEM = WPB * BYTES_PER_WARP;
 };
 constexpr int NST = 3;            // stages per warp of the common-kappa kernels (== their row-loop unroll)
 constexpr size_t RING_SMEM = RingDims<NST>::SMEM;
@@ -184,7 +184,7 @@ struct Geo {
 // index within its band in the peer loop)
 // HALO: columns of overlap per strip side (the operator's column reach): SHALO = 2 for the common-kappa
 // kernels, 4 for the per-phase 4x4 kernels; strips step by SCOLS - 2 HALO
-template <int HALO = SHALO>
+template <int HALO = SHALO, int WPB = SWPB>
 __device__ __forceinline__ Geo geometry(const StencilParams& sp, int cta) {
     constexpr int STEP = SCOLS - 2 * HALO;
     Geo g;
@@ -193,7 +193,7 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp, int cta) {
     // operands directly instead of a per-copy R2UR waterfall
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     g.lane = threadIdx.x & 31;
-    const int gw = cta * SWPB + warp;
+    const int gw = cta * WPB + warp;
     g.live = gw < sp.nitems;
     // work item -> (strip, rows [r_lo, r_hi)); see StencilParams: border pieces (band edges, edge
     // strips) are seg_b rows, interior pieces seg_rows rows

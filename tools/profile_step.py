@@ -16,11 +16,11 @@ a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 n_iter = a.n_iter if a.n_iter is not None else c["n_iter"]
 lr, mag = c["lr"], c["mag"]
-rng = __import__("numpy").random.default_rng(c["seed"])
+import numpy as np  # noqa: E402
 # cheap synthetic stack (phantom generation is irrelevant for profiling): smooth field + noise
-y = synth.random_fields((mag * mag, lr, lr), c["seed"], 0.2, 0.9)
-sh = synth.shift_pattern(mag)
-pl = flmisr.Plan(k=mag * mag, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, n_iter=n_iter)
+y = synth.random_fields((len(c.get("shifts", ())) or mag * mag, lr, lr), c["seed"], 0.2, 0.9)
+sh = np.asarray(c["shifts"], dtype=np.float64) if "shifts" in c else synth.shift_pattern(mag)
+pl = flmisr.Plan(k=len(sh), lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, n_iter=n_iter)
 yd = torch.from_numpy(y).cuda()
 for _ in range(a.reps):
     hr, rep = pl.reconstruct(yd)
