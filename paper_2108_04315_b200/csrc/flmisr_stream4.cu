@@ -39,6 +39,13 @@ static_assert(SCOLS - 2 * H4 == PC_SSTEP, "per-phase strip step");
 // a constant-bank operand)
 #define TK(cls, P, Q) T.k[(cls)][((P) + 1) * 4 + ((Q) + 1)]
 
+// acc += k (a, b) for a pair whose members live in different registers ((c-1, c1), (c2, c4), (c3, c5)):
+// two scalar FFMAs instead of materialising the pair -- the compiler otherwise re-forms such pairs with
+// MOVs at every use (~17 per pixel measured)
+__device__ __forceinline__ float2 fmam(float k, float a, float b, float2 acc) {
+    return F2(fmaf(k, a, acc.x), fmaf(k, b, acc.y));
+}
+
 // ------------------------------------------------------------------------------------------------
 // value + gradient at x' = x + alpha p, streaming.  Step t (ring stage = x, p(t+3), Y(t+1), r_old(t)):
 // x'(t+3) into the window; w(t+1) = -rho'(z(t+1) - Y(t+1)) from window rows t..t+3, gathered into the
@@ -47,10 +54,11 @@ static_assert(SCOLS - 2 * H4 == PC_SSTEP, "per-phase strip step");
 // ------------------------------------------------------------------------------------------------
 template <int BW, int PN, bool BORDER>
 struct VG4 {
-    // x' pairs of the window rows (slot = (row - t0) & 3), each formed once per row: M1 = (c-1, c1)
-    // (c-1 = the left lane's c3), A = (c0, c2), B = (c1, c3), D = (c2, c4), E = (c3, c5) (c4, c5 = the
-    // right lane's c0, c1): every kappa offset Q in [-1, 2] of both pixel pairs is one register pair
-    float2 XM1[4], XA[4], XB[4], XD[4], XE[4];
+    // x' of the window rows (slot = (row - t0) & 3): the pairs A = (c0, c2), B = (c1, c3) and the
+    // neighbours c-1 (left lane's c3), c4, c5 (right lane's c0, c1); the kappa offsets Q = -1 of A and
+    // Q = 1, 2 of B read the mixed pairs (c-1, c1), (c2, c4), (c3, c5) through fmam
+    float2 XA[4], XB[4];
+    float XM[4], X4[4], X5[4];
     float2 GA[4], GB[4], GD[4], GE[4];   // pending r at (c0,c2), (c1,c3), (c2,c4), (c3,c5)
     float2 accd, vb[4], rr, rro;    // .x: columns c0+c1, .y: columns c2+c3
     const float *ix, *ip, *iy, *ir; // interior warps: next rows to stage (strip start column)
@@ -91,9 +99,9 @@ struct VG4 {
             if (g.strip0 && g.lane == 0) xm1 = XA[s].x;                  // clamp at column 0
             if (!g.cv4) { x4 = XB[s].y; x5 = XB[s].y; }                  // clamp at column W-1
         }
-        XM1[s] = F2(xm1, XB[s].x);
-        XD[s] = F2(XA[s].y, x4);
-        XE[s] = F2(XB[s].y, x5);
+        XM[s] = xm1;
+        X4[s] = x4;
+        X5[s] = x5;
     }
 
     template <int PH>
@@ -119,14 +127,14 @@ struct VG4 {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {   // window row j = offset P = j - 1
                 const int q = sl[j];
-                zA = fma2s(TK(cA, j - 1, -1), XM1[q], zA);
+                zA = fmam(TK(cA, j - 1, -1), XM[q], XB[q].x, zA);
                 zA = fma2s(TK(cA, j - 1, 0), XA[q], zA);
                 zA = fma2s(TK(cA, j - 1, 1), XB[q], zA);
-                zA = fma2s(TK(cA, j - 1, 2), XD[q], zA);
+                zA = fmam(TK(cA, j - 1, 2), XA[q].y, X4[q], zA);
                 zB = fma2s(TK(cB, j - 1, -1), XA[q], zB);
                 zB = fma2s(TK(cB, j - 1, 0), XB[q], zB);
-                zB = fma2s(TK(cB, j - 1, 1), XD[q], zB);
-                zB = fma2s(TK(cB, j - 1, 2), XE[q], zB);
+                zB = fmam(TK(cB, j - 1, 1), XA[q].y, X4[q], zB);
+                zB = fmam(TK(cB, j - 1, 2), XB[q].y, X5[q], zB);
             }
             const bool orow = tw >= g.r_lo && tw < g.r_hi;
             const float2 eA = sub2(lo2(fy), zA), eB = sub2(hi2(fy), zB);   // Y - z = -e
@@ -154,7 +162,7 @@ struct VG4 {
                 if (g.strip0 && g.lane == 0) { wm1 = 0.0f; wm2 = 0.0f; }
                 if (!g.cv4) w4 = 0.0f;
             }
-            const float2 wM1 = F2(wm1, wB.x), wM2 = F2(wm2, wA.x), wD = F2(wA.y, w4);
+            // mixed residual pairs (c-1, c1) = (wm1, wB.x), (c-2, c0) = (wm2, wA.x), (c2, c4) = (wA.y, w4)
             // target row t+1+P gets sum_Q kappa_{c(u)}(P,Q) w(u), u = v - (P,Q):
             //   v in A: Q=-1 u=(c1,c3) class B, Q=0 A, Q=1 (c-1,c1) class B, Q=2 (c-2,c0) class A
             //   v in B: Q=-1 u=(c2,c4) class A, Q=0 B, Q=1 A, Q=2 (c-1,c1) class B
@@ -165,12 +173,12 @@ struct VG4 {
                     const int q = sl[j];
                     GA[q] = fma2s(TK(cB, j - 1, -1), wB, GA[q]);
                     GA[q] = fma2s(TK(cA, j - 1, 0), wA, GA[q]);
-                    GA[q] = fma2s(TK(cB, j - 1, 1), wM1, GA[q]);
-                    GA[q] = fma2s(TK(cA, j - 1, 2), wM2, GA[q]);
-                    GB[q] = fma2s(TK(cA, j - 1, -1), wD, GB[q]);
+                    GA[q] = fmam(TK(cB, j - 1, 1), wm1, wB.x, GA[q]);
+                    GA[q] = fmam(TK(cA, j - 1, 2), wm2, wA.x, GA[q]);
+                    GB[q] = fmam(TK(cA, j - 1, -1), wA.y, w4, GB[q]);
                     GB[q] = fma2s(TK(cB, j - 1, 0), wB, GB[q]);
                     GB[q] = fma2s(TK(cA, j - 1, 1), wA, GB[q]);
-                    GB[q] = fma2s(TK(cB, j - 1, 2), wM1, GB[q]);
+                    GB[q] = fmam(TK(cB, j - 1, 2), wm1, wB.x, GB[q]);
                 }
             } else {
                 float2 cAa[4], cBa[4];
@@ -178,12 +186,12 @@ struct VG4 {
                 for (int j = 0; j < 4; ++j) {
                     float2 a = mul2s(TK(cB, j - 1, -1), wB);
                     a = fma2s(TK(cA, j - 1, 0), wA, a);
-                    a = fma2s(TK(cB, j - 1, 1), wM1, a);
-                    cAa[j] = fma2s(TK(cA, j - 1, 2), wM2, a);
-                    float2 c = mul2s(TK(cA, j - 1, -1), wD);
+                    a = fmam(TK(cB, j - 1, 1), wm1, wB.x, a);
+                    cAa[j] = fmam(TK(cA, j - 1, 2), wm2, wA.x, a);
+                    float2 c = F2(TK(cA, j - 1, -1) * wA.y, TK(cA, j - 1, -1) * w4);
                     c = fma2s(TK(cB, j - 1, 0), wB, c);
                     c = fma2s(TK(cA, j - 1, 1), wA, c);
-                    cBa[j] = fma2s(TK(cB, j - 1, 2), wM1, c);
+                    cBa[j] = fmam(TK(cB, j - 1, 2), wm1, wB.x, c);
                 }
                 // columns: the clamped forward reads fold back onto the edge pixels (adjoint of clamp):
                 // v = 0 also takes u = 0 at Q = -1; v = W-1 (c3 of the last in-image group) takes
@@ -230,9 +238,13 @@ struct VG4 {
                     if (dy == 0 && dx == 0) continue;
                     const float lg = sp.lgc[dx + dy - 1];
                     const int cls = dx + dy - 1;
-                    const float2 pA = dx == 0 ? XA[sq] : (dx == 1 ? XB[sq] : XD[sq]);
-                    const float2 pB = dx == 0 ? XB[sq] : (dx == 1 ? XD[sq] : XE[sq]);
-                    const float2 dA = sub2(XA[s0], pA), dB = sub2(XB[s0], pB);
+                    // partners: dx = 0: A, B; dx = 1: B, (c2, c4); dx = 2: (c2, c4), (c3, c5) of row t + dy
+                    const float2 dA = dx == 0 ? sub2(XA[s0], XA[sq])
+                                    : dx == 1 ? sub2(XA[s0], XB[sq])
+                                              : F2(XA[s0].x - XA[sq].y, XA[s0].y - X4[sq]);
+                    const float2 dB = dx == 0 ? sub2(XB[s0], XB[sq])
+                                    : dx == 1 ? F2(XB[s0].x - XA[sq].y, XB[s0].y - X4[sq])
+                                              : F2(XB[s0].x - XB[sq].y, XB[s0].y - X5[sq]);
                     const float2 qA = fma2(dA, dA, e2), qB = fma2(dB, dB, e2);
                     const float2 rA = rsq2(qA), rB = rsq2(qB);
                     float2 uA = mul2(dA, rA), uB = mul2(dB, rB);
@@ -439,25 +451,23 @@ struct UC4 {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int s = sl[j];
-                    const float2 XM1 = F2(XM[s], XB[s].x), XD = F2(XA[s].y, X4[s]), XE = F2(XB[s].y, X5[s]);
-                    const float2 PM1 = F2(PM[s], PB[s].x), PD = F2(PA[s].y, P4[s]), PE = F2(PB[s].y, P5[s]);
-                    aA = fma2s(TK(cA, j - 1, -1), PM1, aA);
+                    aA = fmam(TK(cA, j - 1, -1), PM[s], PB[s].x, aA);
                     aA = fma2s(TK(cA, j - 1, 0), PA[s], aA);
                     aA = fma2s(TK(cA, j - 1, 1), PB[s], aA);
-                    aA = fma2s(TK(cA, j - 1, 2), PD, aA);
+                    aA = fmam(TK(cA, j - 1, 2), PA[s].y, P4[s], aA);
                     aB = fma2s(TK(cB, j - 1, -1), PA[s], aB);
                     aB = fma2s(TK(cB, j - 1, 0), PB[s], aB);
-                    aB = fma2s(TK(cB, j - 1, 1), PD, aB);
-                    aB = fma2s(TK(cB, j - 1, 2), PE, aB);
+                    aB = fmam(TK(cB, j - 1, 1), PA[s].y, P4[s], aB);
+                    aB = fmam(TK(cB, j - 1, 2), PB[s].y, P5[s], aB);
                     if (PN != 2) {
-                        zA = fma2s(TK(cA, j - 1, -1), XM1, zA);
+                        zA = fmam(TK(cA, j - 1, -1), XM[s], XB[s].x, zA);
                         zA = fma2s(TK(cA, j - 1, 0), XA[s], zA);
                         zA = fma2s(TK(cA, j - 1, 1), XB[s], zA);
-                        zA = fma2s(TK(cA, j - 1, 2), XD, zA);
+                        zA = fmam(TK(cA, j - 1, 2), XA[s].y, X4[s], zA);
                         zB = fma2s(TK(cB, j - 1, -1), XA[s], zB);
                         zB = fma2s(TK(cB, j - 1, 0), XB[s], zB);
-                        zB = fma2s(TK(cB, j - 1, 1), XD, zB);
-                        zB = fma2s(TK(cB, j - 1, 2), XE, zB);
+                        zB = fmam(TK(cB, j - 1, 1), XA[s].y, X4[s], zB);
+                        zB = fmam(TK(cB, j - 1, 2), XB[s].y, X5[s], zB);
                     }
                 }
                 if (PN == 2) {
@@ -484,14 +494,18 @@ struct UC4 {
                 for (int dx = 0; dx < BW; ++dx) {
                     if (dy == 0 && dx == 0) continue;
                     const int cls = dx + dy - 1;
-                    const float2 XD = F2(XA[sq].y, X4[sq]), XE = F2(XB[sq].y, X5[sq]);
-                    const float2 PD = F2(PA[sq].y, P4[sq]), PE = F2(PB[sq].y, P5[sq]);
-                    const float2 xA = dx == 0 ? XA[sq] : (dx == 1 ? XB[sq] : XD);
-                    const float2 xB = dx == 0 ? XB[sq] : (dx == 1 ? XD : XE);
-                    const float2 qpA = dx == 0 ? PA[sq] : (dx == 1 ? PB[sq] : PD);
-                    const float2 qpB = dx == 0 ? PB[sq] : (dx == 1 ? PD : PE);
-                    const float2 dxA = sub2(XA[s0], xA), dxB = sub2(XB[s0], xB);
-                    const float2 dpA = sub2(PA[s0], qpA), dpB = sub2(PB[s0], qpB);
+                    const float2 dxA = dx == 0 ? sub2(XA[s0], XA[sq])
+                                     : dx == 1 ? sub2(XA[s0], XB[sq])
+                                               : F2(XA[s0].x - XA[sq].y, XA[s0].y - X4[sq]);
+                    const float2 dxB = dx == 0 ? sub2(XB[s0], XB[sq])
+                                     : dx == 1 ? F2(XB[s0].x - XA[sq].y, XB[s0].y - X4[sq])
+                                               : F2(XB[s0].x - XB[sq].y, XB[s0].y - X5[sq]);
+                    const float2 dpA = dx == 0 ? sub2(PA[s0], PA[sq])
+                                     : dx == 1 ? sub2(PA[s0], PB[sq])
+                                               : F2(PA[s0].x - PA[sq].y, PA[s0].y - P4[sq]);
+                    const float2 dpB = dx == 0 ? sub2(PB[s0], PB[sq])
+                                     : dx == 1 ? F2(PB[s0].x - PA[sq].y, PB[s0].y - P4[sq])
+                                               : F2(PB[s0].x - PB[sq].y, PB[s0].y - P5[sq]);
                     const float2 rA = rsq2(fma2(dxA, dxA, e2)), rB = rsq2(fma2(dxB, dxB, e2));
                     float2 uA = mul2(rA, dpA), uB = mul2(rB, dpB);
                     if (BORDER) {
