@@ -135,6 +135,8 @@ struct flmisr_plan_s {
     cudaGraphExec_t graph_exec = nullptr;   // the captured SCG loop (world == 1)
     cudaGraphExec_t graph_exec_prof = nullptr;   // the same with per-kernel event records
     int no_graph = 0;                       // FLMISR_NO_GRAPH=1: always launch eagerly
+    cudaGraphExec_t virt_graph = nullptr;   // band 0 of a virtual group: the group's captured loop
+    std::vector<const void*> virt_key;      // ... and the bands (plan, buffers) it was captured for
     int persist = 0;                        // 1: the SCG loop runs as one persistent cooperative kernel
     int prof_mode = 0;                      // layout of the profiling marks of the last call (0 per-kernel, 1 loop)
     flmisr_pipeline_s* pipe = nullptr;      // the pipeline driving this plan, if any
@@ -721,6 +723,7 @@ flmisr_status flmisr_destroy(flmisr_plan_t p) {
     for (auto e : p->prof.ev) cudaEventDestroy(e);
     if (p->done_ev) cudaEventDestroy(p->done_ev);
     if (p->graph_exec) cudaGraphExecDestroy(p->graph_exec);
+    if (p->virt_graph) cudaGraphExecDestroy(p->virt_graph);
     if (p->graph_exec_prof) cudaGraphExecDestroy(p->graph_exec_prof);
     if (p->stream) cudaStreamDestroy(p->stream);
     delete p;
@@ -911,7 +914,12 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
             return fail(FLMISR_ERR_CUDA, std::string("persistent SCG loop launch: ") + cudaGetErrorString(le));
         }
     }
-    const bool use_graph = !looped && p->cfg.world == 1 && !p->no_graph;
+    // world > 1 over NCCL: the per-phase kernels, the halo send/recv, the consensus allgather and the
+    // scalar kernels are captured into the same graph (NCCL operations are graph-capturable; SURVEY
+    // 8(e)); every rank captures the same operation sequence, so graph and eager ranks still match.
+    const bool nccl_graph = p->cfg.world > 1 && !p->virt && std::getenv("FLMISR_NO_NCCL_GRAPH") == nullptr;
+    const bool use_graph = !looped && !p->no_graph && (p->cfg.world == 1 || nccl_graph);
+    bool graphed = false;
     if (looped) {
     } else if (use_graph) {
         cudaGraphExec_t& ge = prof ? p->graph_exec_prof : p->graph_exec;
@@ -921,16 +929,26 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
             st = loop(cs, ev, true);
             cudaGraph_t graph = nullptr;
             cudaError_t ce = cudaStreamEndCapture(cs, &graph);
-            if (st != FLMISR_OK) {
-                if (graph) cudaGraphDestroy(graph);
-                return st;
+            if (st == FLMISR_OK && ce == cudaSuccess) {
+                ce = cudaGraphInstantiate(&ge, graph, 0);
+                if (ce != cudaSuccess) ge = nullptr;
             }
-            if (ce != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-            ce = cudaGraphInstantiate(&ge, graph, 0);
-            cudaGraphDestroy(graph);
-            if (ce != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+            if (graph) cudaGraphDestroy(graph);
+            if (p->cfg.world > 1 && (st != FLMISR_OK || ce != cudaSuccess)) {
+                cudaGetLastError();   // the NCCL path could not be captured here: launch eagerly from now on
+                p->no_graph = 1;
+                st = FLMISR_OK;
+            } else {
+                if (st != FLMISR_OK) return st;
+                if (ce != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+            }
         }
-        CUDA_TRY(cudaGraphLaunch(ge, s));
+        if (ge) {
+            CUDA_TRY(cudaGraphLaunch(ge, s));
+            graphed = true;
+        }
+    }
+    if (looped || graphed) {
     } else {
         st = loop(s, ev, false);
         if (st != FLMISR_OK) return st;
@@ -1094,10 +1112,37 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
         for (int h = 0; h < g; ++h) CUDA_TRY(launch_scalar_after_curv(plans[h]->b, g, s));
         return FLMISR_OK;
     };
-    if ((st = value_grad(PH_INIT)) != FLMISR_OK) return st;
-    for (int it = 0; it < plans[0]->cfg.n_iter; ++it) {
-        if ((st = update_curv()) != FLMISR_OK) return st;
-        if ((st = value_grad(PH_ITER)) != FLMISR_OK) return st;
+    auto body = [&]() -> flmisr_status {
+        flmisr_status r;
+        if ((r = value_grad(PH_INIT)) != FLMISR_OK) return r;
+        for (int it = 0; it < plans[0]->cfg.n_iter; ++it) {
+            if ((r = update_curv()) != FLMISR_OK) return r;
+            if ((r = value_grad(PH_ITER)) != FLMISR_OK) return r;
+        }
+        return FLMISR_OK;
+    };
+    // the loop of all bands (kernels, the copies standing in for the NCCL allgather and halo
+    // send/recv, the scalar kernels) as one CUDA graph, captured once per band set (as on one GPU)
+    flmisr_plan_s* p0 = plans[0];
+    std::vector<const void*> key;
+    for (int h = 0; h < g; ++h) { key.push_back(plans[h]); key.push_back(plans[h]->mem); }
+    if (p0->no_graph) {
+        if ((st = body()) != FLMISR_OK) return st;
+    } else {
+        if (!p0->virt_graph || p0->virt_key != key) {
+            if (p0->virt_graph) cudaGraphExecDestroy(p0->virt_graph);
+            p0->virt_graph = nullptr;
+            CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            st = body();
+            cudaGraph_t graph = nullptr;
+            cudaError_t ce = cudaStreamEndCapture(s, &graph);
+            if (st == FLMISR_OK && ce == cudaSuccess) ce = cudaGraphInstantiate(&p0->virt_graph, graph, 0);
+            if (graph) cudaGraphDestroy(graph);
+            if (st != FLMISR_OK) return st;
+            if (ce != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("virtual group graph: ") + cudaGetErrorString(ce));
+            p0->virt_key = key;
+        }
+        CUDA_TRY(cudaGraphLaunch(p0->virt_graph, s));
     }
     for (int h = 0; h < g; ++h)
         CUDA_TRY(launch_finalize(plans[h]->sp, plans[h]->b, hr_out, plans[h]->W, plans[h]->row_lo, plans[h]->row_hi, s));

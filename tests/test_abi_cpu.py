@@ -57,6 +57,9 @@ def cfg(**kw):
     (dict(curv_mode=1, scg_sigma0=0.0), "scg_sigma0"),
     (dict(curv_mode=1, world=2, rank=0, nccl_id=b"\0" * 128), "world must be 1"),
     (dict(btv_offsets=1, world=2, rank=0, nccl_id=b"\0" * 128), "world must be 1"),
+    (dict(x0_mode=2), "x0_mode"),
+    (dict(x0_mode=1, shifts=synth.shift_pattern(2) + 0.1, world=2, rank=0, nccl_id=b"\0" * 128),
+     "x0_mode = 1 with fractional HR shifts needs world == 1"),
 ])
 def test_config_errors_raised_before_gpu_work(fl, kw, msg):
     c = cfg(**kw)
@@ -86,3 +89,19 @@ def test_peer_entry_points_reject_bad_arguments_without_a_gpu(fl):
     assert "2 <= g <= 8" in fl.last_error()
     arr9 = (C.c_void_p * 9)(*([None] * 9))
     assert fl._lib.flmisr_reconstruct_virtual_peer(arr9, 9, None, None, None, None) == -2
+
+
+def test_interp_fuse_and_binding_checks_without_a_gpu(fl):
+    """flmisr_interp_fuse rejects a NULL plan / NULL buffers before any device work; the binding
+    rejects wrong dtypes, devices and sizes before the C call."""
+    assert fl._lib.flmisr_interp_fuse(None, None, None, None) == -2
+    assert "plan" in fl.last_error()
+    import torch
+    with pytest.raises(ValueError, match="dtype"):
+        fl._ptr(torch.zeros(4, dtype=torch.float64), 4, None, "x")
+    with pytest.raises(ValueError, match="elements"):
+        fl._ptr(np.zeros(3, np.float32), 4, None, "x")
+    with pytest.raises(ValueError, match="expected cuda:0"):
+        fl._ptr(torch.zeros(4), 4, 0, "x")
+    with pytest.raises(ValueError, match="contiguous"):
+        fl._ptr(np.zeros((4, 4), np.float32)[:, ::2], 8, None, "x")
