@@ -534,6 +534,8 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     b.trace = p->dmem + npart + NSLOT;
     p->gathered = p->dmem + npart + NSLOT + ntrace;
     b.gbar = reinterpret_cast<unsigned*>(p->dmem + nd - 1);
+    b.mem_lo = p->mem;
+    b.mem_hi = p->mem + (p->hr_bytes * nhr + pad) / sizeof(float);
     {   // the whole SCG loop as one cooperative kernel (streaming path, one GPU):
         // removes the per-phase kernel boundary and reduction tail.  FLMISR_NO_PERSIST=1 falls back to
         // the per-phase kernels (deferred reduction), which bench.py uses for the per-kernel split.

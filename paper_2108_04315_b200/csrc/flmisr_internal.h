@@ -106,6 +106,8 @@ struct Buffers {
     float* send_bot;
     int eta;                     // halo rows per side
     unsigned* gbar;              // grid-barrier arrival counter of the persistent loop kernel (zeroed per call)
+    const float* mem_lo;         // the plan's HR allocation [mem_lo, mem_hi) (all seven buffers + padding
+    const float* mem_hi;         // rows): bounds of every streaming-kernel access in FLMISR_BOUNDS builds
 };
 
 // Row bands over peer memory (flmisr_stream.cu k_scg_peer_loop*).  Pointers

@@ -83,9 +83,12 @@ struct VG4 {
 
     __device__ __forceinline__ void issue(int s, int tt) {
         if (BORDER) {
-            ring.issue(s, rowp(X0, sp, tt + 3) + g.cbase, rowp(P0, sp, tt + 3) + g.cbase,
-                       rowp(b.Y, sp, tt + 1) + g.cbase, rowp(Rold, sp, tt) + g.cbase);
+            const float *a0 = rowp(X0, sp, tt + 3) + g.cbase, *a1 = rowp(P0, sp, tt + 3) + g.cbase;
+            const float *a2 = rowp(b.Y, sp, tt + 1) + g.cbase, *a3 = rowp(Rold, sp, tt) + g.cbase;
+            FL_BCHK(b, a0, SCOLS); FL_BCHK(b, a1, SCOLS); FL_BCHK(b, a2, SCOLS); FL_BCHK(b, a3, SCOLS);
+            ring.issue(s, a0, a1, a2, a3);
         } else {
+            FL_BCHK(b, ix, SCOLS); FL_BCHK(b, ip, SCOLS); FL_BCHK(b, iy, SCOLS); FL_BCHK(b, ir, SCOLS);
             ring.issue(s, ix, ip, iy, ir);
             ix += sp.pitch; ip += sp.pitch; iy += sp.pitch; ir += sp.pitch;
         }
@@ -295,6 +298,7 @@ struct VG4 {
             float* rp = BORDER ? Rnew + (size_t)(t - sp.store_lo) * sp.pitch + g.col0 : qw;
             if (!BORDER) qw += sp.pitch;
             if (orow) {
+                FL_BCHK(b, rp, 4);
                 stp(rp, GA[s0], GB[s0], g.olo, g.ohi);
                 rr = fma2(GA[s0], GA[s0], rr);
                 rr = fma2(GB[s0], GB[s0], rr);
@@ -396,9 +400,12 @@ struct UC4 {
 
     __device__ __forceinline__ void issue(int s, int tt) {
         if (BORDER) {
-            ring.issue(s, rowp(X0, sp, tt + 3) + g.cbase, rowp(P0, sp, tt + 3) + g.cbase,
-                       rowp(R0, sp, tt + 3) + g.cbase, rowp(b.Y, sp, tt + 1) + g.cbase);
+            const float *a0 = rowp(X0, sp, tt + 3) + g.cbase, *a1 = rowp(P0, sp, tt + 3) + g.cbase;
+            const float *a2 = rowp(R0, sp, tt + 3) + g.cbase, *a3 = rowp(b.Y, sp, tt + 1) + g.cbase;
+            FL_BCHK(b, a0, SCOLS); FL_BCHK(b, a1, SCOLS); FL_BCHK(b, a2, SCOLS); FL_BCHK(b, a3, SCOLS);
+            ring.issue(s, a0, a1, a2, a3);
         } else {
+            FL_BCHK(b, ix, SCOLS); FL_BCHK(b, ip, SCOLS); FL_BCHK(b, ir, SCOLS); FL_BCHK(b, iy, SCOLS);
             ring.issue(s, ix, ip, ir, iy);
             ix += sp.pitch; ip += sp.pitch; ir += sp.pitch; iy += sp.pitch;
         }
@@ -411,6 +418,7 @@ struct UC4 {
         PB[s] = fma2s(be, hi2(pv), hi2(rv));
         if (row >= g.w_lo && row < g.w_hi) {
             const size_t off = (size_t)(row - sp.store_lo) * sp.pitch + g.col0;
+            FL_BCHK(b, Xn + off, 4); FL_BCHK(b, Pn + off, 4);
             stp(Xn + off, XA[s], XB[s], g.olo, g.ohi);
             stp(Pn + off, PA[s], PB[s], g.olo, g.ohi);
             if (row >= g.r_lo && row < g.r_hi) {

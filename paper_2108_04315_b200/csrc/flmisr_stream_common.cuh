@@ -129,6 +129,18 @@ struct RingT {
 };
 using Ring = RingT<NST>;
 
+// FLMISR_BOUNDS builds (memory-safety check without compute-sanitizer): every row the streaming
+// kernels stage or load directly and every row segment they store must lie inside the plan's HR
+// allocation; a violation traps (the kernel fails loudly instead of touching foreign memory)
+#ifdef FLMISR_BOUNDS
+__device__ __forceinline__ void bchk(const Buffers& b, const float* p, int nfloats) {
+    if (p < b.mem_lo || p + nfloats > b.mem_hi) __trap();
+}
+#define FL_BCHK(b, p, n) bchk((b), (p), (n))
+#else
+#define FL_BCHK(b, p, n) ((void)0)
+#endif
+
 __device__ __forceinline__ const float* rowp(const float* base, const StencilParams& sp, int row) {
     int r = min(max(row, sp.store_lo), sp.store_hi - 1);
     return base + (size_t)(r - sp.store_lo) * sp.pitch;
