@@ -103,6 +103,7 @@ struct flmisr_plan_s {
     int stream_path = 0;   // 1: register-streaming kernels (flmisr_stream.cu), 0: tiled kernels
     int pc = 0;            // 1: per-phase streaming kernels (flmisr_stream4.cu): complete phases, kappa per frame
     int all_int = 0;       // 1: every frame's HR shift mag * shift_i is integral
+    int complete = 0;      // 1: every phase class holds a frame (polyphase-complete)
     PcTaps pct{};          // their taps per phase class
     int virt = 0;          // 1: band of an in-process virtual group (flmisr_reconstruct_virtual), no NCCL
     float* halo_mem = nullptr;   // send/recv halo rows (world > 1)
@@ -259,11 +260,12 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         else frame_of_phase[ph] = i;
     }
     if (std::getenv("FLMISR_FORCE_GENERAL") || c.btv_offsets == 1 || c.curv_mode == 1) fast = false;
-    // per-phase path (flmisr_stream4.cu): x2 with K = 4 frames whose integer phases tile [0,2)^2 but whose
+    // per-phase path (flmisr_stream4.cu): x2 with K <= 4 frames at distinct integer phases in [0,2)^2 whose
     // composed kernels differ (sub-pixel remainders per frame), PSF <= 3x3, one GPU: the polyphase Y with a
-    // 4x4 kernel per phase class runs on streaming kernels instead of the general path
+    // 4x4 kernel per phase class runs on streaming kernels instead of the general path.  A phase no frame
+    // covers gets a zero kernel and a zero sample: its residual, penalty, weight and curvature are 0.
     bool pc = false;
-    if (!fast && mag == 2 && K == 4 && std::max(c.psf_h, c.psf_w) <= 3 && c.world == 1 && !virt &&
+    if (!fast && mag == 2 && K >= 1 && K <= 4 && std::max(c.psf_h, c.psf_w) <= 3 && c.world == 1 && !virt &&
         c.btv_offsets == 0 && c.curv_mode == 0 && (c.lr_w % 2) == 0 && c.lr_w >= 4 && c.lr_h >= 4 &&
         !std::getenv("FLMISR_FORCE_GENERAL") && !std::getenv("FLMISR_NO_PC")) {
         int seen[4] = {-1, -1, -1, -1};
@@ -297,6 +299,8 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     p->cfg.nccl_unique_id = nullptr;
     p->fast = fast ? 1 : 0;
     p->pc = pc ? 1 : 0;
+    p->complete = 1;
+    for (int ph = 0; ph < mag * mag; ++ph) if (frame_of_phase[ph] < 0) p->complete = 0;
     p->all_int = 1;
     for (int i = 0; i < 2 * K; ++i)
         if (mag * c.shifts[i] != std::floor(mag * c.shifts[i])) p->all_int = 0;
@@ -306,12 +310,13 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     }
     if (pc) {   // kappa of each phase class, offsets [-R, R+1] placed in the 4x4 window [-1, 2]
         for (int ph = 0; ph < 4; ++ph) {
+            for (int j = 0; j < 16; ++j) p->pct.k[ph][j] = 0.0f;
+            if (frame_of_phase[ph] < 0) continue;   // missing phase: zero kernel
             std::vector<double> kap;
             int syi, sxi;
             double fy, fx;
             composed_taps(c, frame_of_phase[ph], kap, syi, sxi, fy, fx);
             const int KD = 2 * R + 2;
-            for (int j = 0; j < 16; ++j) p->pct.k[ph][j] = 0.0f;
             for (int P = -R; P <= R + 1; ++P)
                 for (int Q = -R; Q <= R + 1; ++Q)
                     p->pct.k[ph][(P + 1) * 4 + (Q + 1)] = (float)kap[(size_t)(P + R) * KD + (Q + R)];
@@ -774,7 +779,7 @@ flmisr_status enqueue_setup(flmisr_plan_s* p, const float* lr_stack, const float
     bool p_zeroed = false;
     if (x0) {
         CUDA_TRY(launch_hr_copy(x0 + (size_t)p->store_lo * p->W, p->W, 0, b.X[0], p->pitch, p->sp.perm, srows, p->W, s));
-    } else if (p->cfg.x0_mode == 1 && p->fast && p->all_int) {
+    } else if (p->cfg.x0_mode == 1 && p->fast && p->all_int && p->complete) {
         // interpolation fusion on a polyphase-complete stack of integer phases is the ingested Y itself
         // (every HR site holds one LR pixel), band + halo rows, in the same buffer layout
         CUDA_TRY(cudaMemcpyAsync(b.X[0], b.Y, p->hr_bytes, cudaMemcpyDeviceToDevice, s));
@@ -1422,7 +1427,7 @@ flmisr_status flmisr_interp_fuse(flmisr_plan_t p, const float* lr, float* out, v
     const Buffers& b = p->b;
     IngestParams ip0 = p->ip;
     ip0.perm = 0;
-    if (p->fast && p->all_int) {   // polyphase-complete, integer phases: every HR site holds one LR pixel
+    if (p->fast && p->all_int && p->complete) {   // polyphase-complete, integer phases: one LR pixel per HR site
         CUDA_TRY(launch_ingest(ip0, lr, b.R[0], s));
         CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, p->H, p->W, s));
         return FLMISR_OK;
@@ -1507,7 +1512,7 @@ flmisr_status flmisr_debug_apply(flmisr_plan_t p, int32_t op, const float* lr, c
             break;
         case FLMISR_OP_INTERP:
             if (!lr || !out) return fail(FLMISR_ERR_SHAPE, "INTERP needs lr and out");
-            if (p->fast && p->all_int) {   // polyphase-complete, integer phases: one LR pixel per HR site
+            if (p->fast && p->all_int && p->complete) {   // polyphase-complete, integer phases
                 CUDA_TRY(launch_ingest(ip0, lr, b.R[0], s));
                 CUDA_TRY(launch_hr_copy(b.R[0], p->pitch, 0, out, p->W, 0, H, p->W, s));
             } else {   // bilinear estimate everywhere, then the integer-phase frames' pixels on their sites

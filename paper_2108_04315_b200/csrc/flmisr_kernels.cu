@@ -343,6 +343,10 @@ __global__ void k_ingest(IngestParams ip, const float* __restrict__ lr, float* _
     if (gx >= ip.W || gy >= ip.store_hi) return;
     int ph = (gy % ip.mag) * ip.mag + (gx % ip.mag);
     int f = ip.frame_of_phase[ph];
+    if (f < 0) {   // missing phase (per-phase path): zero sample under a zero kappa
+        Y[(size_t)(gy - ip.store_lo) * ip.pitch + phys_col(gx, ip.perm)] = 0.0f;
+        return;
+    }
     int a = (gy - ip.sy[f]) / ip.mag, c = (gx - ip.sx[f]) / ip.mag;
     Y[(size_t)(gy - ip.store_lo) * ip.pitch + phys_col(gx, ip.perm)] =
         __ldg(lr + ((size_t)f * ip.lr_h + a) * ip.lr_w + c);
@@ -354,6 +358,7 @@ __global__ void k_egest(IngestParams ip, const float* __restrict__ Yhr, float* _
     if (gx >= ip.W || gy >= ip.store_hi) return;
     int ph = (gy % ip.mag) * ip.mag + (gx % ip.mag);
     int f = ip.frame_of_phase[ph];
+    if (f < 0) return;
     int a = (gy - ip.sy[f]) / ip.mag, c = (gx - ip.sx[f]) / ip.mag;
     lr[((size_t)f * ip.lr_h + a) * ip.lr_w + c] = Yhr[(size_t)(gy - ip.store_lo) * ip.pitch + phys_col(gx, ip.perm)];
 }
@@ -495,10 +500,13 @@ __global__ void k_ingest_m2(IngestParams ip, const float* __restrict__ lr, float
     const int gy = ip.store_lo + blockIdx.y;
     if (4 * q >= ip.W || gy >= ip.store_hi) return;
     const int py = gy & 1;
+    // a phase no frame covers (per-phase path with missing phases: its kappa is zero) holds 0
     const int f0 = ip.frame_of_phase[py * 2], f1 = ip.frame_of_phase[py * 2 + 1];
-    const int a0 = (gy - ip.sy[f0]) >> 1, a1 = (gy - ip.sy[f1]) >> 1;
-    const float2 v0 = __ldg(reinterpret_cast<const float2*>(lr + ((size_t)f0 * ip.lr_h + a0) * ip.lr_w + 2 * q));
-    const float2 v1 = __ldg(reinterpret_cast<const float2*>(lr + ((size_t)f1 * ip.lr_h + a1) * ip.lr_w + 2 * q));
+    const int a0 = (gy - py) >> 1, a1 = (gy - py) >> 1;
+    const float2 v0 = f0 < 0 ? make_float2(0.f, 0.f)
+                             : __ldg(reinterpret_cast<const float2*>(lr + ((size_t)f0 * ip.lr_h + a0) * ip.lr_w + 2 * q));
+    const float2 v1 = f1 < 0 ? make_float2(0.f, 0.f)
+                             : __ldg(reinterpret_cast<const float2*>(lr + ((size_t)f1 * ip.lr_h + a1) * ip.lr_w + 2 * q));
     *reinterpret_cast<float4*>(Y + (size_t)(gy - ip.store_lo) * ip.pitch + 4 * q) = make_float4(v0.x, v0.y, v1.x, v1.y);
 }
 

@@ -63,10 +63,22 @@ def impl(request, monkeypatch):
 
 
 def make(orc, name, n_iter=20, impl=None):
+    """A plan on the general-geometry kernels (FLMISR_NO_PC=1: geometries the per-phase streaming path
+    also covers -- missing phases at x2 -- stay on the kernels this module tests; tests/test_gpu_pc.py
+    runs them on the per-phase path)."""
+    import os
     lr_h, lr_w, mag, psf, sh, pn, lam, w = CASES[name]
     k = len(sh)
-    pl = flmisr.Plan(k=k, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=mag, p_norm=pn, lam=lam,
-                     btv_window=w, n_iter=n_iter)
+    prev = os.environ.get("FLMISR_NO_PC")
+    os.environ["FLMISR_NO_PC"] = "1"
+    try:
+        pl = flmisr.Plan(k=k, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=mag, p_norm=pn, lam=lam,
+                         btv_window=w, n_iter=n_iter)
+    finally:
+        if prev is None:
+            del os.environ["FLMISR_NO_PC"]
+        else:
+            os.environ["FLMISR_NO_PC"] = prev
     if impl is None:
         assert pl.fast_path in (0, 3)
     else:

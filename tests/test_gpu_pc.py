@@ -30,6 +30,9 @@ CASES = {
     "p2_w2": (30, 66, synth.gaussian_psf(0.7), G3SH, 2, 0.2, 2),
     "delta_w1": (24, 36, synth.delta_psf(), G3SH, 1, 0.05, 1),
     "nonsep": (41, 70, NONSEP, G3SH, 1, 0.05, 3),
+    # missing phases: a phase no frame covers gets a zero kernel and a zero sample
+    "missing_one": (29, 36, synth.gaussian_psf(), np.array([[0.0, 0.1], [0.55, 0.5], [0.5, 0.0]]), 1, 0.05, 3),
+    "single_frame": (30, 40, synth.gaussian_psf(), np.array([[0.25, 0.0]]), 1, 0.05, 2),
 }
 
 
@@ -44,10 +47,11 @@ def dev(a):
 
 def make(orc, name, n_iter=20):
     lr_h, lr_w, psf, sh, pn, lam, w = CASES[name]
-    pl = flmisr.Plan(k=4, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=2, p_norm=pn, lam=lam, btv_window=w,
+    k = len(sh)
+    pl = flmisr.Plan(k=k, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=2, p_norm=pn, lam=lam, btv_window=w,
                      n_iter=n_iter)
     assert pl.fast_path == 4, pl.fast_path
-    pb = orc.Problem(k=4, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=2, p_norm=pn, lam=lam, btv_window=w)
+    pb = orc.Problem(k=k, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=psf, mag=2, p_norm=pn, lam=lam, btv_window=w)
     return pl, pb
 
 
@@ -55,11 +59,11 @@ def make(orc, name, n_iter=20):
 def test_forward_adjoint(orc, name):
     pl, pb = make(orc, name)
     x = synth.random_fields((pb.H, pb.W), 1)
-    out = torch.zeros((4, pb.lr_h, pb.lr_w), device="cuda")
+    out = torch.zeros((pb.k, pb.lr_h, pb.lr_w), device="cuda")
     pl.debug(flmisr.OP_FORWARD, in0=dev(x), out=out)
     ref = orc.forward(pb, x.astype(np.float64))
     assert rel(out.cpu().numpy(), ref) <= 1e-5
-    w = synth.random_fields((4, pb.lr_h, pb.lr_w), 2, -1, 1)
+    w = synth.random_fields((pb.k, pb.lr_h, pb.lr_w), 2, -1, 1)
     outa = torch.zeros((pb.H, pb.W), device="cuda")
     pl.debug(flmisr.OP_ADJOINT, in0=dev(w), out=outa)
     assert rel(outa.cpu().numpy(), orc.adjoint(pb, w.astype(np.float64))) <= 1e-5
@@ -70,7 +74,7 @@ def test_gradient_value_curvature_random(orc, name):
     """The hot-loop kernels themselves (k_vg4 / k_uc4) on O(1) random fields."""
     pl, pb = make(orc, name)
     x = synth.random_fields((pb.H, pb.W), 3)
-    y = synth.random_fields((4, pb.lr_h, pb.lr_w), 4)
+    y = synth.random_fields((pb.k, pb.lr_h, pb.lr_w), 4)
     p = synth.random_fields((pb.H, pb.W), 7, -1, 1)
     out = torch.zeros((pb.H, pb.W), device="cuda")
     D, R, rr, _ = pl.debug(flmisr.OP_GRAD, lr=dev(y), in0=dev(x), out=out)
@@ -158,7 +162,7 @@ def test_general_path_agrees(orc, monkeypatch):
 def test_interp_and_x0_mode_fractional(orc):
     """Interpolation fusion with fractional frames inserts only the integer-phase frame (reading 24)."""
     lr_h, lr_w, psf, sh, pn, lam, w = CASES["perm_order"]
-    y = synth.random_fields((4, lr_h, lr_w), 94)
+    y = synth.random_fields((len(sh), lr_h, lr_w), 94)
     pl, pb = make(orc, "perm_order")
     got = pl.interp_fuse(dev(y)).cpu().numpy()
     np.testing.assert_allclose(got, orc.interp_fuse(pb, y.astype(np.float64)), rtol=0, atol=2e-6)
