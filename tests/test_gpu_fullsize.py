@@ -121,3 +121,39 @@ def test_g3_gradient_value_curvature_random_inputs(orc, g3):
     delta, pp, mu, _ = pl.debug(flmisr.OP_CURV, lr=yd, in0=x0, in1=torch.from_numpy(p).cuda())
     dref = orc.curv(pb, x, y.astype(np.float64), p.astype(np.float64))
     assert abs(delta - dref) <= 1e-5 * abs(dref) + curv_rounding_bound(orc, pb, xr, y, p)
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C6"])
+def test_full_size_operators_c4_c6(orc, cfg):
+    """The other BASELINE-size workloads in the configuration bench.py times: C4 (K=9 LR 2048^2 -> x3
+    6144^2, 37.7 MP) and C6 (K=4 LR 4096^2 -> x2 8192^2, 67.1 MP, the paper's largest case): value,
+    gradient and curvature on O(1) random fields against the fp64 oracle over the whole image
+    (relative L2 <= 1e-5, north_star's per-operator bar)."""
+    c = synth.CONFIGS[cfg]
+    mag, lr = c["mag"], c["lr"]
+    k = mag * mag
+    sh = synth.shift_pattern(mag)
+    pl = flmisr.Plan(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag, n_iter=c["n_iter"])
+    pb = orc.Problem(k=k, lr_h=lr, lr_w=lr, shifts=sh, psf=synth.gaussian_psf(), mag=mag)
+    assert pl.fast_path == 2 and pl.loop_kernel
+    y = synth.random_fields((k, lr, lr), 90)
+    yd = torch.from_numpy(y).cuda()
+    xr = synth.random_fields((pl.H, pl.W), 91)
+    x0 = torch.from_numpy(xr).cuda()
+    r = torch.zeros_like(x0)
+    D, R, rr, _ = pl.debug(flmisr.OP_GRAD, lr=yd, in0=x0, out=r)
+    x, y64 = xr.astype(np.float64), y.astype(np.float64)
+    g = orc.grad(pb, x, y64)
+    rn = r.cpu().numpy().astype(np.float64)
+    e_g = np.linalg.norm(rn + g) / np.linalg.norm(g)
+    assert e_g <= 1e-5
+    del rn, r
+    Do, Ro = orc.value(pb, x, y64)
+    assert abs(D - Do) <= 1e-5 * Do and abs(R - Ro) <= 1e-5 * Ro
+    p = synth.random_fields((pl.H, pl.W), 92, -1, 1)
+    delta, pp, mu, _ = pl.debug(flmisr.OP_CURV, lr=yd, in0=x0, in1=torch.from_numpy(p).cuda())
+    dref = orc.curv(pb, x, y64, p.astype(np.float64))
+    print(f"\n{cfg}: gradient rel L2 {e_g:.2e}, value D rel {abs(D - Do) / Do:.2e}, "
+          f"curvature rel {abs(delta - dref) / abs(dref):.2e}")
+    assert abs(delta - dref) <= 1e-5 * abs(dref)
+    pl.destroy()
