@@ -30,6 +30,8 @@ CASES = {
     "p2_w2": (30, 66, synth.gaussian_psf(0.7), G3SH, 2, 0.2, 2),
     "delta_w1": (24, 36, synth.delta_psf(), G3SH, 1, 0.05, 1),
     "nonsep": (41, 70, NONSEP, G3SH, 1, 0.05, 3),
+    # the smallest admissible image (HR 8 x 8: one strip, every warp a border warp)
+    "tiny": (4, 4, synth.gaussian_psf(), G3SH, 1, 0.05, 3),
     # missing phases: a phase no frame covers gets a zero kernel and a zero sample
     "missing_one": (29, 36, synth.gaussian_psf(), np.array([[0.0, 0.1], [0.55, 0.5], [0.5, 0.0]]), 1, 0.05, 3),
     "single_frame": (30, 40, synth.gaussian_psf(), np.array([[0.25, 0.0]]), 1, 0.05, 2),
