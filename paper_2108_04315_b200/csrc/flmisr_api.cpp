@@ -426,7 +426,10 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             // instantiation, ~1.4x slower per row (per-warp timing), so border pieces
             // get seg_b ~ seg_rows / 1.4 rows: interior strips are split seg_b | seg_rows ... | seg_b,
             // the two edge strips (column 0 / W-1) into pieces of seg_b.
-            double ratio = 1.4;
+            // measured border/interior cost ratios (border-piece sweeps, profiles/r02_edge_ratio_sweep.txt):
+            // 1.4 for the common-kappa kernels at x2 (C2, C3), 1.6 at x3 (C4), 1.8 for the per-phase
+            // kernels (G3: 262 vs 242 proj/s at 1.4)
+            double ratio = pc ? 1.8 : (mag == 3 ? 1.6 : 1.4);
             if (const char* ev = std::getenv("FLMISR_EDGE_RATIO")) ratio = std::max(1.0, std::atof(ev));
             sp.ne = sp.nstrips >= 2 ? 2 : 1;
             sp.ni = sp.nstrips - sp.ne;
@@ -448,14 +451,18 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             int S0 = 4;
             if (const char* ev = std::getenv("FLMISR_SEG_MIN")) S0 = std::max(4, std::atoi(ev));
             int S = to1mod3(S0);
-            int Sb = to1mod3((int)(S / ratio));
+            // a piece of S rows streams S + 2 rows (2 warm-up rows); a border piece streams at 1/ratio the
+            // speed, so it gets Sb with Sb + 2 = (S + 2) / ratio (measured: C2 452 -> 498 proj/s over
+            // Sb = S / ratio; C3 unchanged)
+            auto border_rows = [&](int Si) { return to1mod3((int)((Si + 2) / ratio - 2.0)); };
+            int Sb = border_rows(S);
             while (S < rows && items(S, Sb) > cap) {
                 S += pc ? 4 : 3;
-                Sb = to1mod3((int)(S / ratio));
+                Sb = border_rows(S);
             }
             if (const char* ev = std::getenv("FLMISR_SEG_ROWS")) {   // tuning override (S = 1 mod 3), never
                 const int v = std::atoi(ev);                        // below the one-wave minimum
-                if (v >= 4 && to1mod3(v) > S) { S = to1mod3(v); Sb = to1mod3((int)(S / ratio)); }
+                if (v >= 4 && to1mod3(v) > S) { S = to1mod3(v); Sb = border_rows(S); }
             }
             S = std::min(S, pc ? to1mod3(rows) : rows + ((1 - rows % 3) + 3) % 3);   // smallest admissible >= rows
             Sb = std::min(Sb, S);
