@@ -501,6 +501,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     ip.t0y = (float)(mag * c.shifts[0]);
     ip.t0x = (float)(mag * c.shifts[1]);
     ip.perm = sp.perm = p->stream_path;
+    ip.complete = p->complete;
     // streaming kernels on one GPU: per-CTA slots are reduced by every CTA of the next kernel instead of
     // by the last CTA of the producing one (no serial last-CTA tail)
     sp.deferred = p->stream_path && !pc && c.world == 1 && std::getenv("FLMISR_NO_DEFER") == nullptr;

@@ -165,6 +165,7 @@ struct IngestParams {
     int sy[16], sx[16];          // integer phase of frame i
     float t0y, t0x;              // HR shift of frame 0 (bilinear initial estimate)
     int perm;                    // 1: HR buffers use the streaming path's permuted column layout
+    int complete;                // 1: every phase class holds a frame (no missing phase)
 };
 
 // General-geometry path (flmisr_general.cu): per-frame integer phase and composed kernel.

@@ -510,6 +510,113 @@ __global__ void k_ingest_m2(IngestParams ip, const float* __restrict__ lr, float
     *reinterpret_cast<float4*>(Y + (size_t)(gy - ip.store_lo) * ip.pitch + 4 * q) = make_float4(v0.x, v0.y, v1.x, v1.y);
 }
 
+// x3 polyphase ingest (complete phases, lr_w % 4 == 0): a thread turns four LR columns of the three
+// frames of its row phase into twelve HR columns -- three 16-byte loads, three 16-byte stores
+__global__ void k_ingest_m3(IngestParams ip, const float* __restrict__ lr, float* __restrict__ Y) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = ip.store_lo + blockIdx.y;
+    if (12 * k >= ip.W || gy >= ip.store_hi) return;
+    const int py = gy % 3, a = (gy - py) / 3;
+    float4 L[3];
+#pragma unroll
+    for (int px = 0; px < 3; ++px) {
+        const int f = ip.frame_of_phase[py * 3 + px];
+        L[px] = __ldg(reinterpret_cast<const float4*>(lr + ((size_t)f * ip.lr_h + a) * ip.lr_w + 4 * k));
+    }
+    auto at = [&](int c) -> float {   // HR column 12k + c = 3 (4k + c / 3) + c % 3
+        const float4& v = L[c % 3];
+        const int m = c / 3;
+        return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w;
+    };
+    float* row = Y + (size_t)(gy - ip.store_lo) * ip.pitch + 12 * k;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        *reinterpret_cast<float4*>(row + 4 * i) = make_float4(at(4 * i), at(4 * i + 2), at(4 * i + 1), at(4 * i + 3));
+}
+
+// polyphase ingest for any magnification in the permuted layout: one 16-byte store per group of four
+// HR columns, each column's LR sample from its phase's frame (a missing phase holds 0)
+template <int MAG>
+__global__ void k_ingest_v4(IngestParams ip, const float* __restrict__ lr, float* __restrict__ Y) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = ip.store_lo + blockIdx.y;
+    if (4 * q >= ip.W || gy >= ip.store_hi) return;
+    const int py = gy % MAG;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int gx = 4 * q + j, px = gx % MAG;
+        const int f = ip.frame_of_phase[py * MAG + px];
+        v[j] = f < 0 ? 0.0f
+                     : __ldg(lr + ((size_t)f * ip.lr_h + (gy - ip.sy[f]) / MAG) * ip.lr_w + (gx - ip.sx[f]) / MAG);
+    }
+    *reinterpret_cast<float4*>(Y + (size_t)(gy - ip.store_lo) * ip.pitch + 4 * q) = make_float4(v[0], v[2], v[1], v[3]);
+}
+
+// x0 (reading 14) when frame 0's HR shift is integral: integer floor division by the magnification and
+// exact fractions j / MAG (no float division of the coordinates), four columns per thread, permuted
+// layout, p0 = 0 in the same pass
+template <int MAG>
+__global__ void k_init_x0_int(IngestParams ip, int t0y, int t0x, const float* __restrict__ lr, float* __restrict__ X,
+                              float* __restrict__ P0) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = ip.store_lo + blockIdx.y;
+    if (4 * q >= ip.W || gy >= ip.store_hi) return;
+    const int an = gy - t0y;
+    const int a0 = an >= 0 ? an / MAG : -((-an + MAG - 1) / MAG);
+    const float fa = (float)(an - a0 * MAG) * (1.0f / MAG);
+    const float* r0 = lr + (size_t)clampi(a0, 0, ip.lr_h - 1) * ip.lr_w;
+    const float* r1 = lr + (size_t)clampi(a0 + 1, 0, ip.lr_h - 1) * ip.lr_w;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int cn = 4 * q + j - t0x;
+        const int c0 = cn >= 0 ? cn / MAG : -((-cn + MAG - 1) / MAG);
+        const float fc = (float)(cn - c0 * MAG) * (1.0f / MAG);
+        const int ic0 = clampi(c0, 0, ip.lr_w - 1), ic1 = clampi(c0 + 1, 0, ip.lr_w - 1);
+        v[j] = (1.f - fa) * (1.f - fc) * __ldg(r0 + ic0) + (1.f - fa) * fc * __ldg(r0 + ic1) +
+               fa * (1.f - fc) * __ldg(r1 + ic0) + fa * fc * __ldg(r1 + ic1);
+    }
+    const size_t o = (size_t)(gy - ip.store_lo) * ip.pitch + 4 * q;
+    *reinterpret_cast<float4*>(X + o) = make_float4(v[0], v[2], v[1], v[3]);
+    if (P0) *reinterpret_cast<float4*>(P0 + o) = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// x0 at x2 / x3 when frame 0's HR column shift is a multiple of the magnification: a thread's HR columns
+// (4 at x2, 12 at x3) read a fixed window of 3 / 5 consecutive LR columns per LR row, so every tap is a
+// compile-time register (vector loads, no per-column address arithmetic)
+template <int MAG>
+__global__ void k_init_x0_vec(IngestParams ip, int t0y, int t0x, const float* __restrict__ lr, float* __restrict__ X) {
+    constexpr int NC = MAG == 2 ? 4 : 12;          // HR columns per thread
+    constexpr int NL = NC / MAG + 1;               // LR columns read per row
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gy = ip.store_lo + blockIdx.y;
+    if (NC * k >= ip.W || gy >= ip.store_hi) return;
+    const int an = gy - t0y;
+    const int a0 = an >= 0 ? an / MAG : -((-an + MAG - 1) / MAG);
+    const float fa = (float)(an - a0 * MAG) * (1.0f / MAG);
+    const float* r0 = lr + (size_t)clampi(a0, 0, ip.lr_h - 1) * ip.lr_w;
+    const float* r1 = lr + (size_t)clampi(a0 + 1, 0, ip.lr_h - 1) * ip.lr_w;
+    const int b0 = (NC * k - t0x) / MAG;           // exact: t0x % MAG == 0
+    float c[NL];
+#pragma unroll
+    for (int m = 0; m < NL; ++m) {
+        const int ic = clampi(b0 + m, 0, ip.lr_w - 1);
+        c[m] = (1.f - fa) * __ldg(r0 + ic) + fa * __ldg(r1 + ic);   // the row interpolation at LR column b0 + m
+    }
+    float v[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        const int m = j / MAG;
+        const float fc = (float)(j % MAG) * (1.0f / MAG);
+        v[j] = (1.f - fc) * c[m] + fc * c[m + 1];
+    }
+    float* row = X + (size_t)(gy - ip.store_lo) * ip.pitch + NC * k;
+#pragma unroll
+    for (int i = 0; i < NC / 4; ++i)
+        *reinterpret_cast<float4*>(row + 4 * i) = make_float4(v[4 * i], v[4 * i + 2], v[4 * i + 1], v[4 * i + 3]);
+}
+
 __device__ __forceinline__ float bilerp_x0(const IngestParams& ip, const float* __restrict__ y, int gy, int gx) {
     float a = ((float)gy - ip.t0y) / (float)ip.mag, c = ((float)gx - ip.t0x) / (float)ip.mag;
     float a0 = floorf(a), c0 = floorf(c);
@@ -564,8 +671,15 @@ __global__ void k_finalize_perm(StencilParams sp, Buffers b, float* __restrict__
 static bool vec4_ok(int perm, int W, int pitch) { return perm && W % 4 == 0 && pitch % 4 == 0; }
 
 cudaError_t launch_ingest(const IngestParams& ip, const float* lr, float* Y, cudaStream_t s) {
+    const dim3 g4 = rowgrid(ip.W / 4, ip.store_hi - ip.store_lo);
     if (vec4_ok(ip.perm, ip.W, ip.pitch) && ip.mag == 2 && ip.lr_w % 2 == 0)
-        k_ingest_m2<<<rowgrid(ip.W / 4, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, Y);
+        k_ingest_m2<<<g4, 256, 0, s>>>(ip, lr, Y);
+    else if (vec4_ok(ip.perm, ip.W, ip.pitch) && ip.mag == 3 && ip.lr_w % 4 == 0 && ip.complete)
+        k_ingest_m3<<<rowgrid(ip.W / 12, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, Y);
+    else if (vec4_ok(ip.perm, ip.W, ip.pitch) && ip.mag == 3)
+        k_ingest_v4<3><<<g4, 256, 0, s>>>(ip, lr, Y);
+    else if (vec4_ok(ip.perm, ip.W, ip.pitch) && ip.mag == 4)
+        k_ingest_v4<4><<<g4, 256, 0, s>>>(ip, lr, Y);
     else
         k_ingest<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, Y);
     return cudaGetLastError();
@@ -580,9 +694,32 @@ cudaError_t launch_hr_copy(const float* src, int src_pitch, int src_perm, float*
     k_hr_copy<<<rowgrid(W, rows), 256, 0, s>>>(src, src_pitch, src_perm, dst, dst_pitch, dst_perm, W);
     return cudaGetLastError();
 }
-bool init_x0_zeroes_p(const IngestParams& ip) { return vec4_ok(ip.perm, ip.W, ip.pitch); }
+static bool x0_int_path(const IngestParams& ip) {
+    return vec4_ok(ip.perm, ip.W, ip.pitch) && ip.t0y == floorf(ip.t0y) && ip.t0x == floorf(ip.t0x) && ip.mag >= 1 &&
+           ip.mag <= 4;
+}
+// the integer-phase x0 kernel writes X only (p0 = 0 by a memset: measured faster than a second
+// 16-byte store stream from the same kernel, 41 -> ~25 us at C3)
+bool init_x0_zeroes_p(const IngestParams& ip) { return vec4_ok(ip.perm, ip.W, ip.pitch) && !x0_int_path(ip); }
 cudaError_t launch_init_x0(const IngestParams& ip, const float* lr, float* X, cudaStream_t s, float* P0) {
-    if (vec4_ok(ip.perm, ip.W, ip.pitch))
+    const dim3 g4 = rowgrid(ip.W / 4, ip.store_hi - ip.store_lo);
+    if (x0_int_path(ip)) {
+        const int ty = (int)ip.t0y, tx = (int)ip.t0x;
+        if (ip.mag == 2 && tx % 2 == 0) {
+            k_init_x0_vec<2><<<g4, 256, 0, s>>>(ip, ty, tx, lr, X);
+            return cudaGetLastError();
+        }
+        if (ip.mag == 3 && tx % 3 == 0 && ip.W % 12 == 0) {
+            k_init_x0_vec<3><<<rowgrid(ip.W / 12, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, ty, tx, lr, X);
+            return cudaGetLastError();
+        }
+        switch (ip.mag) {
+            case 1: k_init_x0_int<1><<<g4, 256, 0, s>>>(ip, ty, tx, lr, X, nullptr); break;
+            case 2: k_init_x0_int<2><<<g4, 256, 0, s>>>(ip, ty, tx, lr, X, nullptr); break;
+            case 3: k_init_x0_int<3><<<g4, 256, 0, s>>>(ip, ty, tx, lr, X, nullptr); break;
+            default: k_init_x0_int<4><<<g4, 256, 0, s>>>(ip, ty, tx, lr, X, nullptr); break;
+        }
+    } else if (vec4_ok(ip.perm, ip.W, ip.pitch))
         k_init_x0_perm<<<rowgrid(ip.W / 4, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X, P0);
     else
         k_init_x0<<<rowgrid(ip.W, ip.store_hi - ip.store_lo), 256, 0, s>>>(ip, lr, X);
