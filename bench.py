@@ -462,6 +462,25 @@ def run_flmisr(args):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     s = torch.cuda.current_stream(dev)
 
+    if partitioned and transport == "peer":
+        # the first peer-loop call is the handshake: a rank whose peer memory does not work makes every
+        # band abandon the loop after the barrier timeout (an error, not a hang); then all ranks move
+        # to the NCCL transport together (auto) or fail loudly (--transport peer)
+        err = None
+        try:
+            pl.reconstruct(y_d, out=out_d)
+            torch.cuda.synchronize()
+        except Exception as e:   # noqa: BLE001 -- any failure means: not this transport
+            err = f"rank {rank}: {e}"
+        if not collective_all(dist, err is None, dev):
+            errs = [None] * world
+            dist.all_gather_object(errs, err)
+            why = next((e for e in errs if e), "a peer rank failed")
+            if args.transport == "peer":
+                raise RuntimeError(f"peer band loop failed: {why}")
+            pl.destroy()
+            pl, transport, _ = make_band_plan(flmisr, dist, kw, rank, world, "nccl", dev)
+            fallback = f"peer band loop failed on its first call ({why}); NCCL used"
     for _ in range(args.warmup):
         pl.reconstruct(y_d, out=out_d)
     torch.cuda.synchronize()

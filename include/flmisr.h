@@ -209,7 +209,10 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
  *   n_iter.  Errors: FLMISR_ERR_CONFIG (not a streaming band plan, bad blobs, already connected, a
  *   peer that planned a different problem, a peer device without peer access or native peer
  *   atomics), FLMISR_ERR_CUDA (IPC mapping failed).  On any error the plan stays on the NCCL
- *   transport and remains usable.  Status: EXPERIMENTAL on real multi-GPU nodes -- the kernel code
+ *   transport and remains usable.  A peer-loop reconstruction whose band barrier does not complete
+ *   within 20 s (a lost rank, peer memory without working system-scope atomics) abandons the loop on
+ *   every band and returns FLMISR_ERR_CUDA naming the timeout (failed_stage 3) instead of hanging;
+ *   the device stays usable.  Status: EXPERIMENTAL on real multi-GPU nodes -- the kernel code
  *   is parity-tested in the single-device emulation (flmisr_reconstruct_virtual_peer); the IPC /
  *   system-scope path has not run on more than one GPU in this repository's test environment.
  */

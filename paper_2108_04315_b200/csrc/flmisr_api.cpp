@@ -155,6 +155,13 @@ size_t peer_mem_bytes(int world) { return 64 + (size_t)2 * world * PEER_MAXCTAS 
 unsigned long long* peer_cnt(unsigned char* m) { return reinterpret_cast<unsigned long long*>(m); }
 unsigned* peer_epoch(unsigned char* m) { return reinterpret_cast<unsigned*>(m + 8); }
 double* peer_mbox(unsigned char* m) { return reinterpret_cast<double*>(m + 64); }
+static flmisr_status failed_status(const ScgState& hs, const char* what) {
+    if (hs.failed_stage == FAIL_PEER_TIMEOUT)
+        return fail(FLMISR_ERR_CUDA, std::string(what) + ": the peer band barrier timed out at SCG pass " +
+                                         std::to_string(hs.failed_iter) + " (a rank or its peer memory is unreachable)");
+    return fail(FLMISR_ERR_NUMERIC, std::string(what) + ": non-finite consensus scalar at SCG pass " +
+                                        std::to_string(hs.failed_iter) + " (stage " + std::to_string(hs.failed_stage) + ")");
+}
 
 namespace {
 
@@ -1045,9 +1052,7 @@ flmisr_status flmisr_finish(flmisr_plan_t p, flmisr_report* rep) {
         cudaError_t pe = cudaGetLastError();   // do not leave a timing error sticky for the next launch
         if (pe != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("profiling events: ") + cudaGetErrorString(pe));
     }
-    if (h.failed_stage)
-        return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar at SCG pass " + std::to_string(h.failed_iter) +
-                                            " (stage " + std::to_string(h.failed_stage) + ")");
+    if (h.failed_stage) return failed_status(h, "reconstruct");
     return FLMISR_OK;
 }
 
@@ -1182,7 +1187,7 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
         report->failed_iter = hs.failed_iter;
         if (report->f_trace) std::memcpy(report->f_trace, plans[0]->trace_host, ntrace * sizeof(double));
     }
-    if (hs.failed_stage) return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar");
+    if (hs.failed_stage) return failed_status(hs, "virtual group");
     return FLMISR_OK;
 }
 
@@ -1193,6 +1198,12 @@ static void peer_fill(PeerLoop& pl, int world, unsigned char* const* mem_of_rank
         pl.mbox[q] = peer_mbox(mem_of_rank[q]);
         pl.cnt[q] = peer_cnt(mem_of_rank[q]);
     }
+    // a phase takes well under a millisecond: 20 s without every arrival means a lost rank or CTA
+    // (FLMISR_PEER_TIMEOUT_MS overrides; tests use a short one)
+    pl.timeout_ns = 20000000000ull;
+    if (const char* ev = std::getenv("FLMISR_PEER_TIMEOUT_MS")) pl.timeout_ns = (unsigned long long)std::atoll(ev) * 1000000ull;
+    pl.drop_band = -1;
+    if (const char* ev = std::getenv("FLMISR_PEER_TEST_DROP")) pl.drop_band = std::atoi(ev);
 }
 static int peer_ctas(const flmisr_plan_s* p) { return (p->sp.nitems + SWPB - 1) / SWPB; }
 
@@ -1247,6 +1258,8 @@ flmisr_status flmisr_reconstruct_virtual_peer(flmisr_plan_t* plans, int32_t g, c
     }
     cudaError_t se = cudaStreamSynchronize(s);
     if (se != cudaSuccess) return fail(FLMISR_ERR_CUDA, std::string("virtual peer group: ") + cudaGetErrorString(se));
+    for (int h = 0; h < g; ++h)   // a band that abandoned the loop (barrier timeout) reports first
+        if (plans[h]->st_host->failed_stage == FAIL_PEER_TIMEOUT) return failed_status(*plans[h]->st_host, "virtual peer group");
     for (int h = 1; h < g; ++h)
         if (std::memcmp(plans[h]->trace_host, plans[0]->trace_host, ntrace * sizeof(double)) != 0 ||
             plans[h]->st_host->k != plans[0]->st_host->k)
@@ -1260,7 +1273,7 @@ flmisr_status flmisr_reconstruct_virtual_peer(flmisr_plan_t* plans, int32_t g, c
         report->failed_iter = hs.failed_iter;
         if (report->f_trace) std::memcpy(report->f_trace, plans[0]->trace_host, ntrace * sizeof(double));
     }
-    if (hs.failed_stage) return fail(FLMISR_ERR_NUMERIC, "non-finite consensus scalar");
+    if (hs.failed_stage) return failed_status(hs, "virtual group");
     return FLMISR_OK;
 }
 

@@ -123,7 +123,10 @@ struct PeerLoop {
     double* mbox[PMAX];          // rank q's mailbox [2][world][ctas][NSLOT]: every CTA's partial sums
     unsigned long long* cnt[PMAX];   // rank q's arrival counter (monotonic across calls)
     unsigned* epoch_word[PMAX];  // band l: phases completed over all calls
+    unsigned long long timeout_ns;   // a barrier wait longer than this abandons the loop (failed_stage 3)
+    int drop_band;               // test hook (FLMISR_PEER_TEST_DROP, emulation): this band never arrives; -1 none
 };
+enum FailStage : int { FAIL_NONE = 0, FAIL_CURV = 1, FAIL_VALUE = 2, FAIL_PEER_TIMEOUT = 3 };
 struct PeerBands {               // g > 1 (one device): every band's parameters, kernel-parameter space
     StencilParams sp[PMAX];
     Buffers b[PMAX];

@@ -792,9 +792,13 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     return v;
 }
 
-// all threads of every CTA: consensus sums of this phase into tot
-__device__ void peer_sum(const StencilParams& sp, const PeerLoop& pl, int l, int j, int which,
+// all threads of every CTA: consensus sums of this phase into tot.  Returns false (every thread of the
+// CTA) when the arrivals did not complete within pl.timeout_ns: a rank or CTA is lost (e.g. peer memory
+// without working system-scope atomics); the caller abandons the loop instead of trapping, so the
+// context survives and the host can fall back to the NCCL transport.
+__device__ bool peer_sum(const StencilParams& sp, const PeerLoop& pl, int l, int j, int which,
                          const double (&acc)[NSLOT], unsigned epoch, double (&tot)[NSLOT]) {
+    __shared__ int s_timeout;
     __shared__ double sred[32][NSLOT];
     __shared__ double stot[NSLOT];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -825,18 +829,23 @@ __device__ void peer_sum(const StencilParams& sp, const PeerLoop& pl, int l, int
         }
         if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
         else asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        for (int q = 0; q < world; ++q) {
-            if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(pl.cnt[q]) : "memory");
-            else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pl.cnt[q]) : "memory");
+        if (h != pl.drop_band) {
+            for (int q = 0; q < world; ++q) {
+                if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(pl.cnt[q]) : "memory");
+                else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pl.cnt[q]) : "memory");
+            }
         }
         FL_TMARK(epoch, 1)
         const unsigned long long target = (unsigned long long)(epoch + 1) * (unsigned long long)(world * C);
         unsigned spins = 0;
         const unsigned long long tstart = now_ns();
-        while (ld_acquire_u64(pl.cnt[h], sys) < target)   // a lost rank or CTA: fail loudly after 60 s
-            if ((++spins & 1023u) == 0 && now_ns() - tstart > 60000000000ull) __trap();
+        int to = 0;
+        while (ld_acquire_u64(pl.cnt[h], sys) < target)   // a lost rank or CTA: give up after timeout_ns
+            if ((++spins & 1023u) == 0 && now_ns() - tstart > pl.timeout_ns) { to = 1; break; }
+        s_timeout = to;
     }
     __syncthreads();
+    if (s_timeout) return false;
     FL_TMARK(epoch, 2)
     // fixed-order sum of the world x C slots: slot i = (rank, cta) by thread i % blockDim, then a fixed
     // shuffle tree and cross-warp order
@@ -866,6 +875,7 @@ __device__ void peer_sum(const StencilParams& sp, const PeerLoop& pl, int l, int
     FL_TMARK(epoch, 3)
     // the next phase reads peer-written halo rows through the bulk-copy (async) proxy
     asm volatile("fence.proxy.async.global;" ::: "memory");
+    return true;
 }
 
 template <int BW, int PN>
@@ -890,7 +900,11 @@ __device__ __forceinline__ void peer_loop_body(const StencilParams& sp, const Bu
         if (pass > 0) {
             if (ui(S.success)) {
                 uc_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f), par, acc);
-                peer_sum(sp, pl, l, j, 1, acc, epoch++, tot);
+                if (!peer_sum(sp, pl, l, j, 1, acc, epoch++, tot)) {
+                    if (threadIdx.x == 0) { S.done = 1; S.failed_stage = FAIL_PEER_TIMEOUT; S.failed_iter = S.k; }
+                    __syncthreads();
+                    break;
+                }
                 if (threadIdx.x == 0) {
                     S.xcur ^= 1;
                     scg_after_curv(&S, tot);
@@ -902,7 +916,11 @@ __device__ __forceinline__ void peer_loop_body(const StencilParams& sp, const Bu
             if (ui(S.done)) break;
         }
         vg_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par, acc);
-        peer_sum(sp, pl, l, j, 0, acc, epoch++, tot);
+        if (!peer_sum(sp, pl, l, j, 0, acc, epoch++, tot)) {
+            if (threadIdx.x == 0) { S.done = 1; S.failed_stage = FAIL_PEER_TIMEOUT; S.failed_iter = S.k; }
+            __syncthreads();
+            break;
+        }
         if (threadIdx.x == 0) scg_after_value(&S, tot, trace, pass > 0 ? PH_ITER : PH_INIT);
         __syncthreads();
     }

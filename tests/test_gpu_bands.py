@@ -91,6 +91,31 @@ def test_virtual_copies_graph_replay_is_deterministic():
         p.destroy()
 
 
+def test_peer_barrier_timeout_is_an_error_not_a_hang(monkeypatch):
+    """A band that never arrives (test hook FLMISR_PEER_TEST_DROP) makes every band abandon the loop
+    after FLMISR_PEER_TIMEOUT_MS instead of trapping: the call returns FLMISR_ERR_CUDA naming the
+    barrier timeout, and the device stays usable (fresh plans reconstruct normally afterwards)."""
+    lr_h, lr_w, mag, n_iter, g = 32, 64, 2, 6, 2
+    sh = synth.shift_pattern(mag)
+    y = synth.detector_stack(synth.phantom(mag * lr_h, mag * lr_w, seed=67), mag, sh, 1 / 255, seed=67)
+    yd = torch.from_numpy(y.astype(np.float32)).cuda()
+    pls = bands(lr_h, lr_w, mag, g, n_iter)
+    monkeypatch.setenv("FLMISR_PEER_TEST_DROP", "1")
+    monkeypatch.setenv("FLMISR_PEER_TIMEOUT_MS", "200")
+    with pytest.raises(flmisr.FlmisrError) as ei:
+        flmisr.reconstruct_virtual_peer(pls, yd)
+    assert ei.value.status == flmisr.ERR_CUDA and "timed out" in str(ei.value)
+    monkeypatch.delenv("FLMISR_PEER_TEST_DROP")
+    monkeypatch.delenv("FLMISR_PEER_TIMEOUT_MS")
+    for p in pls:
+        p.destroy()
+    fresh = bands(lr_h, lr_w, mag, g, n_iter)
+    h, r = flmisr.reconstruct_virtual_peer(fresh, yd)
+    assert torch.isfinite(h).all() and r["iters_run"] == n_iter
+    for p in fresh:
+        p.destroy()
+
+
 def test_band_gradient_equals_full_gradient(orc):
     """One value+gradient pass at x0 in band mode (n_iter = 0 returns x0, the trace row 0 holds
     f0 = J(x0) and <r0, r0>): identical consensus scalars to the single-band plan."""
