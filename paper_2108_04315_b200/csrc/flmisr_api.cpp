@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -150,8 +151,9 @@ struct flmisr_plan_s {
 };
 
 // peer_mem layout: arrival counter (u64), epoch word (u32), mailbox [2][world][PEER_MAXCTAS][NSLOT] fp64
+// (det mode: [2][world][PEER_MAXCTAS][FXW] 128-bit words)
 constexpr int PEER_MAXCTAS = 256;
-size_t peer_mem_bytes(int world) { return 64 + (size_t)2 * world * PEER_MAXCTAS * NSLOT * sizeof(double); }
+size_t peer_mem_bytes(int world) { return 64 + (size_t)2 * world * PEER_MAXCTAS * FXW * 16; }
 unsigned long long* peer_cnt(unsigned char* m) { return reinterpret_cast<unsigned long long*>(m); }
 unsigned* peer_epoch(unsigned char* m) { return reinterpret_cast<unsigned*>(m + 8); }
 double* peer_mbox(unsigned char* m) { return reinterpret_cast<double*>(m + 64); }
@@ -212,6 +214,8 @@ flmisr_status validate(const flmisr_config* c, bool virt) {
     if (c->n_iter < 0) return fail(FLMISR_ERR_CONFIG, "n_iter must be >= 0");
     if (c->x0_mode != 0 && c->x0_mode != 1)
         return fail(FLMISR_ERR_CONFIG, "x0_mode must be 0 (bilinear frame 0) or 1 (interpolation fusion)");
+    if (c->det_rows != 0 && (c->det_rows < 4 || c->det_rows > 4096))
+        return fail(FLMISR_ERR_CONFIG, "det_rows must be 0 (off) or in [4, 4096] HR rows");
     if (!(c->scg_lambda0 > 0.0) || !std::isfinite(c->scg_lambda0))
         return fail(FLMISR_ERR_CONFIG, "scg_lambda0 must be > 0 (S:362)");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(FLMISR_ERR_CONFIG, "need 0 <= rank < world");
@@ -273,6 +277,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     // covers gets a zero kernel and a zero sample: its residual, penalty, weight and curvature are 0.
     bool pc = false;
     if (!fast && mag == 2 && K >= 1 && K <= 4 && std::max(c.psf_h, c.psf_w) <= 3 && c.world == 1 && !virt &&
+        c.det_rows == 0 &&
         c.btv_offsets == 0 && c.curv_mode == 0 && (c.lr_w % 2) == 0 && c.lr_w >= 4 && c.lr_h >= 4 &&
         !std::getenv("FLMISR_FORCE_GENERAL") && !std::getenv("FLMISR_NO_PC")) {
         int seen[4] = {-1, -1, -1, -1};
@@ -339,18 +344,20 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     p->pn = c.p_norm;
     p->eta = std::max(2 * kr, c.btv_window - 1);
 
-    // ---- row band (Eq. subfunction): multiples of mag, remainder to the last band ----
+    // ---- row band (Eq. subfunction): multiples of mag (det mode: of lcm(det_rows, mag), so every
+    // band is a union of the fixed global tiles), remainder to the last band ----
     const int world = c.world, rank = c.rank;
+    const int bunit = c.det_rows ? c.det_rows / std::gcd(c.det_rows, mag) * mag : mag;
     auto band = [&](int h, int& lo, int& hi) {
-        lo = (int)(((long long)h * p->H / world) / mag * mag);
-        hi = (h == world - 1) ? p->H : (int)(((long long)(h + 1) * p->H / world) / mag * mag);
+        lo = (int)(((long long)h * p->H / world) / bunit * bunit);
+        hi = (h == world - 1) ? p->H : (int)(((long long)(h + 1) * p->H / world) / bunit * bunit);
     };
     for (int h = 0; h < world && world > 1; ++h) {
         int lo, hi;
         band(h, lo, hi);
-        if (hi - lo < std::max(p->eta, 1)) {
-            const int need = std::max(p->eta, 1);
-            const int minH = world * need * mag;
+        if (hi - lo < std::max(p->eta, 1) || (c.det_rows && hi - lo < bunit)) {
+            const int need = std::max(std::max(p->eta, 1), c.det_rows ? bunit : 1);
+            const int minH = world * (c.det_rows ? bunit : need * mag);
             delete p;
             return fail(FLMISR_ERR_CONFIG, "image too small for " + std::to_string(world) +
                                                " partitions: every band needs >= eta = " + std::to_string(need) +
@@ -416,6 +423,11 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         const bool separable = kr <= 1 && err <= 1e-12 * std::fabs(K3[pm]);
         p->stream_path = (fast && separable && (p->W % 4 == 0) && p->W >= 8 && p->H >= 4 &&
                           std::getenv("FLMISR_FORCE_TILED") == nullptr) || pc;
+        if (c.det_rows && !p->stream_path) {
+            delete p;
+            return fail(FLMISR_ERR_CONFIG, "det_rows needs the streaming path (fast_path 2: polyphase-complete stack, "
+                                           "separable composed kernel of radius <= 1, HR width % 4 == 0)");
+        }
         if (p->stream_path) {
             for (int i = 0; i < 3; ++i) { sp.ka[i] = (float)a3[i]; sp.kb[i] = (float)b3[i]; }
             sp.wpb = pc ? PC_WPB : SWPB;
@@ -473,14 +485,20 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             }
             S = std::min(S, pc ? to1mod3(rows) : rows + ((1 - rows % 3) + 3) % 3);   // smallest admissible >= rows
             Sb = std::min(Sb, S);
+            if (c.det_rows) S = Sb = c.det_rows;   // det mode: the fixed global tiles (bands are unions of them)
             sp.seg_rows = S;
             sp.seg_b = Sb;
             sp.nseg_i = nseg_int(S, Sb);
             if (rows <= 2 * Sb) sp.seg_rows = Sb;   // short bands: interior strips in seg_b pieces too
+            if (c.det_rows) sp.nseg_i = (rows + Sb - 1) / Sb;
             sp.nseg_b = (rows + Sb - 1) / Sb;
             sp.n_int = sp.ni * sp.nseg_i;
             sp.nitems = sp.n_int + sp.ne * sp.nseg_b;
             sp.nsegs = sp.nseg_i;
+            // persistent loop kernels: one warp per item (one wave by construction), or in det mode at most
+            // one wave of warps taking the fixed tiles in a grid-stride loop
+            sp.loop_warps = c.det_rows ? (int)std::min<long long>(sp.nitems, cap) : sp.nitems;
+            sp.det = c.det_rows ? 1 : 0;
             // hoisted constants: D = sum q rs - eps N, R = sum gamma q rs - eps sum_d gamma_d n_d,
             // curvature sums carry eps^2 (p = 1) or 2 (p = 2)
             const double eps = c.l1_eps;
@@ -495,6 +513,16 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             sp.aff_vg[NSLOT + 1] = -eps * npairs_g;
             sp.aff_uc[0] = c.p_norm == 1 ? eps * eps : 2.0;
             sp.aff_uc[1] = eps * eps;
+            // det mode: the offsets of the whole image, applied once to the exact all-band total
+            double npairs_all = 0.0;
+            for (int dy = 0; dy < c.btv_window; ++dy)
+                for (int dx = 0; dx < c.btv_window; ++dx) {
+                    if (!dy && !dx) continue;
+                    npairs_all += std::pow(c.btv_alpha, dx + dy) * (double)(p->H - dy) * (double)(p->W - dx);
+                }
+            for (int k = 0; k < NSLOT; ++k) { sp.det_off_vg[k] = 0.0; sp.det_off_uc[k] = sp.aff_uc[NSLOT + k]; }
+            sp.det_off_vg[0] = c.p_norm == 1 ? -eps * (double)p->H * p->W : 0.0;
+            sp.det_off_vg[1] = -eps * npairs_all;
         }
     }
     IngestParams& ip = p->ip;
@@ -543,7 +571,9 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
                                                      gen3_blocks(p->W, p->H, gcap));
     const size_t ntiles = std::max<size_t>(std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk), ngblk);
     // x2: the persistent loop kernel double-buffers its per-CTA slots by phase parity
-    const size_t npart = std::max<size_t>(2 * NSLOT * ntiles, (size_t)NSLOT * world);
+    // det mode: FXW 128-bit words (2 doubles each) per CTA slot
+    const size_t npart = std::max<size_t>(std::max<size_t>(2 * NSLOT * ntiles, (size_t)NSLOT * world),
+                                          (size_t)2 * 2 * FXW * nsblk);
     const size_t ntrace = (size_t)(c.n_iter + 1) * 6;
     const size_t nd = npart + NSLOT + ntrace + (size_t)NSLOT * world + 1;   // + the grid-barrier counter
     e = cudaMalloc(&p->dmem, nd * sizeof(double));
@@ -561,7 +591,10 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         // the per-phase kernels (deferred reduction), which bench.py uses for the per-kernel split.
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c.device);
-        p->persist = p->stream_path && world == 1 && !virt && coop && std::getenv("FLMISR_NO_PERSIST") == nullptr;
+        p->persist = p->stream_path && world == 1 && !virt && coop &&
+                     (c.det_rows || std::getenv("FLMISR_NO_PERSIST") == nullptr);
+        if (c.det_rows && world == 1 && !virt && !coop)
+            return cleanup_fail(fail(FLMISR_ERR_CONFIG, "det_rows needs cooperative launch (the persistent loop kernel)"));
     }
     e = cudaMalloc(&p->st, sizeof(ScgState));
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc state: ") + cudaGetErrorString(e)));
@@ -929,13 +962,15 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
             looped = true;
             CUDA_TRY(mark());   // ev2: end of the loop kernel
             p->prof_mode = 1;
-        } else if (le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorNotSupported) {
+        } else if ((le == cudaErrorCooperativeLaunchTooLarge || le == cudaErrorNotSupported) && !p->sp.det) {
             cudaGetLastError();   // not co-resident on this device / context: per-kernel launches instead
             p->persist = 0;
         } else {
             return fail(FLMISR_ERR_CUDA, std::string("persistent SCG loop launch: ") + cudaGetErrorString(le));
         }
     }
+    if (!looped && p->sp.det)   // the per-phase kernels (NCCL transport) sum in fp64, not exactly
+        return fail(FLMISR_ERR_CONFIG, "det_rows at world > 1 needs the peer transport (flmisr_peer_connect)");
     // world > 1 over NCCL: the per-phase kernels, the halo send/recv, the consensus allgather and the
     // scalar kernels are captured into the same graph (NCCL operations are graph-capturable; SURVEY
     // 8(e)); every rank captures the same operation sequence, so graph and eager ranks still match.
@@ -1093,6 +1128,8 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
         if (!q || !q->virt || q->cfg.world != g || q->cfg.rank != h || q->H != plans[0]->H || q->W != plans[0]->W ||
             q->cfg.n_iter != plans[0]->cfg.n_iter || q->cfg.device != plans[0]->cfg.device)
             return fail(FLMISR_ERR_SHAPE, "plans must be flmisr_plan_virtual bands 0..g-1 of one configuration");
+        if (q->cfg.det_rows)
+            return fail(FLMISR_ERR_CONFIG, "det_rows bands run on the peer protocol: use flmisr_reconstruct_virtual_peer");
     }
     CUDA_TRY(cudaSetDevice(plans[0]->cfg.device));
     cudaStream_t s = plans[0]->stream;
@@ -1205,7 +1242,7 @@ static void peer_fill(PeerLoop& pl, int world, unsigned char* const* mem_of_rank
     pl.drop_band = -1;
     if (const char* ev = std::getenv("FLMISR_PEER_TEST_DROP")) pl.drop_band = std::atoi(ev);
 }
-static int peer_ctas(const flmisr_plan_s* p) { return (p->sp.nitems + SWPB - 1) / SWPB; }
+static int peer_ctas(const flmisr_plan_s* p) { return (p->sp.loop_warps + SWPB - 1) / SWPB; }
 
 // The g row bands of one reconstruction on ONE device, synchronised through the peer-loop protocol
 // (mailboxes, flags, halo rows stored into the neighbours' buffers) in one cooperative launch of
@@ -1218,7 +1255,8 @@ flmisr_status flmisr_reconstruct_virtual_peer(flmisr_plan_t* plans, int32_t g, c
     for (int h = 0; h < g; ++h) {
         flmisr_plan_s* q = plans[h];
         if (!q || !q->virt || q->cfg.world != g || q->cfg.rank != h || q->H != plans[0]->H || q->W != plans[0]->W ||
-            q->cfg.n_iter != plans[0]->cfg.n_iter || q->cfg.device != plans[0]->cfg.device || !q->stream_path)
+            q->cfg.n_iter != plans[0]->cfg.n_iter || q->cfg.device != plans[0]->cfg.device || !q->stream_path ||
+            q->cfg.det_rows != plans[0]->cfg.det_rows)
             return fail(FLMISR_ERR_SHAPE, "plans must be flmisr_plan_virtual streaming bands 0..g-1 of one configuration");
         ctas = std::max(ctas, peer_ctas(q));
     }
@@ -1299,7 +1337,7 @@ static uint64_t cfg_digest(const flmisr_config& c) {
         for (size_t i = 0; i < n; ++i) { h ^= ((const unsigned char*)d)[i]; h *= 1099511628211ull; }
     };
     const int32_t iv[] = {c.k, c.lr_h, c.lr_w, c.psf_h, c.psf_w, c.mag, c.p_norm, c.btv_window, c.n_iter,
-                          c.btv_offsets, c.curv_mode, c.scg_rules, c.x0_mode};
+                          c.btv_offsets, c.curv_mode, c.scg_rules, c.x0_mode, c.det_rows};
     const double dv[] = {c.l1_eps, c.lambda, c.btv_alpha, c.scg_sigma0, c.scg_lambda0};
     mix(iv, sizeof(iv));
     mix(dv, sizeof(dv));

@@ -65,7 +65,14 @@ struct StencilParams {
     // affine correction of the raw CTA sums before the scalar logic: tot = raw * aff[k] + aff[4+k]
     double aff_vg[2 * NSLOT], aff_uc[2 * NSLOT];
     int deferred;                // streaming kernels: deferred reduction (world == 1), see ScgState::pend
+    // det mode (flmisr_config.det_rows > 0): work items are fixed global tiles, sums exact 128-bit fixed
+    // point; the affine offsets are the whole image's (applied once to the exact all-band total)
+    int det;
+    int loop_warps;              // warps of the persistent loop kernels: nitems, or (det) at most one wave
+    double det_off_vg[NSLOT], det_off_uc[NSLOT];
 };
+// det mode: 128-bit words per CTA partial (NSLOT exact sums + the count of non-finite tile values)
+constexpr int FXW = NSLOT + 1;
 
 // Streaming kernels (flmisr_stream.cu): strips of SCOLS columns per warp, stepping by SSTEP.
 #ifndef FLMISR_SWPB

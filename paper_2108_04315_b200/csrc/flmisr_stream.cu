@@ -200,15 +200,17 @@ struct VG {
                             if (dx >= 2) uA.y = 0.f;
                             if (dx >= 1) uB.y = 0.f;
                         }
-                        if (orow) {
-                            float2 vA = mul2(qA, rA), vB = mul2(qB, rB);
-                            if (!g.cv0) { vA = F2(0.f, 0.f); vB = vA; }
+                        if (orow) {   // masked q: fma(0, rs, v) = v, and a valid pair rounds exactly as in
+                                      // the interior code (det mode: a tile's sums do not depend on whether
+                                      // a band edge made it a border piece)
+                            float2 mA = qA, mB = qB;
+                            if (!g.cv0) { mA = F2(0.f, 0.f); mB = mA; }
                             if (!g.cv4) {
-                                if (dx >= 2) vA.y = 0.f;
-                                if (dx >= 1) vB.y = 0.f;
+                                if (dx >= 2) mA.y = 0.f;
+                                if (dx >= 1) mB.y = 0.f;
                             }
-                            vb[cls] = fma2s(1.0f, vA, vb[cls]);
-                            vb[cls] = fma2s(1.0f, vB, vb[cls]);
+                            vb[cls] = fma2(mA, rA, vb[cls]);
+                            vb[cls] = fma2(mB, rB, vb[cls]);
                         }
                     } else if (orow) {
                         vb[cls] = fma2(qA, rA, vb[cls]);
@@ -650,6 +652,41 @@ __device__ FL_PHASE_INLINE void uc_phase(const StencilParams& sp, const Buffers&
     acc[3] = a_mu;
 }
 
+// det mode: the CTA's exact per-warp accumulators (one instance per CTA in the kernels that use them)
+__device__ __forceinline__ FxCta<SWPB>& fx_shared() {
+    __shared__ FxCta<SWPB> fc;
+    return fc;
+}
+
+// det mode: this warp's work items it0, it0 + stride, ... (fixed global tiles); each tile's sums are
+// committed exactly, so neither the item -> warp assignment nor the band split changes the totals
+template <int BW, int PN>
+__device__ __forceinline__ void vg_items(const StencilParams& sp, const Buffers& b, const Ring& ring, int it0,
+                                         int stride, int xcur, int rcur, float alpha, uint32_t& par) {
+    FxCta<SWPB>& fc = fx_shared();
+    fx_zero(fc);
+    __syncthreads();
+    for (int it = it0; it < sp.nitems; it += stride) {
+        const Geo g = geometry_item(sp, it);
+        double acc[NSLOT];
+        vg_phase<BW, PN>(sp, b, g, ring, xcur, rcur, alpha, par, acc);
+        fx_commit(fc, acc);
+    }
+}
+template <int BW, int PN>
+__device__ __forceinline__ void uc_items(const StencilParams& sp, const Buffers& b, const Ring& ring, int it0,
+                                         int stride, int xcur, int rcur, float au, float be, uint32_t& par) {
+    FxCta<SWPB>& fc = fx_shared();
+    fx_zero(fc);
+    __syncthreads();
+    for (int it = it0; it < sp.nitems; it += stride) {
+        const Geo g = geometry_item(sp, it);
+        double acc[NSLOT];
+        uc_phase<BW, PN>(sp, b, g, ring, xcur, rcur, au, be, par, acc);
+        fx_commit(fc, acc);
+    }
+}
+
 template <int BW, int PN>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -721,12 +758,13 @@ __global__ void k_settle(StencilParams sp, Buffers b) {
 // reduction or on kernel teardown and relaunch.  CTA 0 writes the trace and the final state.
 // ------------------------------------------------------------------------------------------------
 
-template <int BW, int PN>
+template <int BW, int PN, bool DET>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_loop(const __grid_constant__ StencilParams sp,
                                                                 const __grid_constant__ Buffers b) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ ScgState S;
-    const Geo g = geometry(sp, blockIdx.x);
+    const Geo g = geometry(sp, blockIdx.x);   // DET: unused (items are taken in a grid-stride loop)
+    const int it0 = blockIdx.x * SWPB + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     if (threadIdx.x == 0) S = *b.st;
@@ -745,11 +783,18 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_loop(const __grid_cons
     for (int pass = 0; !ui(S.done); ++pass) {
         if (pass > 0) {
             if (ui(S.success)) {   // update x, p and the curvature at the new direction
-                uc_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f), par, acc);
-                grid_sum(acc, b.part, b.gbar, epoch++, tot);
+                if constexpr (DET) {
+                    uc_items<BW, PN>(sp, b, ring, it0, gridDim.x * SWPB, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f),
+                                     uf(S.beta_f), par);
+                    grid_sum_det(fx_shared(), b.part, b.gbar, epoch++, tot);
+                } else {
+                    uc_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f), par, acc);
+                    grid_sum(acc, b.part, b.gbar, epoch++, tot);
+                }
                 if (threadIdx.x == 0) {
                     S.xcur ^= 1;
-                    affine<1>(sp, tot);
+                    if constexpr (DET) affine_det<1>(sp, tot);
+                    else affine<1>(sp, tot);
                     scg_after_curv(&S, tot);
                 }
             } else if (threadIdx.x == 0) {   // rejected step: delta is reused
@@ -758,10 +803,17 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_loop(const __grid_cons
             __syncthreads();
             if (ui(S.done)) break;
         }
-        vg_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par, acc);
-        grid_sum(acc, b.part, b.gbar, epoch++, tot);
+        if constexpr (DET) {
+            vg_items<BW, PN>(sp, b, ring, it0, gridDim.x * SWPB, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f,
+                             par);
+            grid_sum_det(fx_shared(), b.part, b.gbar, epoch++, tot);
+        } else {
+            vg_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par, acc);
+            grid_sum(acc, b.part, b.gbar, epoch++, tot);
+        }
         if (threadIdx.x == 0) {
-            affine<0>(sp, tot);
+            if constexpr (DET) affine_det<0>(sp, tot);
+            else affine<0>(sp, tot);
             scg_after_value(&S, tot, trace, pass > 0 ? PH_ITER : PH_INIT);
         }
         __syncthreads();
@@ -878,10 +930,56 @@ __device__ bool peer_sum(const StencilParams& sp, const PeerLoop& pl, int l, int
     return true;
 }
 
-template <int BW, int PN>
+// det mode: peer_sum with exact fixed-point CTA slots (FXW words) and the whole image's affine offsets
+// applied once to the exact all-band total -- the same bits at every band count
+__device__ bool peer_sum_det(const StencilParams& sp, const PeerLoop& pl, int l, int j, int which, unsigned epoch,
+                             double (&tot)[NSLOT]) {
+    __shared__ int s_timeout;
+    const int C = pl.ctas, h = pl.rank0 + l, world = pl.world;
+    const bool sys = pl.g == 1;
+    const size_t par = (size_t)(epoch & 1) * world * C * FXW;
+    const FxCta<SWPB>& fc = fx_shared();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __int128 v[FXW];
+#pragma unroll
+        for (int k = 0; k < FXW; ++k) v[k] = fx_cta(fc, k);
+        const size_t o = par + ((size_t)h * C + j) * FXW;
+        for (int q = 0; q < world; ++q) {
+            __int128* mb = reinterpret_cast<__int128*>(pl.mbox[q]);
+#pragma unroll
+            for (int k = 0; k < FXW; ++k) mb[o + k] = v[k];
+        }
+        if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (h != pl.drop_band) {
+            for (int q = 0; q < world; ++q) {
+                if (sys) asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(pl.cnt[q]) : "memory");
+                else asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(pl.cnt[q]) : "memory");
+            }
+        }
+        const unsigned long long target = (unsigned long long)(epoch + 1) * (unsigned long long)(world * C);
+        unsigned spins = 0;
+        const unsigned long long tstart = now_ns();
+        int to = 0;
+        while (ld_acquire_u64(pl.cnt[h], sys) < target)
+            if ((++spins & 1023u) == 0 && now_ns() - tstart > pl.timeout_ns) { to = 1; break; }
+        s_timeout = to;
+    }
+    __syncthreads();
+    if (s_timeout) return false;
+    fx_sum_slots(reinterpret_cast<const __int128*>(pl.mbox[h]) + par, world * C, tot);
+    if (which == 0) affine_det<0>(sp, tot);
+    else affine_det<1>(sp, tot);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    return true;
+}
+
+template <int BW, int PN, bool DET>
 __device__ __forceinline__ void peer_loop_body(const StencilParams& sp, const Buffers& b, const PeerLoop& pl, int l,
                                                int j, unsigned char* smem, ScgState& S) {
-    const Geo g = geometry(sp, j);
+    const Geo g = geometry(sp, j);   // DET: unused (grid-stride items of the band)
+    const int it0 = j * SWPB + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), stride = pl.ctas * SWPB;
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     __shared__ unsigned s_e0;
@@ -899,8 +997,16 @@ __device__ __forceinline__ void peer_loop_body(const StencilParams& sp, const Bu
     for (int pass = 0; !ui(S.done); ++pass) {
         if (pass > 0) {
             if (ui(S.success)) {
-                uc_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f), par, acc);
-                if (!peer_sum(sp, pl, l, j, 1, acc, epoch++, tot)) {
+                bool ok;
+                if constexpr (DET) {
+                    uc_items<BW, PN>(sp, b, ring, it0, stride, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f),
+                                     par);
+                    ok = peer_sum_det(sp, pl, l, j, 1, epoch++, tot);
+                } else {
+                    uc_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f), par, acc);
+                    ok = peer_sum(sp, pl, l, j, 1, acc, epoch++, tot);
+                }
+                if (!ok) {
                     if (threadIdx.x == 0) { S.done = 1; S.failed_stage = FAIL_PEER_TIMEOUT; S.failed_iter = S.k; }
                     __syncthreads();
                     break;
@@ -915,8 +1021,15 @@ __device__ __forceinline__ void peer_loop_body(const StencilParams& sp, const Bu
             __syncthreads();
             if (ui(S.done)) break;
         }
-        vg_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par, acc);
-        if (!peer_sum(sp, pl, l, j, 0, acc, epoch++, tot)) {
+        bool ok;
+        if constexpr (DET) {
+            vg_items<BW, PN>(sp, b, ring, it0, stride, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par);
+            ok = peer_sum_det(sp, pl, l, j, 0, epoch++, tot);
+        } else {
+            vg_phase<BW, PN>(sp, b, g, ring, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par, acc);
+            ok = peer_sum(sp, pl, l, j, 0, acc, epoch++, tot);
+        }
+        if (!ok) {
             if (threadIdx.x == 0) { S.done = 1; S.failed_stage = FAIL_PEER_TIMEOUT; S.failed_iter = S.k; }
             __syncthreads();
             break;
@@ -931,25 +1044,25 @@ __device__ __forceinline__ void peer_loop_body(const StencilParams& sp, const Bu
 }
 
 // one band per launch (multi-GPU): parameters in the constant bank
-template <int BW, int PN>
+template <int BW, int PN, bool DET>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_peer_loop(const __grid_constant__ StencilParams sp,
                                                                      const __grid_constant__ Buffers b,
                                                                      const __grid_constant__ PeerLoop pl) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ ScgState S;
-    peer_loop_body<BW, PN>(sp, b, pl, 0, blockIdx.x, smem, S);
+    peer_loop_body<BW, PN, DET>(sp, b, pl, 0, blockIdx.x, smem, S);
 }
 
 // all bands in one cooperative launch (one device): band l = blockIdx.x / ctas; every band's
 // parameters in the constant bank (block-uniform index)
-template <int BW, int PN>
+template <int BW, int PN, bool DET>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_scg_peer_loop_multi(const __grid_constant__ PeerLoop pl,
                                                                            const __grid_constant__ PeerBands pb) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ ScgState S;
     const int l = __shfl_sync(0xffffffffu, (int)(blockIdx.x / pl.ctas), 0);
     const int j = blockIdx.x - l * pl.ctas;
-    peer_loop_body<BW, PN>(pb.sp[l], pb.b[l], pl, l, j, smem, S);
+    peer_loop_body<BW, PN, DET>(pb.sp[l], pb.b[l], pl, l, j, smem, S);
 }
 
 bool pdl_enabled() {
@@ -1042,7 +1155,9 @@ cudaError_t launch_settle(const StencilParams& sp, const Buffers& b, cudaStream_
 cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, const Buffers& b, cudaStream_t s) {
     switch (bw * 10 + pn) {
 #define FL_LCASE(BW_, PN_) \
-    case BW_ * 10 + PN_: return launch_loop(k_scg_loop<BW_, PN_>, sp.nitems, sp, b, s);
+    case BW_ * 10 + PN_:   \
+        return sp.det ? launch_loop(k_scg_loop<BW_, PN_, true>, sp.loop_warps, sp, b, s) \
+                      : launch_loop(k_scg_loop<BW_, PN_, false>, sp.loop_warps, sp, b, s);
         FL_LCASE(1, 1) FL_LCASE(1, 2) FL_LCASE(2, 1) FL_LCASE(2, 2) FL_LCASE(3, 1) FL_LCASE(3, 2)
 #undef FL_LCASE
         default: return cudaErrorInvalidValue;
@@ -1071,8 +1186,11 @@ cudaError_t launch_scg_peer_loop(int bw, int pn, const StencilParams& sp, const 
     switch (bw * 10 + pn) {
 #define FL_PCASE(BW_, PN_) \
     case BW_ * 10 + PN_:   \
-        return pl.g == 1 ? launch_coop(k_scg_peer_loop<BW_, PN_>, pl.ctas, s, sp, b, pl) \
-                         : launch_coop(k_scg_peer_loop_multi<BW_, PN_>, pl.g * pl.ctas, s, pl, *pb);
+        if (sp.det)        \
+            return pl.g == 1 ? launch_coop(k_scg_peer_loop<BW_, PN_, true>, pl.ctas, s, sp, b, pl) \
+                             : launch_coop(k_scg_peer_loop_multi<BW_, PN_, true>, pl.g * pl.ctas, s, pl, *pb); \
+        return pl.g == 1 ? launch_coop(k_scg_peer_loop<BW_, PN_, false>, pl.ctas, s, sp, b, pl) \
+                         : launch_coop(k_scg_peer_loop_multi<BW_, PN_, false>, pl.g * pl.ctas, s, pl, *pb);
         FL_PCASE(1, 1) FL_PCASE(1, 2) FL_PCASE(2, 1) FL_PCASE(2, 2) FL_PCASE(3, 1) FL_PCASE(3, 2)
 #undef FL_PCASE
         default: return cudaErrorInvalidValue;

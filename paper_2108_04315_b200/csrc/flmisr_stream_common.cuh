@@ -196,16 +196,12 @@ struct Geo {
 // index within its band in the peer loop)
 // HALO: columns of overlap per strip side (the operator's column reach): SHALO = 2 for the common-kappa
 // kernels, 4 for the per-phase 4x4 kernels; strips step by SCOLS - 2 HALO
-template <int HALO = SHALO, int WPB = SWPB>
-__device__ __forceinline__ Geo geometry(const StencilParams& sp, int cta) {
+// gw: the work item (warp-uniform); geometry() below takes the item of this warp of CTA cta
+template <int HALO = SHALO>
+__device__ __forceinline__ Geo geometry_item(const StencilParams& sp, int gw) {
     constexpr int STEP = SCOLS - 2 * HALO;
     Geo g;
-    // warp index through a lane-0 shuffle so the compiler sees it (and every row pointer and the
-    // ring addresses derived from it) as warp-uniform: the bulk copies then take uniform-register
-    // operands directly instead of a per-copy R2UR waterfall
-    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     g.lane = threadIdx.x & 31;
-    const int gw = cta * WPB + warp;
     g.live = gw < sp.nitems;
     // work item -> (strip, rows [r_lo, r_hi)); see StencilParams: border pieces (band edges, edge
     // strips) are seg_b rows, interior pieces seg_rows rows
@@ -259,6 +255,113 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp, int cta) {
     g.border = true;
 #endif
     return g;
+}
+
+template <int HALO = SHALO, int WPB = SWPB>
+__device__ __forceinline__ Geo geometry(const StencilParams& sp, int cta) {
+    // warp index through a lane-0 shuffle so the compiler sees it (and every row pointer and the
+    // ring addresses derived from it) as warp-uniform: the bulk copies then take uniform-register
+    // operands directly instead of a per-copy R2UR waterfall
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    return geometry_item<HALO>(sp, cta * WPB + warp);
+}
+
+// ---- det mode: exact sums in 128-bit fixed point (value = s 2^-64) ----
+// Integer addition is associative, so a sum of fixed-point values does not depend on the order or the
+// grouping of its terms: the per-tile fp64 values (bit-identical at every band count, same rows, same
+// arithmetic) give the same total whether they are summed per CTA, per band or over all bands.  The
+// conversion of a tile value truncates below 2^-64 (deterministic); |value| < 2^63 (the sums here are
+// <= ~1e12); a non-finite tile value is counted instead (the total becomes NaN -> FLMISR_ERR_NUMERIC).
+__device__ __forceinline__ __int128 fx_of(double v) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    if (ex == 0) return 0;   // zero / subnormal: below the grid
+    const unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+    const int sh = ex - 1075 + 64;   // v = m 2^(ex - 1075) = (m << sh) 2^-64
+    unsigned __int128 a;
+    if (sh >= 0) a = sh < 74 ? (unsigned __int128)m << sh : ((unsigned __int128)1 << 126);   // saturate
+    else a = sh > -53 ? (unsigned __int128)(m >> (-sh)) : 0;
+    return (bits >> 63) ? -(__int128)a : (__int128)a;
+}
+__device__ __forceinline__ double fx_to_double(__int128 s) {
+    const long long hi = (long long)(s >> 64);
+    const unsigned long long lo = (unsigned long long)s;
+    return (double)hi + (double)lo * 5.421010862427522e-20;   // 2^-64
+}
+__device__ __forceinline__ __int128 fx_shfl_xor(__int128 v, int o) {
+    const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(v >> 64), o);
+    const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)v, o);
+    return (__int128)(((unsigned __int128)(unsigned long long)hi << 64) | lo);
+}
+__device__ __forceinline__ __int128 fx_warp_sum(__int128 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += fx_shfl_xor(v, o);
+    return v;
+}
+__device__ __forceinline__ __int128 ld_relaxed_fx(const __int128* p) {
+    unsigned long long lo, hi;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+    return (__int128)(((unsigned __int128)hi << 64) | lo);
+}
+
+// per-warp exact accumulators of one phase (shared memory; lane 0 of each warp owns its row)
+template <int WPB>
+struct FxCta {
+    __int128 s[WPB][FXW];
+};
+// every lane of a warp: this tile's per-lane fp64 partials -> fp64 warp tree (the same tile gives the same
+// bits in every launch configuration) -> exact add into the warp's accumulators
+template <int WPB>
+__device__ __forceinline__ void fx_commit(FxCta<WPB>& fc, const double (&acc)[NSLOT]) {
+    const int warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        const double v = warp_sum(acc[k]);
+        if ((threadIdx.x & 31) == 0) {
+            if (isfinite(v)) fc.s[warp][k] += fx_of(v);
+            else fc.s[warp][NSLOT] += 1;
+        }
+    }
+}
+// all threads: zero the accumulators (before a phase; a __syncthreads must separate it from any use)
+template <int WPB>
+__device__ __forceinline__ void fx_zero(FxCta<WPB>& fc) {
+    for (int i = threadIdx.x; i < WPB * FXW; i += blockDim.x) (&fc.s[0][0])[i] = 0;
+}
+// threads k < FXW after a __syncthreads: this CTA's exact sum k (fixed order, exact anyway)
+template <int WPB>
+__device__ __forceinline__ __int128 fx_cta(const FxCta<WPB>& fc, int k) {
+    __int128 t = 0;
+    for (int w = 0; w < WPB; ++w) t += fc.s[w][k];
+    return t;
+}
+// all threads: exact sum of n slots of FXW words at slot[i * FXW + k] -> tot (scaled and offset by the
+// caller); the count of non-finite tile values makes every total NaN
+__device__ __forceinline__ void fx_sum_slots(const __int128* slot, int n, double (&tot)[NSLOT]) {
+    __shared__ __int128 sred[32][FXW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __int128 loc[FXW];
+#pragma unroll
+    for (int k = 0; k < FXW; ++k) loc[k] = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < FXW; ++k) loc[k] += ld_relaxed_fx(slot + (size_t)i * FXW + k);
+#pragma unroll
+    for (int k = 0; k < FXW; ++k) {
+        const __int128 v = fx_warp_sum(loc[k]);
+        if (lane == 0) sred[warp][k] = v;
+    }
+    __syncthreads();
+    __int128 t[FXW];
+#pragma unroll
+    for (int k = 0; k < FXW; ++k) {
+        t[k] = 0;
+        for (int w = 0; w < nw; ++w) t[k] += sred[w][k];
+    }
+    __syncthreads();   // sred is reused by the next call
+    const bool bad = t[NSLOT] != 0;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) tot[k] = bad ? __longlong_as_double(0x7ff8000000000000ll) : fx_to_double(t[k]);
 }
 
 __device__ __forceinline__ float shup(float v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -370,6 +473,36 @@ __device__ void grid_sum(const double (&acc)[NSLOT], double* part, unsigned* gba
     FL_TMARK(epoch, 3)
     // the next phase reads other CTAs' generic-proxy stores through the bulk-copy (async) proxy
     asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// det mode: the grid barrier of grid_sum with exact fixed-point CTA slots (FXW words each)
+template <int WPB>
+__device__ void grid_sum_det(const FxCta<WPB>& fc, double* part, unsigned* gbar, unsigned epoch,
+                             double (&tot)[NSLOT]) {
+    const int G = gridDim.x;
+    __int128* slot = reinterpret_cast<__int128*>(part) + (size_t)(epoch & 1) * FXW * G;
+    __syncthreads();
+    if (threadIdx.x < FXW) slot[(size_t)blockIdx.x * FXW + threadIdx.x] = fx_cta(fc, threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
+        const unsigned target = (epoch + 1) * (unsigned)G;
+        unsigned spins = 0;
+        const unsigned long long tstart = now_ns();
+        while (ld_acquire_u32(gbar) < target)
+            if ((++spins & 1023u) == 0 && now_ns() - tstart > 10000000000ull) __trap();
+    }
+    __syncthreads();
+    fx_sum_slots(slot, G, tot);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// det mode: total -> the SCG sums (scale of the affine correction, the whole image's offsets)
+template <int WHICH>
+__device__ __forceinline__ void affine_det(const StencilParams& sp, double (&t)[NSLOT]) {
+    const double* aff = WHICH == 0 ? sp.aff_vg : sp.aff_uc;
+    const double* off = WHICH == 0 ? sp.det_off_vg : sp.det_off_uc;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) t[k] = t[k] * aff[k] + off[k];
 }
 
 template <int WHICH>

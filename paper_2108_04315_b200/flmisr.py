@@ -40,6 +40,7 @@ class Config(C.Structure):
         ("nccl_unique_id", C.c_void_p), ("device", C.c_int32),
         ("btv_offsets", C.c_int32), ("curv_mode", C.c_int32), ("scg_rules", C.c_int32),
         ("x0_mode", C.c_int32),
+        ("det_rows", C.c_int32),
     ]
 
 
@@ -176,7 +177,7 @@ class Plan:
     def __init__(self, k, lr_h, lr_w, shifts, psf, mag=2, p_norm=1, l1_eps=1e-3, lam=0.05,
                  btv_alpha=0.4, btv_window=3, n_iter=20, scg_sigma0=1e-4, scg_lambda0=1e-6,
                  rank=0, world=1, nccl_id: bytes | None = None, device=0, virtual=False,
-                 btv_offsets=0, scg_rules=0, curv_mode=0, x0_mode=0):
+                 btv_offsets=0, scg_rules=0, curv_mode=0, x0_mode=0, det_rows=0):
         self.shifts = np.ascontiguousarray(np.asarray(shifts, dtype=np.float64).reshape(k, 2))
         self.psf = np.ascontiguousarray(np.asarray(psf, dtype=np.float64))
         self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
@@ -184,7 +185,7 @@ class Plan:
                      self.psf.ctypes.data_as(C.POINTER(C.c_double)), self.psf.shape[0], self.psf.shape[1],
                      mag, p_norm, l1_eps, lam, btv_alpha, btv_window, n_iter, scg_sigma0, scg_lambda0,
                      rank, world, C.cast(self._id, C.c_void_p) if self._id is not None else None, device,
-                     btv_offsets, curv_mode, scg_rules, x0_mode)
+                     btv_offsets, curv_mode, scg_rules, x0_mode, det_rows)
         self.k, self.lr_h, self.lr_w, self.mag, self.n_iter = k, lr_h, lr_w, mag, n_iter
         self.rank, self.world, self.device = rank, world, device
         self._pipes = weakref.WeakSet()   # pipelines driving this plan (destroyed first)
