@@ -74,15 +74,16 @@ typedef struct {
     int32_t x0_mode;     /* initial estimate when flmisr_reconstruct* gets x0 == NULL: 0 = bilinear
                             upsample of frame 0 (reading 14); 1 = multi-image interpolation
                             fusion (reading 24: the flmisr_interp_fuse image)                */
-    int32_t det_rows;    /* 0 = off.  T >= 4: results bit-identical for every band count g (SURVEY
-                            8(e) "bit-stable"; "consensus equals centralised"): the streaming
-                            kernels' work items become fixed global tiles of T HR rows (one warp
-                            strip x T rows, the same pieces at every g), band boundaries are
-                            multiples of lcm(T, mag), and every sum (tile -> CTA -> band -> all
-                            bands) is an exact 128-bit fixed-point sum (grid 2^-64), so its value
-                            does not depend on the order or the grouping.  Needs the streaming
-                            path (fast_path 2) and, at world > 1, the peer transport
-                            (flmisr_peer_connect); costs ~2 warm-up rows per tile */
+    int32_t det_rows;    /* 0 = off.  T in [3, 4095], a multiple of 3: results bit-identical for
+                            every band count g (SURVEY 8(e) "bit-stable"; "consensus equals
+                            centralised"): rows are cut into fixed global tiles of T HR rows, band
+                            boundaries are multiples of lcm(T, mag), every warp segment is a union
+                            of whole tiles, each tile's partial sums are committed separately and
+                            every sum (tile -> lane -> CTA -> band -> all bands) is an exact 128-bit
+                            fixed-point sum (grid 2^-64), independent of order and grouping.  Needs
+                            the streaming path (fast_path 2) and, at world > 1, the peer transport
+                            (flmisr_peer_connect); else FLMISR_ERR_CONFIG.  ~1.45x the loop time on
+                            one GPU                                                  */
 } flmisr_config;
 
 typedef struct {

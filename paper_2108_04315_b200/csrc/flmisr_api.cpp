@@ -214,8 +214,8 @@ flmisr_status validate(const flmisr_config* c, bool virt) {
     if (c->n_iter < 0) return fail(FLMISR_ERR_CONFIG, "n_iter must be >= 0");
     if (c->x0_mode != 0 && c->x0_mode != 1)
         return fail(FLMISR_ERR_CONFIG, "x0_mode must be 0 (bilinear frame 0) or 1 (interpolation fusion)");
-    if (c->det_rows != 0 && (c->det_rows < 4 || c->det_rows > 4096))
-        return fail(FLMISR_ERR_CONFIG, "det_rows must be 0 (off) or in [4, 4096] HR rows");
+    if (c->det_rows != 0 && (c->det_rows < 3 || c->det_rows > 4095 || c->det_rows % 3 != 0))
+        return fail(FLMISR_ERR_CONFIG, "det_rows must be 0 (off) or a multiple of 3 in [3, 4095] HR rows");
     if (!(c->scg_lambda0 > 0.0) || !std::isfinite(c->scg_lambda0))
         return fail(FLMISR_ERR_CONFIG, "scg_lambda0 must be > 0 (S:362)");
     if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return fail(FLMISR_ERR_CONFIG, "need 0 <= rank < world");
@@ -485,18 +485,39 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             }
             S = std::min(S, pc ? to1mod3(rows) : rows + ((1 - rows % 3) + 3) % 3);   // smallest admissible >= rows
             Sb = std::min(Sb, S);
-            if (c.det_rows) S = Sb = c.det_rows;   // det mode: the fixed global tiles (bands are unions of them)
             sp.seg_rows = S;
             sp.seg_b = Sb;
             sp.nseg_i = nseg_int(S, Sb);
             if (rows <= 2 * Sb) sp.seg_rows = Sb;   // short bands: interior strips in seg_b pieces too
-            if (c.det_rows) sp.nseg_i = (rows + Sb - 1) / Sb;
-            sp.nseg_b = (rows + Sb - 1) / Sb;
+            if (c.det_rows) {
+                // det mode: the same one-wave search in units of the fixed tiles of T rows (bands are unions
+                // of them; flmisr_stream_common.cuh geometry_item), so every segment is a union of whole
+                // tiles and each tile's sums are committed exactly inside the row loop
+                const int T = c.det_rows, nt = (rows + T - 1) / T;
+                auto nseg_t = [&](int m, int mb) {
+                    return nt <= 2 * mb ? (nt + mb - 1) / mb : 2 + (nt - 2 * mb + m - 1) / m;
+                };
+                auto items_t = [&](int m, int mb) {
+                    return (long long)sp.ni * nseg_t(m, mb) + (long long)sp.ne * ((nt + mb - 1) / mb);
+                };
+                auto mb_of = [&](int m) {
+                    return std::min(m, std::max(1, (int)std::lround(((double)(m * T + 2) / ratio - 2.0) / T)));
+                };
+                int m = 1, mb = mb_of(1);
+                while (m < nt && items_t(m, mb) > cap) { ++m; mb = mb_of(m); }
+                sp.seg_rows = m * T;
+                sp.seg_b = mb * T;
+                sp.nseg_i = nseg_t(m, mb);
+                sp.nseg_b = (nt + mb - 1) / mb;
+                sp.det_rows = T;
+            } else {
+                sp.nseg_b = (rows + Sb - 1) / Sb;
+            }
             sp.n_int = sp.ni * sp.nseg_i;
             sp.nitems = sp.n_int + sp.ne * sp.nseg_b;
             sp.nsegs = sp.nseg_i;
-            // persistent loop kernels: one warp per item (one wave by construction), or in det mode at most
-            // one wave of warps taking the fixed tiles in a grid-stride loop
+            // persistent loop kernels: one warp per item (one wave by construction; in det mode unless a band
+            // has more strips x tiles than a wave holds, then a grid-stride loop over the items)
             sp.loop_warps = c.det_rows ? (int)std::min<long long>(sp.nitems, cap) : sp.nitems;
             sp.det = c.det_rows ? 1 : 0;
             // hoisted constants: D = sum q rs - eps N, R = sum gamma q rs - eps sum_d gamma_d n_d,

@@ -67,7 +67,8 @@ struct StencilParams {
     int deferred;                // streaming kernels: deferred reduction (world == 1), see ScgState::pend
     // det mode (flmisr_config.det_rows > 0): work items are fixed global tiles, sums exact 128-bit fixed
     // point; the affine offsets are the whole image's (applied once to the exact all-band total)
-    int det;
+    int det;                     // 1: det mode; det_rows = T, the tile height (segments are unions of tiles)
+    int det_rows;
     int loop_warps;              // warps of the persistent loop kernels: nitems, or (det) at most one wave
     double det_off_vg[NSLOT], det_off_uc[NSLOT];
 };

@@ -39,13 +39,33 @@ namespace {
 
 // (shared helpers, the ring, warp geometry, the grid barrier: flmisr_stream_common.cuh)
 
+// a lane-0 shuffle of a (warp-uniform) condition: the compiler then sees it as uniform, so code under it
+// needs no divergence handling and later bulk copies keep their uniform-register operands
+__device__ __forceinline__ bool uni(bool c) { return __shfl_sync(0xffffffffu, (int)c, 0) != 0; }
+
+// det mode: the CTA's exact per-lane accumulators, in dynamic shared memory after the warps' rings (the
+// det kernels are launched with RING_SMEM + FX_SMEM bytes)
+__device__ __forceinline__ FxCta<SWPB>& fx_shared() {
+    extern __shared__ __align__(128) unsigned char smem[];
+    return *reinterpret_cast<FxCta<SWPB>*>(smem + RING_SMEM);
+}
+// out of line: once per tile and slot.  Inlined, the branch-free conversion is if-converted into the
+// streaming loop body and executed (predicated off) at every row step
+__device__ __noinline__ void fx_add_f(int k, float v) { fx_lane_add(fx_shared(), k, v); }
+__device__ __noinline__ void fx_add_d(int k, double v) { fx_lane_add(fx_shared(), k, v); }
+
 // ------------------------------------------------------------------------------------------------
 // value + gradient at x' = x + alpha p (Alg. 1 lines 14-19), streaming.
 //   step t (ring stage = x,p(t+2), Y(t+1), r_old(t)): x'(t+2) -> horizontal kappa pass;
 //   w(t+1) = rho'(kappa x' - Y) -> horizontal adjoint pass hw(t+1), scattered into the pending rows
 //   t, t+1, t+2 of r = -grad J; BTV pairs of row t scattered into rows t..t+2; row t is complete.
 // ------------------------------------------------------------------------------------------------
-template <int BW, int PN, bool BORDER>
+// DET (det mode): every accumulator is committed exactly (fx_commit1) when its row closes a fixed tile
+// of T rows -- the data value of row t+1 (group A) and the BTV / <r,r> / <r,r_old> sums of row t
+// (group B) in step t.  T % 3 == 0 and segments start on a tile boundary, so every tile boundary inside
+// a segment falls on the same unrolled step of each group (A: step<0>, B: step<1>): one commit site per
+// group in the loop body; the segment's last (possibly short) tile is flushed after the loop.
+template <int BW, int PN, bool BORDER, bool DET = false>
 struct VG {
     float2 XA[3], XB[3];            // x' pairs (c0,c2), (c1,c3) of rows t, t+1, t+2 (slot (t+k)%3)
     float X4[3], X5[3];             // x' at c4, c5 (the right lane's c0, c1)
@@ -55,6 +75,7 @@ struct VG {
     const float *ix, *ip, *iy, *ir; // interior warps: next rows to stage (strip start column)
     float* qw;                      // interior warps: r_new row of the current step (lane column)
     int t0, nstep;
+    int bA, bB;                     // DET: end row of the tile the data value / the row-t sums are in
 
     const StencilParams& sp;
     const Buffers& b;
@@ -139,6 +160,12 @@ struct VG {
                 }
                 wA = mul2(eA, rA);
                 wB = mul2(eB, rB);
+            }
+            if constexpr (DET && PH == 0) {
+                if (uni(orow && tw + 1 == bA)) {   // row tw closes its tile: the tile's data value
+                    commit_a();
+                    bA = min(bA + sp.det_rows, g.r_hi);
+                }
             }
             if (BORDER && !(tw >= 0 && tw < sp.H && g.cv0)) { wA = F2(0.f, 0.f); wB = wA; }   // zero-padded
             float wm1 = shup(wB.y), w4 = shdn(wA.x);
@@ -260,11 +287,32 @@ struct VG {
                         g.ohi);
             }
             GA[s0] = GB[s0] = GD[s0] = GE[s0] = F2(0.f, 0.f);
+            if constexpr (DET && PH == 1) {
+                if (uni(orow && t + 1 == bB)) {   // row t closes its tile: BTV value, <r,r>, <r,r_old>
+                    commit_b();
+                    bB = min(bB + sp.det_rows, g.r_hi);
+                }
+            }
         }
 
         // the stage is consumed: refill it with the rows of step t + NST
         ring.release();
         if (t + NST < t0 + nstep) issue(rs_, t + NST);
+    }
+
+    // DET: exact commits of the partial tile sums (the same per-lane combination as vg_phase's msum)
+    __device__ __forceinline__ void commit_a() {
+        fx_add_f(0, msum(accd, g));
+        accd = F2(0.f, 0.f);
+    }
+    __device__ __forceinline__ void commit_b() {
+        fx_add_d(1, sp.gcls[0] * msum(vb[0], g) + sp.gcls[1] * msum(vb[1], g) + sp.gcls[2] * msum(vb[2], g) +
+                        sp.gcls[3] * msum(vb[3], g));
+        fx_add_f(2, msum(rr, g));
+        fx_add_f(3, msum(rro, g));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) vb[c] = F2(0.f, 0.f);
+        rr = rro = F2(0.f, 0.f);
     }
 
     // par: the ring's current mbarrier phase parity (all stages advance together); carried across
@@ -276,6 +324,7 @@ struct VG {
         for (int c = 0; c < 4; ++c) vb[c] = z;
 #pragma unroll
         for (int s = 0; s < 3; ++s) GA[s] = GB[s] = GD[s] = GE[s] = z;
+        if (DET) bA = bB = min(g.r_lo + sp.det_rows, g.r_hi);   // segments start on a tile boundary
         t0 = g.r_lo - 2;
         nstep = (g.r_hi - g.r_lo + 4) / 3 * 3;   // rows r_lo - 2 .. r_hi - 1, rounded up to the unroll
         if (!BORDER) {
@@ -295,6 +344,10 @@ struct VG {
             step<1>(t + 1, par);
             step<2>(t + 2, par);
             par ^= 1u;
+        }
+        if (DET) {   // the segment's last tile (an exact zero when the loop committed it already)
+            commit_a();
+            commit_b();
         }
     }
 };
@@ -383,13 +436,25 @@ __device__ __forceinline__ void publish(const double (&acc)[NSLOT], double* part
 
 // One value+gradient phase of this CTA's warps: acc = this thread's share of {D, R (gamma-weighted),
 // <r',r'>, <r',r_old>} (summed over the CTA and the grid by the caller).
-template <int BW, int PN>
+// DET: the sums are committed per tile inside the row loop (fx_shared); acc is not written
+template <int BW, int PN, bool DET = false>
 __device__ FL_PHASE_INLINE void vg_phase(const StencilParams& sp, const Buffers& b, const Geo& g, const Ring& ring,
                                          int xcur, int rcur, float alpha, uint32_t& par, double (&acc)[NSLOT]) {
     const float* X = pick(b.X, xcur);
     const float* P = pick(b.P, xcur);
     const float* Ro = pick(b.R, rcur);
     float* Rn = pick(b.R, rcur ^ 1);
+    if constexpr (DET) {
+        if (!g.live) {
+        } else if (g.border) {
+            VG<BW, PN, true, true> v(sp, b, g, ring, X, P, Ro, Rn, alpha);
+            v.run(par);
+        } else {
+            VG<BW, PN, false, true> v(sp, b, g, ring, X, P, Ro, Rn, alpha);
+            v.run(par);
+        }
+        return;
+    }
     float ad = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, a_rr = 0.f, a_rro = 0.f;
     if (!g.live) {
     } else if (g.border) {
@@ -461,7 +526,10 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp
 // p^T Hess J p, <p,p>, <p,r> at the new (x, p) (lines 6-12; reading 16), streaming.
 //   ring stage of step t: x, p, r at row t+2, Y at row t+1.
 // ------------------------------------------------------------------------------------------------
-template <int BW, int PN, bool BORDER>
+// DET: as in VG -- the data curvature of row t+1 (group A, step<0>), the BTV curvature of row t (group
+// B, step<1>) and <p,p>, <p,r> of row t+2 (group C, set in step t, step<2>) are committed when their row
+// closes a tile; the last tile after the loop
+template <int BW, int PN, bool BORDER, bool DET = false>
 struct UC {
     float2 XA[3], XB[3], PA[3], PB[3];   // new x / p pairs (c0,c2), (c1,c3)
     float X4[3], X5[3], P4[3], P5[3];    // new x / p at c4, c5
@@ -469,6 +537,7 @@ struct UC {
     float2 cd, cb[4], pp, mu;            // .x: columns c0+c1, .y: columns c2+c3
     const float *ix, *ip, *ir, *iy;      // interior warps: next rows to stage (strip start column)
     int t0, nstep;
+    int bA, bB, bC;                      // DET: tile end rows of the cd / cb / (pp, mu) rows
     const StencilParams& sp;
     const Buffers& b;
     const Geo& g;
@@ -535,6 +604,12 @@ struct UC {
         ring.wait(rs_, par);
         set_row(sa, t + 2, fixr<BORDER>(ring.get(rs_, 0, g.lane), g), fixr<BORDER>(ring.get(rs_, 1, g.lane), g),
                 fixr<BORDER>(ring.get(rs_, 2, g.lane), g));
+        if constexpr (DET && PH == 2) {
+            if (uni(t + 2 >= g.r_lo && t + 2 < g.r_hi && t + 3 == bC)) {   // row t+2 closes its tile: <p,p>, <p,r>
+                commit_c();
+                bC = min(bC + sp.det_rows, g.r_hi);
+            }
+        }
         const float4 fy = fixr<BORDER>(ring.get(rs_, 3, g.lane), g);
         // data curvature at row t+1: rho''(e) (A p)^2 = eps^2 rs^3 (A p)^2 (eps^2 in the affine term)
         {
@@ -553,6 +628,12 @@ struct UC {
                     const float2 uA = mul2(rA, apA), uB = mul2(rB, apB);
                     cd = fma2(mul2(uA, uA), rA, cd);
                     cd = fma2(mul2(uB, uB), rB, cd);
+                }
+                if constexpr (DET && PH == 0) {
+                    if (uni(tz + 1 == bA)) {   // row tz closes its tile: the tile's data curvature
+                        commit_a();
+                        bA = min(bA + sp.det_rows, g.r_hi);
+                    }
                 }
             }
         }
@@ -589,7 +670,29 @@ struct UC {
                     cb[cls] = fma2(mul2(uB, uB), rB, cb[cls]);
                 }
             }
+            if constexpr (DET && PH == 1) {
+                if (uni(t + 1 == bB)) {   // row t closes its tile: the tile's BTV curvature
+                    commit_b();
+                    bB = min(bB + sp.det_rows, g.r_hi);
+                }
+            }
         }
+    }
+
+    __device__ __forceinline__ void commit_a() {
+        fx_add_f(0, msum(cd, g));
+        cd = F2(0.f, 0.f);
+    }
+    __device__ __forceinline__ void commit_b() {
+        fx_add_d(1, sp.gcls[0] * msum(cb[0], g) + sp.gcls[1] * msum(cb[1], g) + sp.gcls[2] * msum(cb[2], g) +
+                        sp.gcls[3] * msum(cb[3], g));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cb[c] = F2(0.f, 0.f);
+    }
+    __device__ __forceinline__ void commit_c() {
+        fx_add_f(2, msum(pp, g));
+        fx_add_f(3, msum(mu, g));
+        pp = mu = F2(0.f, 0.f);
     }
 
     // par: the ring's current mbarrier phase parity (all stages advance together); carried across
@@ -599,6 +702,7 @@ struct UC {
         cd = pp = mu = z;
 #pragma unroll
         for (int c = 0; c < 4; ++c) cb[c] = z;
+        if (DET) bA = bB = bC = min(g.r_lo + sp.det_rows, g.r_hi);   // segments start on a tile boundary
         t0 = g.r_lo - 2;
         nstep = (g.r_hi - g.r_lo + 4) / 3 * 3;
         if (!BORDER) {
@@ -619,12 +723,17 @@ struct UC {
             step<2>(t + 2, par);
             par ^= 1u;
         }
+        if (DET) {   // the segment's last tile
+            commit_a();
+            commit_b();
+            commit_c();
+        }
     }
 };
 
 // One update+curvature phase of this CTA's warps: acc = {sum rho'' (A p)^2, BTV curvature
 // (gamma-weighted), <p,p>, <p,r>} at the new (x, p).
-template <int BW, int PN>
+template <int BW, int PN, bool DET = false>
 __device__ FL_PHASE_INLINE void uc_phase(const StencilParams& sp, const Buffers& b, const Geo& g, const Ring& ring,
                                          int xcur, int rcur, float au, float be, uint32_t& par,
                                          double (&acc)[NSLOT]) {
@@ -634,6 +743,17 @@ __device__ FL_PHASE_INLINE void uc_phase(const StencilParams& sp, const Buffers&
     const float* R = pick(b.R, rcur);
     float* Xn = pick(b.X, xcur ^ 1);
     float* Pn = pick(b.P, xcur ^ 1);
+    if constexpr (DET) {
+        if (!g.live) {
+        } else if (g.border) {
+            UC<BW, PN, true, true> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
+            u.run(par);
+        } else {
+            UC<BW, PN, false, true> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
+            u.run(par);
+        }
+        return;
+    }
     if (!g.live) {
     } else if (g.border) {
         UC<BW, PN, true> u(sp, b, g, ring, X, P, R, Xn, Pn, au, be);
@@ -652,25 +772,19 @@ __device__ FL_PHASE_INLINE void uc_phase(const StencilParams& sp, const Buffers&
     acc[3] = a_mu;
 }
 
-// det mode: the CTA's exact per-warp accumulators (one instance per CTA in the kernels that use them)
-__device__ __forceinline__ FxCta<SWPB>& fx_shared() {
-    __shared__ FxCta<SWPB> fc;
-    return fc;
-}
-
-// det mode: this warp's work items it0, it0 + stride, ... (fixed global tiles); each tile's sums are
-// committed exactly, so neither the item -> warp assignment nor the band split changes the totals
+// det mode: this warp's work items it0, it0 + stride, ... (segments that are unions of the fixed global
+// tiles; normally one item per warp); each tile's sums are committed exactly inside the row loop, so
+// neither the segmentation, the item -> warp assignment nor the band split changes the totals
 template <int BW, int PN>
 __device__ __forceinline__ void vg_items(const StencilParams& sp, const Buffers& b, const Ring& ring, int it0,
                                          int stride, int xcur, int rcur, float alpha, uint32_t& par) {
     FxCta<SWPB>& fc = fx_shared();
     fx_zero(fc);
     __syncthreads();
-    for (int it = it0; it < sp.nitems; it += stride) {
-        const Geo g = geometry_item(sp, it);
+    for (int it = it0; uni(it < sp.nitems); it += stride) {
+        const Geo g = geometry_item(sp, __shfl_sync(0xffffffffu, it, 0));
         double acc[NSLOT];
-        vg_phase<BW, PN>(sp, b, g, ring, xcur, rcur, alpha, par, acc);
-        fx_commit(fc, acc);
+        vg_phase<BW, PN, true>(sp, b, g, ring, xcur, rcur, alpha, par, acc);   // commits per tile
     }
 }
 template <int BW, int PN>
@@ -679,11 +793,10 @@ __device__ __forceinline__ void uc_items(const StencilParams& sp, const Buffers&
     FxCta<SWPB>& fc = fx_shared();
     fx_zero(fc);
     __syncthreads();
-    for (int it = it0; it < sp.nitems; it += stride) {
-        const Geo g = geometry_item(sp, it);
+    for (int it = it0; uni(it < sp.nitems); it += stride) {
+        const Geo g = geometry_item(sp, __shfl_sync(0xffffffffu, it, 0));
         double acc[NSLOT];
-        uc_phase<BW, PN>(sp, b, g, ring, xcur, rcur, au, be, par, acc);
-        fx_commit(fc, acc);
+        uc_phase<BW, PN, true>(sp, b, g, ring, xcur, rcur, au, be, par, acc);   // commits per tile
     }
 }
 
@@ -938,7 +1051,9 @@ __device__ bool peer_sum_det(const StencilParams& sp, const PeerLoop& pl, int l,
     const int C = pl.ctas, h = pl.rank0 + l, world = pl.world;
     const bool sys = pl.g == 1;
     const size_t par = (size_t)(epoch & 1) * world * C * FXW;
-    const FxCta<SWPB>& fc = fx_shared();
+    FxCta<SWPB>& fc = fx_shared();
+    __syncthreads();
+    fx_cta_reduce(fc);
     __syncthreads();
     if (threadIdx.x == 0) {
         __int128 v[FXW];
@@ -1104,7 +1219,7 @@ cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers
     case BW_ * 10 + PN_: return launch_ring(K<BW_, PN_>, sp.nitems, sp, b, phase, s);
 
 template <typename K>
-cudaError_t launch_loop(K kernel, int nw, const StencilParams& sp, const Buffers& b, cudaStream_t s) {
+cudaError_t launch_loop(K kernel, int nw, const StencilParams& sp, const Buffers& b, cudaStream_t s, size_t smem) {
     static const void* done[64];
     static int ndone = 0;
     int dev = 0;
@@ -1113,14 +1228,14 @@ cudaError_t launch_loop(K kernel, int nw, const StencilParams& sp, const Buffers
     bool configured = false;
     for (int i = 0; i < ndone; ++i) configured = configured || done[i] == key;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         if (ndone < 64) done[ndone++] = key;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((nw + SWPB - 1) / SWPB);
     cfg.blockDim = dim3(SWPB * 32);
-    cfg.dynamicSmemBytes = RING_SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;   // every CTA co-resident: the grid barrier cannot deadlock
@@ -1156,8 +1271,8 @@ cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, cons
     switch (bw * 10 + pn) {
 #define FL_LCASE(BW_, PN_) \
     case BW_ * 10 + PN_:   \
-        return sp.det ? launch_loop(k_scg_loop<BW_, PN_, true>, sp.loop_warps, sp, b, s) \
-                      : launch_loop(k_scg_loop<BW_, PN_, false>, sp.loop_warps, sp, b, s);
+        return sp.det ? launch_loop(k_scg_loop<BW_, PN_, true>, sp.loop_warps, sp, b, s, RING_SMEM + FX_SMEM) \
+                      : launch_loop(k_scg_loop<BW_, PN_, false>, sp.loop_warps, sp, b, s, RING_SMEM);
         FL_LCASE(1, 1) FL_LCASE(1, 2) FL_LCASE(2, 1) FL_LCASE(2, 2) FL_LCASE(3, 1) FL_LCASE(3, 2)
 #undef FL_LCASE
         default: return cudaErrorInvalidValue;
@@ -1165,13 +1280,13 @@ cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, cons
 }
 
 template <typename K, typename... A>
-cudaError_t launch_coop(K kernel, int grid, cudaStream_t s, A... args) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
+cudaError_t launch_coop(K kernel, size_t smem, int grid, cudaStream_t s, A... args) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(SWPB * 32);
-    cfg.dynamicSmemBytes = RING_SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;   // co-residency: the barriers cannot deadlock
@@ -1187,10 +1302,11 @@ cudaError_t launch_scg_peer_loop(int bw, int pn, const StencilParams& sp, const 
 #define FL_PCASE(BW_, PN_) \
     case BW_ * 10 + PN_:   \
         if (sp.det)        \
-            return pl.g == 1 ? launch_coop(k_scg_peer_loop<BW_, PN_, true>, pl.ctas, s, sp, b, pl) \
-                             : launch_coop(k_scg_peer_loop_multi<BW_, PN_, true>, pl.g * pl.ctas, s, pl, *pb); \
-        return pl.g == 1 ? launch_coop(k_scg_peer_loop<BW_, PN_, false>, pl.ctas, s, sp, b, pl) \
-                         : launch_coop(k_scg_peer_loop_multi<BW_, PN_, false>, pl.g * pl.ctas, s, pl, *pb);
+            return pl.g == 1 ? launch_coop(k_scg_peer_loop<BW_, PN_, true>, RING_SMEM + FX_SMEM, pl.ctas, s, sp, b, pl) \
+                             : launch_coop(k_scg_peer_loop_multi<BW_, PN_, true>, RING_SMEM + FX_SMEM, pl.g * pl.ctas, \
+                                           s, pl, *pb);                                                              \
+        return pl.g == 1 ? launch_coop(k_scg_peer_loop<BW_, PN_, false>, RING_SMEM, pl.ctas, s, sp, b, pl) \
+                         : launch_coop(k_scg_peer_loop_multi<BW_, PN_, false>, RING_SMEM, pl.g * pl.ctas, s, pl, *pb);
         FL_PCASE(1, 1) FL_PCASE(1, 2) FL_PCASE(2, 1) FL_PCASE(2, 2) FL_PCASE(3, 1) FL_PCASE(3, 2)
 #undef FL_PCASE
         default: return cudaErrorInvalidValue;

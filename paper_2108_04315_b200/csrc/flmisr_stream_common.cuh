@@ -207,7 +207,31 @@ __device__ __forceinline__ Geo geometry_item(const StencilParams& sp, int gw) {
     // strips) are seg_b rows, interior pieces seg_rows rows
     int strip = 0, seg = 0, nseg = 1;
     g.r_lo = g.r_hi = sp.row_lo;
-    if (g.live && gw < sp.n_int) {            // interior strip 1 .. ni: seg_b | seg_rows ... | seg_b
+    if (sp.det && g.live) {
+        // det mode: the same layout in units of the fixed tiles of T rows (from row_lo, a multiple of T; the
+        // band's last tile is short when it ends at an image height H % T != 0), so every segment is a
+        // union of whole tiles whatever its length
+        const int T = sp.det_rows, nt = (sp.row_hi - sp.row_lo + T - 1) / T;
+        const int m = sp.seg_rows / T, mb = sp.seg_b / T;
+        int tlo, thi;
+        if (gw < sp.n_int) {
+            strip = 1 + gw % sp.ni;
+            seg = gw / sp.ni;
+            nseg = sp.nseg_i;
+            if (seg == 0) { tlo = 0; thi = min(mb, nt); }
+            else if (seg == nseg - 1) { tlo = max(nt - mb, mb); thi = nt; }
+            else { tlo = mb + (seg - 1) * m; thi = min(tlo + m, nt - mb); }
+        } else {
+            const int e = gw - sp.n_int;
+            strip = (sp.ne == 1 || (e & 1) == 0) ? 0 : sp.nstrips - 1;
+            seg = e / sp.ne;
+            nseg = sp.nseg_b;
+            tlo = seg * mb;
+            thi = min(tlo + mb, nt);
+        }
+        g.r_lo = min(sp.row_lo + tlo * T, sp.row_hi);
+        g.r_hi = min(sp.row_lo + thi * T, sp.row_hi);
+    } else if (g.live && gw < sp.n_int) {     // interior strip 1 .. ni: seg_b | seg_rows ... | seg_b
         strip = 1 + gw % sp.ni;
         seg = gw / sp.ni;
         nseg = sp.nseg_i;
@@ -272,16 +296,34 @@ __device__ __forceinline__ Geo geometry(const StencilParams& sp, int cta) {
 // arithmetic) give the same total whether they are summed per CTA, per band or over all bands.  The
 // conversion of a tile value truncates below 2^-64 (deterministic); |value| < 2^63 (the sums here are
 // <= ~1e12); a non-finite tile value is counted instead (the total becomes NaN -> FLMISR_ERR_NUMERIC).
+// m 2^(sh - 64) as a two's-complement 128-bit integer (truncated below 2^-64), without branches: the
+// lanes of a warp convert different exponents, and a data-dependent branch here would diverge
+// (mbits: the mantissa width; sh is clamped so that |value| < 2^62 -- saturation, never reached by the
+// sums here, which stay below ~1e12)
+template <int MBITS>
+__device__ __forceinline__ __int128 fx_shift(unsigned long long m, int sh, bool neg) {
+    sh = max(min(sh, 126 - MBITS), -127);
+    const int r = -sh;                                        // right shift for sh < 0
+    const unsigned long long lo_pos = sh < 64 ? m << (sh & 63) : 0ull;
+    const unsigned long long hi_pos = sh == 0 ? 0ull : (sh < 64 ? m >> ((64 - sh) & 63) : m << ((sh - 64) & 63));
+    const unsigned long long lo_neg = r < 64 ? m >> (r & 63) : 0ull;
+    unsigned long long lo = sh >= 0 ? lo_pos : lo_neg, hi = sh >= 0 ? hi_pos : 0ull;
+    const unsigned long long nlo = ~lo + 1ull, nhi = ~hi + (lo == 0ull ? 1ull : 0ull);
+    lo = neg ? nlo : lo;
+    hi = neg ? nhi : hi;
+    return (__int128)(((unsigned __int128)hi << 64) | lo);
+}
 __device__ __forceinline__ __int128 fx_of(double v) {
     const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
     const int ex = (int)((bits >> 52) & 0x7ff);
-    if (ex == 0) return 0;   // zero / subnormal: below the grid
-    const unsigned long long m = (bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
-    const int sh = ex - 1075 + 64;   // v = m 2^(ex - 1075) = (m << sh) 2^-64
-    unsigned __int128 a;
-    if (sh >= 0) a = sh < 74 ? (unsigned __int128)m << sh : ((unsigned __int128)1 << 126);   // saturate
-    else a = sh > -53 ? (unsigned __int128)(m >> (-sh)) : 0;
-    return (bits >> 63) ? -(__int128)a : (__int128)a;
+    const unsigned long long m = ex ? ((bits & 0xFFFFFFFFFFFFFull) | (1ull << 52)) : 0ull;   // zero / subnormal: 0
+    return fx_shift<53>(m, ex - 1075 + 64, (bits >> 63) != 0);   // v = m 2^(ex - 1075)
+}
+__device__ __forceinline__ __int128 fx_of(float v) {
+    const unsigned bits = __float_as_uint(v);
+    const int ex = (int)((bits >> 23) & 0xff);
+    const unsigned long long m = ex ? ((bits & 0x7fffffu) | 0x800000u) : 0ull;
+    return fx_shift<24>(m, ex - 150 + 64, (bits >> 31) != 0);     // v = m 2^(ex - 150)
 }
 __device__ __forceinline__ double fx_to_double(__int128 s) {
     const long long hi = (long long)(s >> 64);
@@ -304,35 +346,44 @@ __device__ __forceinline__ __int128 ld_relaxed_fx(const __int128* p) {
     return (__int128)(((unsigned __int128)hi << 64) | lo);
 }
 
-// per-warp exact accumulators of one phase (shared memory; lane 0 of each warp owns its row)
+// per-lane exact accumulators of one phase (dynamic shared memory after the ring, det kernels only):
+// every lane adds its own tile partials -- no cross-lane dependency at a tile boundary, so the warps of
+// an SM, which reach their tile boundaries together, do not stall on shuffle trees there; the lanes
+// are reduced once per phase (fx_cta_reduce)
 template <int WPB>
 struct FxCta {
-    __int128 s[WPB][FXW];
+    __int128 s[WPB][FXW][32];
+    __int128 red[WPB][FXW];
 };
-// every lane of a warp: this tile's per-lane fp64 partials -> fp64 warp tree (the same tile gives the same
-// bits in every launch configuration) -> exact add into the warp's accumulators
-template <int WPB>
-__device__ __forceinline__ void fx_commit(FxCta<WPB>& fc, const double (&acc)[NSLOT]) {
-    const int warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int k = 0; k < NSLOT; ++k) {
-        const double v = warp_sum(acc[k]);
-        if ((threadIdx.x & 31) == 0) {
-            if (isfinite(v)) fc.s[warp][k] += fx_of(v);
-            else fc.s[warp][NSLOT] += 1;
-        }
-    }
+constexpr size_t FX_SMEM = sizeof(FxCta<SWPB>);
+// every lane: this lane's tile partial of slot k, exactly (a non-finite value is counted instead)
+template <int WPB, typename V>
+__device__ __forceinline__ void fx_lane_add(FxCta<WPB>& fc, int k, V v) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool ok = isfinite(v);
+    fc.s[warp][k][lane] += ok ? fx_of(v) : (__int128)0;
+    if (!ok) fc.s[warp][NSLOT][lane] += 1;
 }
 // all threads: zero the accumulators (before a phase; a __syncthreads must separate it from any use)
 template <int WPB>
 __device__ __forceinline__ void fx_zero(FxCta<WPB>& fc) {
-    for (int i = threadIdx.x; i < WPB * FXW; i += blockDim.x) (&fc.s[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < WPB * FXW * 32; i += blockDim.x) (&fc.s[0][0][0])[i] = 0;
 }
-// threads k < FXW after a __syncthreads: this CTA's exact sum k (fixed order, exact anyway)
+// all threads, after a __syncthreads: each warp's lanes -> red[warp][k] (exact)
+template <int WPB>
+__device__ __forceinline__ void fx_cta_reduce(FxCta<WPB>& fc) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < FXW; ++k) {
+        const __int128 v = fx_warp_sum(fc.s[warp][k][lane]);
+        if (lane == 0) fc.red[warp][k] = v;
+    }
+}
+// after fx_cta_reduce and a __syncthreads: this CTA's exact sum k
 template <int WPB>
 __device__ __forceinline__ __int128 fx_cta(const FxCta<WPB>& fc, int k) {
     __int128 t = 0;
-    for (int w = 0; w < WPB; ++w) t += fc.s[w][k];
+    for (int w = 0; w < WPB; ++w) t += fc.red[w][k];
     return t;
 }
 // all threads: exact sum of n slots of FXW words at slot[i * FXW + k] -> tot (scaled and offset by the
@@ -477,10 +528,12 @@ __device__ void grid_sum(const double (&acc)[NSLOT], double* part, unsigned* gba
 
 // det mode: the grid barrier of grid_sum with exact fixed-point CTA slots (FXW words each)
 template <int WPB>
-__device__ void grid_sum_det(const FxCta<WPB>& fc, double* part, unsigned* gbar, unsigned epoch,
+__device__ void grid_sum_det(FxCta<WPB>& fc, double* part, unsigned* gbar, unsigned epoch,
                              double (&tot)[NSLOT]) {
     const int G = gridDim.x;
     __int128* slot = reinterpret_cast<__int128*>(part) + (size_t)(epoch & 1) * FXW * G;
+    __syncthreads();
+    fx_cta_reduce(fc);
     __syncthreads();
     if (threadIdx.x < FXW) slot[(size_t)blockIdx.x * FXW + threadIdx.x] = fx_cta(fc, threadIdx.x);
     __syncthreads();

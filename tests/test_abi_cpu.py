@@ -60,7 +60,8 @@ def cfg(**kw):
     (dict(x0_mode=2), "x0_mode"),
     (dict(x0_mode=1, shifts=synth.shift_pattern(2) + 0.1, world=2, rank=0, nccl_id=b"\0" * 128),
      "x0_mode = 1 with fractional HR shifts needs world == 1"),
-    (dict(det_rows=3), "det_rows"),
+    (dict(det_rows=4), "det_rows"),
+    (dict(det_rows=2), "det_rows"),
     (dict(det_rows=-1), "det_rows"),
     (dict(det_rows=5000), "det_rows"),
 ])
@@ -82,11 +83,11 @@ def test_band_too_small_names_minimum_height(fl):
 
 def test_det_band_too_small_names_tile_minimum(fl):
     """det mode: every band must hold at least one lcm(det_rows, mag) tile row block"""
-    c = cfg(lr_h=20, lr_w=16, world=4, rank=0, nccl_id=b"\0" * 128, det_rows=7)
+    c = cfg(lr_h=8, lr_w=16, world=4, rank=0, nccl_id=b"\0" * 128, det_rows=6)
     with pytest.raises(fl.FlmisrError) as ei:
         fl.Plan(**c)
     assert ei.value.status == fl.ERR_CONFIG
-    assert "minimum HR height 56" in str(ei.value)
+    assert "minimum HR height 24" in str(ei.value)
 
 
 def test_peer_entry_points_reject_bad_arguments_without_a_gpu(fl):
