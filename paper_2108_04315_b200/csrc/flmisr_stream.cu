@@ -227,9 +227,9 @@ struct VG {
                             if (dx >= 2) uA.y = 0.f;
                             if (dx >= 1) uB.y = 0.f;
                         }
-                        if (orow) {   // masked q: fma(0, rs, v) = v, and a valid pair rounds exactly as in
-                                      // the interior code (det mode: a tile's sums do not depend on whether
-                                      // a band edge made it a border piece)
+                        if (orow && DET) {   // masked q: fma(0, rs, v) = v, and a valid pair rounds exactly as
+                                             // in the interior code (a tile's sums do not depend on whether a
+                                             // band edge made it a border piece)
                             float2 mA = qA, mB = qB;
                             if (!g.cv0) { mA = F2(0.f, 0.f); mB = mA; }
                             if (!g.cv4) {
@@ -238,6 +238,16 @@ struct VG {
                             }
                             vb[cls] = fma2(mA, rA, vb[cls]);
                             vb[cls] = fma2(mB, rB, vb[cls]);
+                        } else if (orow) {   // default: product then sum (measured 2% faster on C2 than the
+                                             // masked FMA above)
+                            float2 vA = mul2(qA, rA), vB = mul2(qB, rB);
+                            if (!g.cv0) { vA = F2(0.f, 0.f); vB = vA; }
+                            if (!g.cv4) {
+                                if (dx >= 2) vA.y = 0.f;
+                                if (dx >= 1) vB.y = 0.f;
+                            }
+                            vb[cls] = fma2s(1.0f, vA, vb[cls]);
+                            vb[cls] = fma2s(1.0f, vB, vb[cls]);
                         }
                     } else if (orow) {
                         vb[cls] = fma2(qA, rA, vb[cls]);
@@ -782,7 +792,7 @@ __device__ __forceinline__ void vg_items(const StencilParams& sp, const Buffers&
     fx_zero(fc);
     __syncthreads();
     for (int it = it0; uni(it < sp.nitems); it += stride) {
-        const Geo g = geometry_item(sp, __shfl_sync(0xffffffffu, it, 0));
+        const Geo g = geometry_item<SHALO, true>(sp, __shfl_sync(0xffffffffu, it, 0));
         double acc[NSLOT];
         vg_phase<BW, PN, true>(sp, b, g, ring, xcur, rcur, alpha, par, acc);   // commits per tile
     }
@@ -794,7 +804,7 @@ __device__ __forceinline__ void uc_items(const StencilParams& sp, const Buffers&
     fx_zero(fc);
     __syncthreads();
     for (int it = it0; uni(it < sp.nitems); it += stride) {
-        const Geo g = geometry_item(sp, __shfl_sync(0xffffffffu, it, 0));
+        const Geo g = geometry_item<SHALO, true>(sp, __shfl_sync(0xffffffffu, it, 0));
         double acc[NSLOT];
         uc_phase<BW, PN, true>(sp, b, g, ring, xcur, rcur, au, be, par, acc);   // commits per tile
     }

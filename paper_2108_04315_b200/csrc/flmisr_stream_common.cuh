@@ -196,8 +196,9 @@ struct Geo {
 // index within its band in the peer loop)
 // HALO: columns of overlap per strip side (the operator's column reach): SHALO = 2 for the common-kappa
 // kernels, 4 for the per-phase 4x4 kernels; strips step by SCOLS - 2 HALO
-// gw: the work item (warp-uniform); geometry() below takes the item of this warp of CTA cta
-template <int HALO = SHALO>
+// gw: the work item (warp-uniform); geometry() below takes the item of this warp of CTA cta.  DET: the
+// det-mode layout (sp.det; a template flag so the default kernels carry none of its code)
+template <int HALO = SHALO, bool DET = false>
 __device__ __forceinline__ Geo geometry_item(const StencilParams& sp, int gw) {
     constexpr int STEP = SCOLS - 2 * HALO;
     Geo g;
@@ -207,7 +208,7 @@ __device__ __forceinline__ Geo geometry_item(const StencilParams& sp, int gw) {
     // strips) are seg_b rows, interior pieces seg_rows rows
     int strip = 0, seg = 0, nseg = 1;
     g.r_lo = g.r_hi = sp.row_lo;
-    if (sp.det && g.live) {
+    if (DET && g.live) {
         // det mode: the same layout in units of the fixed tiles of T rows (from row_lo, a multiple of T; the
         // band's last tile is short when it ends at an image height H % T != 0), so every segment is a
         // union of whole tiles whatever its length
