@@ -60,7 +60,7 @@ __device__ __noinline__ void fx_add_d(int k, double v) { fx_lane_add(fx_shared()
 //   w(t+1) = rho'(kappa x' - Y) -> horizontal adjoint pass hw(t+1), scattered into the pending rows
 //   t, t+1, t+2 of r = -grad J; BTV pairs of row t scattered into rows t..t+2; row t is complete.
 // ------------------------------------------------------------------------------------------------
-// DET (det mode): every accumulator is committed exactly (fx_commit1) when its row closes a fixed tile
+// DET (det mode): every accumulator is committed exactly (fx_add_f / fx_add_d) when its row closes a fixed tile
 // of T rows -- the data value of row t+1 (group A) and the BTV / <r,r> / <r,r_old> sums of row t
 // (group B) in step t.  T % 3 == 0 and segments start on a tile boundary, so every tile boundary inside
 // a segment falls on the same unrolled step of each group (A: step<0>, B: step<1>): one commit site per
