@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -56,14 +57,17 @@ struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
 };
 
-NcclApi& nccl() {
+static void nccl_load(NcclApi& api);
+NcclApi& nccl() {   // loaded once, thread-safe (plans may be created from several host threads)
     static NcclApi api;
-    static bool tried = false;
-    if (tried) return api;
-    tried = true;
+    static std::once_flag once;
+    std::call_once(once, [] { nccl_load(api); });
+    return api;
+}
+static void nccl_load(NcclApi& api) {
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return api;
+    if (!h) return;
     api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
     api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
@@ -75,7 +79,6 @@ NcclApi& nccl() {
     api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
     api.ok = api.CommInitRank && api.CommDestroy && api.AllGather && api.Send && api.Recv && api.GroupStart &&
              api.GroupEnd && api.GetErrorString;
-    return api;
 }
 
 #define NCCL_TRY(expr)                                                                              \
@@ -452,8 +455,9 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
             if (const char* ev = std::getenv("FLMISR_EDGE_RATIO")) ratio = std::max(1.0, std::atof(ev));
             sp.ne = sp.nstrips >= 2 ? 2 : 1;
             sp.ni = sp.nstrips - sp.ne;
-            // segment lengths: 1 mod 3 for the common-kappa kernels (row loop unrolled by 3), multiples of 4
-            // for the per-phase kernels (unrolled by 4; every segment starts on an even row)
+            // segment lengths: 1 mod 3 for the common-kappa kernels (row loop unrolled by 3; a partial last
+            // group -- any length -- measured 2-3% slower on C2/C3, profiles/r02_any_length_segments.txt),
+            // multiples of 4 for the per-phase kernels (unrolled by 4; every segment starts on an even row)
             auto to1mod3 = [pc](int v) {
                 v = std::max(v, 4);
                 return pc ? (v + 3) / 4 * 4 : v + ((1 - v % 3) + 3) % 3;

@@ -1198,18 +1198,8 @@ bool pdl_enabled() {
 template <typename K>
 cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers& b, int phase, cudaStream_t s) {
     // opt in to > 48 KB of dynamic shared memory once per kernel instantiation (per device)
-    static const void* done[64];
-    static int ndone = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(kernel) ^ (uintptr_t)dev);
-    bool configured = false;
-    for (int i = 0; i < ndone; ++i) configured = configured || done[i] == key;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
-        if (e != cudaSuccess) return e;
-        if (ndone < 64) done[ndone++] = key;
-    }
+    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), RING_SMEM);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((nw + SWPB - 1) / SWPB);
     cfg.blockDim = dim3(SWPB * 32);
@@ -1230,18 +1220,8 @@ cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers
 
 template <typename K>
 cudaError_t launch_loop(K kernel, int nw, const StencilParams& sp, const Buffers& b, cudaStream_t s, size_t smem) {
-    static const void* done[64];
-    static int ndone = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(kernel) ^ (uintptr_t)dev);
-    bool configured = false;
-    for (int i = 0; i < ndone; ++i) configured = configured || done[i] == key;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        if (ndone < 64) done[ndone++] = key;
-    }
+    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), smem);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((nw + SWPB - 1) / SWPB);
     cfg.blockDim = dim3(SWPB * 32);
@@ -1291,7 +1271,7 @@ cudaError_t launch_scg_loop_stream(int bw, int pn, const StencilParams& sp, cons
 
 template <typename K, typename... A>
 cudaError_t launch_coop(K kernel, size_t smem, int grid, cudaStream_t s, A... args) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

@@ -719,16 +719,7 @@ __global__ void k_pc_adjoint(StencilParams sp, PcTaps T, const float* __restrict
 
 template <typename K>
 cudaError_t set_smem(K kernel) {
-    static const void* done[64];
-    static int ndone = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const void* key = reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(kernel) ^ (uintptr_t)dev);
-    for (int i = 0; i < ndone; ++i)
-        if (done[i] == key) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING4_SMEM);
-    if (e == cudaSuccess && ndone < 64) done[ndone++] = key;
-    return e;
+    return ensure_dyn_smem(reinterpret_cast<const void*>(kernel), RING4_SMEM);
 }
 
 template <typename K, typename... A>
