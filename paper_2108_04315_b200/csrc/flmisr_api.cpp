@@ -579,7 +579,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     const size_t pad = (size_t)8 * p->pitch * sizeof(float);   // also covers the L2 prefetch distance
     e = cudaMalloc(&p->mem, p->hr_bytes * nhr + pad);
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc HR buffers: ") + cudaGetErrorString(e)));
-    cudaMemset(p->mem, 0, p->hr_bytes * nhr + pad);
+    cudaMemsetAsync(p->mem, 0, p->hr_bytes * nhr + pad, p->stream);
     const size_t fl = p->hr_bytes / sizeof(float);
     Buffers& b = p->b;
     b.Y = p->mem;
@@ -603,7 +603,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     const size_t nd = npart + NSLOT + ntrace + (size_t)NSLOT * world + 1;   // + the grid-barrier counter
     e = cudaMalloc(&p->dmem, nd * sizeof(double));
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc partials: ") + cudaGetErrorString(e)));
-    cudaMemset(p->dmem, 0, nd * sizeof(double));
+    cudaMemsetAsync(p->dmem, 0, nd * sizeof(double), p->stream);
     b.part = p->dmem;
     b.rank_sums = p->dmem + npart;
     b.trace = p->dmem + npart + NSLOT;
@@ -623,7 +623,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     }
     e = cudaMalloc(&p->st, sizeof(ScgState));
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc state: ") + cudaGetErrorString(e)));
-    cudaMemset(p->st, 0, sizeof(ScgState));
+    cudaMemsetAsync(p->st, 0, sizeof(ScgState), p->stream);
     b.st = p->st;
     e = cudaEventCreateWithFlags(&p->done_ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaEventCreate"));
@@ -699,7 +699,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc general-path buffers"));
         e = cudaMalloc(&p->gpart, (size_t)NSLOT * ngblk * sizeof(double));
         if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc general-path partials"));
-        cudaMemcpy(p->gmem, taps.data(), ntap * sizeof(float), cudaMemcpyHostToDevice);
+        cudaMemcpyAsync(p->gmem, taps.data(), ntap * sizeof(float), cudaMemcpyHostToDevice, p->stream);
         gp.taps = p->gmem;
         gp.lr = p->gmem + ntap;
         gp.w = p->gmem + ntap + nlr_px;
@@ -721,7 +721,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         // + 1 row: the bulk copies of a right-border strip read up to 512 B past a row's end
         e = cudaMalloc(&hm, 4 * hb + (size_t)p->pitch * sizeof(float));
         if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc halo buffers"));
-        cudaMemset(hm, 0, 4 * hb + (size_t)p->pitch * sizeof(float));
+        cudaMemsetAsync(hm, 0, 4 * hb + (size_t)p->pitch * sizeof(float), p->stream);
         p->halo_mem = hm;
         const size_t hf = hb / sizeof(float);
         if (rank > 0) { b.send_top = hm; p->recv_top = hm + 2 * hf; b.halo_top = p->recv_top; }
@@ -729,7 +729,7 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
         if (world > PMAX) return cleanup_fail(fail(FLMISR_ERR_CONFIG, "row bands: world <= 8"));
         e = cudaMalloc(&p->peer_mem, peer_mem_bytes(world));
         if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, "cudaMalloc peer mailbox"));
-        cudaMemset(p->peer_mem, 0, peer_mem_bytes(world));
+        cudaMemsetAsync(p->peer_mem, 0, peer_mem_bytes(world), p->stream);
         if (!virt) {
             NcclApi& api = nccl();
             if (!api.ok) return cleanup_fail(fail(FLMISR_ERR_NCCL, "libnccl.so.2 could not be loaded"));
@@ -740,7 +740,9 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
                 return cleanup_fail(fail(FLMISR_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)));
         }
     }
-    e = cudaDeviceSynchronize();
+    // the plan's own (non-blocking) stream, not a device-wide sync: another host thread may be capturing
+    // a graph on its plan's stream meanwhile
+    e = cudaStreamSynchronize(p->stream);
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("plan sync: ") + cudaGetErrorString(e)));
     *out = p;
     g_last_error.clear();

@@ -549,8 +549,8 @@ __global__ void __launch_bounds__(G3T, G3MINB_UC) k_gen3_uc(StencilParams sp, Ge
 template <typename K>
 cudaError_t g3_launch(K kernel, size_t smem, const StencilParams& sp, const GenParams& gp, const Buffers& b, int phase,
                       cudaStream_t s) {
-    // > 48 KB of dynamic shared memory needs the opt-in (idempotent)
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // > 48 KB of dynamic shared memory needs the opt-in (raised only, thread-safe)
+    cudaError_t e = raise_dyn_smem(reinterpret_cast<const void*>(kernel), smem);
     if (e != cudaSuccess) return e;
     kernel<<<gp.nblk3, G3T, smem, s>>>(sp, gp, b, phase);
     return cudaGetLastError();

@@ -6,9 +6,6 @@
 #pragma once
 #include <cstdint>
 #include <cstdlib>
-#include <mutex>
-#include <utility>
-#include <vector>
 #include <cuda_runtime.h>
 
 #include "flmisr_common.cuh"
@@ -19,18 +16,7 @@ namespace {
 
 // Host: opt a kernel in to smem bytes of dynamic shared memory once per (kernel, device).  Thread-safe:
 // plans may be created and launched from several host threads.
-inline cudaError_t ensure_dyn_smem(const void* kernel, size_t smem) {
-    static std::mutex mu;
-    static std::vector<std::pair<const void*, int>> done;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lock(mu);
-    for (const auto& d : done)
-        if (d.first == kernel && d.second == dev) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) done.emplace_back(kernel, dev);
-    return e;
-}
+inline cudaError_t ensure_dyn_smem(const void* kernel, size_t smem) { return raise_dyn_smem(kernel, smem); }
 
 // ---- packed fp32x2 helpers (PTX f32x2 -> SASS FFMA2 / FADD2 / FMUL2 on sm_100a) ----
 __device__ __forceinline__ float2 F2(float a, float b) { return make_float2(a, b); }
