@@ -80,10 +80,10 @@ typedef struct {
                             boundaries are multiples of lcm(T, mag), every warp segment is a union
                             of whole tiles, each tile's partial sums are committed separately and
                             every sum (tile -> lane -> CTA -> band -> all bands) is an exact 128-bit
-                            fixed-point sum (grid 2^-64), independent of order and grouping.  Needs
-                            the streaming path (fast_path 2) and, at world > 1, the peer transport
-                            (flmisr_peer_connect); else FLMISR_ERR_CONFIG.  ~1.45x the loop time on
-                            one GPU                                                  */
+                            fixed-point sum (grid 2^-64), independent of order and grouping, over
+                            both band transports (peer memory and NCCL).  Needs the streaming path
+                            (fast_path 2); else FLMISR_ERR_CONFIG.  ~1.45x the loop time on one GPU
+                                                                                      */
 } flmisr_config;
 
 typedef struct {

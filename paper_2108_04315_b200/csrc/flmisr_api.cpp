@@ -119,7 +119,7 @@ struct flmisr_plan_s {
     double* gpart = nullptr; // general path: first-pass partials
     size_t hr_bytes = 0;     // bytes of one stored HR buffer
     float* mem = nullptr;    // one allocation for all HR buffers
-    double* dmem = nullptr;  // partials + rank sums + trace + gathered
+    double* dmem = nullptr;  // partials + rank sums + trace + grid-barrier counter
     ScgState* st = nullptr;
     ScgState* st_host = nullptr;  // pinned
     double* trace_host = nullptr; // pinned
@@ -131,7 +131,6 @@ struct flmisr_plan_s {
     ncclComm_t comm = nullptr;
     float* recv_top = nullptr;
     float* recv_bot = nullptr;
-    double* gathered = nullptr;
     cudaEvent_t done_ev = nullptr;
     cudaStream_t last_stream = nullptr;
     int pending = 0;
@@ -597,17 +596,17 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     const size_t ntiles = std::max<size_t>(std::max<size_t>((size_t)sp.tiles_x * sp.tiles_y, nsblk), ngblk);
     // x2: the persistent loop kernel double-buffers its per-CTA slots by phase parity
     // det mode: FXW 128-bit words (2 doubles each) per CTA slot
-    const size_t npart = std::max<size_t>(std::max<size_t>(2 * NSLOT * ntiles, (size_t)NSLOT * world),
+    // (and the allgathered rank-sum records: RSW doubles per rank)
+    const size_t npart = std::max<size_t>(std::max<size_t>(2 * NSLOT * ntiles, (size_t)RSW * world),
                                           (size_t)2 * 2 * FXW * nsblk);
     const size_t ntrace = (size_t)(c.n_iter + 1) * 6;
-    const size_t nd = npart + NSLOT + ntrace + (size_t)NSLOT * world + 1;   // + the grid-barrier counter
+    const size_t nd = npart + RSW + ntrace + 1;   // + the grid-barrier counter
     e = cudaMalloc(&p->dmem, nd * sizeof(double));
     if (e != cudaSuccess) return cleanup_fail(fail(FLMISR_ERR_CUDA, std::string("cudaMalloc partials: ") + cudaGetErrorString(e)));
     cudaMemsetAsync(p->dmem, 0, nd * sizeof(double), p->stream);
     b.part = p->dmem;
-    b.rank_sums = p->dmem + npart;
-    b.trace = p->dmem + npart + NSLOT;
-    p->gathered = p->dmem + npart + NSLOT + ntrace;
+    b.rank_sums = p->dmem + npart;   // RSW doubles: 16-byte aligned (npart is even)
+    b.trace = p->dmem + npart + RSW;
     b.gbar = reinterpret_cast<unsigned*>(p->dmem + nd - 1);
     b.mem_lo = p->mem;
     b.mem_hi = p->mem + (p->hr_bytes * nhr + pad) / sizeof(float);
@@ -897,7 +896,7 @@ flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
         const int rank = p->cfg.rank, world = p->cfg.world;
         const size_t hcount = (size_t)p->eta * p->pitch;
         NCCL_TRY(api.GroupStart());
-        NCCL_TRY(api.AllGather(p->b.rank_sums, p->b.part, NSLOT, ncclFloat64, p->comm, s));
+        NCCL_TRY(api.AllGather(p->b.rank_sums, p->b.part, p->sp.det ? RSW : NSLOT, ncclFloat64, p->comm, s));
         if (rank > 0) {
             NCCL_TRY(api.Send(p->b.send_top, hcount, ncclFloat32, rank - 1, p->comm, s));
             NCCL_TRY(api.Recv(p->recv_top, hcount, ncclFloat32, rank - 1, p->comm, s));
@@ -907,7 +906,7 @@ flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
             NCCL_TRY(api.Recv(p->recv_bot, hcount, ncclFloat32, rank + 1, p->comm, s));
         }
         NCCL_TRY(api.GroupEnd());
-        CUDA_TRY(launch_scalar_after_value(p->b, world, phase, s));
+        CUDA_TRY(launch_scalar_after_value(p->sp, p->b, world, phase, s));
     }
     return FLMISR_OK;
 }
@@ -915,8 +914,8 @@ flmisr_status enqueue_value_grad(flmisr_plan_s* p, int phase, cudaStream_t s) {
 flmisr_status enqueue_update_curv(flmisr_plan_s* p, int phase, cudaStream_t s) {
     CUDA_TRY(launch_uc(p, phase, s));
     if (p->cfg.world > 1 && !p->virt) {
-        NCCL_TRY(nccl().AllGather(p->b.rank_sums, p->b.part, NSLOT, ncclFloat64, p->comm, s));
-        CUDA_TRY(launch_scalar_after_curv(p->b, p->cfg.world, s));
+        NCCL_TRY(nccl().AllGather(p->b.rank_sums, p->b.part, p->sp.det ? RSW : NSLOT, ncclFloat64, p->comm, s));
+        CUDA_TRY(launch_scalar_after_curv(p->sp, p->b, p->cfg.world, s));
     }
     return FLMISR_OK;
 }
@@ -996,8 +995,8 @@ flmisr_status flmisr_reconstruct_async(flmisr_plan_t p, const float* lr_stack, c
             return fail(FLMISR_ERR_CUDA, std::string("persistent SCG loop launch: ") + cudaGetErrorString(le));
         }
     }
-    if (!looped && p->sp.det)   // the per-phase kernels (NCCL transport) sum in fp64, not exactly
-        return fail(FLMISR_ERR_CONFIG, "det_rows at world > 1 needs the peer transport (flmisr_peer_connect)");
+    if (!looped && p->sp.det && p->cfg.world == 1)   // det mode at world 1 is the persistent loop kernel
+        return fail(FLMISR_ERR_CONFIG, "det_rows needs the persistent loop kernel (cooperative launch)");
     // world > 1 over NCCL: the per-phase kernels, the halo send/recv, the consensus allgather and the
     // scalar kernels are captured into the same graph (NCCL operations are graph-capturable; SURVEY
     // 8(e)); every rank captures the same operation sequence, so graph and eager ranks still match.
@@ -1155,17 +1154,18 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
         if (!q || !q->virt || q->cfg.world != g || q->cfg.rank != h || q->H != plans[0]->H || q->W != plans[0]->W ||
             q->cfg.n_iter != plans[0]->cfg.n_iter || q->cfg.device != plans[0]->cfg.device)
             return fail(FLMISR_ERR_SHAPE, "plans must be flmisr_plan_virtual bands 0..g-1 of one configuration");
-        if (q->cfg.det_rows)
-            return fail(FLMISR_ERR_CONFIG, "det_rows bands run on the peer protocol: use flmisr_reconstruct_virtual_peer");
+        if (q->cfg.det_rows != plans[0]->cfg.det_rows)
+            return fail(FLMISR_ERR_SHAPE, "plans must be flmisr_plan_virtual bands 0..g-1 of one configuration");
     }
     CUDA_TRY(cudaSetDevice(plans[0]->cfg.device));
     cudaStream_t s = plans[0]->stream;
     const size_t hb = (size_t)plans[0]->eta * plans[0]->pitch * sizeof(float);
+    const size_t rec = plans[0]->sp.det ? RSW : NSLOT;   // doubles per rank-sum record
     auto gather = [&]() -> flmisr_status {
         for (int h = 0; h < g; ++h)
             for (int r = 0; r < g; ++r)
-                CUDA_TRY(cudaMemcpyAsync(plans[h]->b.part + (size_t)r * NSLOT, plans[r]->b.rank_sums,
-                                         NSLOT * sizeof(double), cudaMemcpyDeviceToDevice, s));
+                CUDA_TRY(cudaMemcpyAsync(plans[h]->b.part + (size_t)r * rec, plans[r]->b.rank_sums,
+                                         rec * sizeof(double), cudaMemcpyDeviceToDevice, s));
         return FLMISR_OK;
     };
     auto exchange = [&]() -> flmisr_status {
@@ -1185,7 +1185,7 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
         for (int h = 0; h < g; ++h)
             if ((r = enqueue_value_grad(plans[h], phase, s)) != FLMISR_OK) return r;
         if ((r = gather()) != FLMISR_OK || (r = exchange()) != FLMISR_OK) return r;
-        for (int h = 0; h < g; ++h) CUDA_TRY(launch_scalar_after_value(plans[h]->b, g, phase, s));
+        for (int h = 0; h < g; ++h) CUDA_TRY(launch_scalar_after_value(plans[h]->sp, plans[h]->b, g, phase, s));
         return FLMISR_OK;
     };
     auto update_curv = [&]() -> flmisr_status {
@@ -1193,7 +1193,7 @@ flmisr_status flmisr_reconstruct_virtual(flmisr_plan_t* plans, int32_t g, const 
         for (int h = 0; h < g; ++h)
             if ((r = enqueue_update_curv(plans[h], PH_ITER, s)) != FLMISR_OK) return r;
         if ((r = gather()) != FLMISR_OK) return r;
-        for (int h = 0; h < g; ++h) CUDA_TRY(launch_scalar_after_curv(plans[h]->b, g, s));
+        for (int h = 0; h < g; ++h) CUDA_TRY(launch_scalar_after_curv(plans[h]->sp, plans[h]->b, g, s));
         return FLMISR_OK;
     };
     auto body = [&]() -> flmisr_status {

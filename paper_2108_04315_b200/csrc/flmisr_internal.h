@@ -74,6 +74,7 @@ struct StencilParams {
 };
 // det mode: 128-bit words per CTA partial (NSLOT exact sums + the count of non-finite tile values)
 constexpr int FXW = NSLOT + 1;
+constexpr int RSW = 2 * FXW;   // doubles per rank-sum record (det mode: FXW 128-bit words; else NSLOT fp64)
 
 // Streaming kernels (flmisr_stream.cu): strips of SCOLS columns per warp, stepping by SSTEP.
 #ifndef FLMISR_SWPB
@@ -164,8 +165,9 @@ cudaError_t launch_pc_uc(int bw, int pn, const StencilParams& sp, const Buffers&
 cudaError_t launch_pc_loop(int bw, int pn, const StencilParams& sp, const Buffers& b, const PcTaps& T, cudaStream_t s);
 cudaError_t launch_pc_forward_debug(const StencilParams& sp, const PcTaps& T, const float* x, float* z, cudaStream_t s);
 cudaError_t launch_pc_adjoint_debug(const StencilParams& sp, const PcTaps& T, const float* w, float* g, cudaStream_t s);
-cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s);  // world > 1
-cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s);   // world > 1
+cudaError_t launch_scalar_after_value(const StencilParams& sp, const Buffers& b, int world, int phase,
+                                      cudaStream_t s);   // world > 1
+cudaError_t launch_scalar_after_curv(const StencilParams& sp, const Buffers& b, int world, cudaStream_t s);   // world > 1
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,
                               int rules, cudaStream_t s);
 

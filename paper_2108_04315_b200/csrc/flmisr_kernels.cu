@@ -301,22 +301,41 @@ __global__ void __launch_bounds__(NTHREADS) k_update_curv(StencilParams sp, Buff
 // Multi-GPU scalar kernels: the rank sums were allgathered into b.part[0 .. world*NSLOT); sum them
 // in rank order (identical on every rank) and run the scalar logic (Alg. 1 "Central" lines).
 // ------------------------------------------------------------------------------------------------
-__global__ void k_scalar_after_value(Buffers b, int world, int phase) {
+// rank sums -> consensus sums.  Default: fp64 records of NSLOT (band affine applied), summed in rank
+// order.  det mode (sp.det): records of FXW exact 128-bit words, summed exactly, converted once, with
+// the whole image's affine correction -- the same bits at every band count.
+__device__ void rank_totals(const StencilParams& sp, const Buffers& b, int world, int which, double (&t)[NSLOT]) {
+    if (!sp.det) {
+        for (int k = 0; k < NSLOT; ++k) t[k] = 0.0;
+        for (int r = 0; r < world; ++r)
+            for (int k = 0; k < NSLOT; ++k) t[k] += b.part[r * NSLOT + k];
+        return;
+    }
+    const __int128* w = reinterpret_cast<const __int128*>(b.part);
+    __int128 s[FXW];
+    for (int k = 0; k < FXW; ++k) s[k] = 0;
+    for (int r = 0; r < world; ++r)
+        for (int k = 0; k < FXW; ++k) s[k] += w[r * FXW + k];
+    const double* aff = which == 0 ? sp.aff_vg : sp.aff_uc;
+    const double* off = which == 0 ? sp.det_off_vg : sp.det_off_uc;
+    for (int k = 0; k < NSLOT; ++k)
+        t[k] = s[NSLOT] != 0 ? __longlong_as_double(0x7ff8000000000000ll) : fx_to_double(s[k]) * aff[k] + off[k];
+}
+
+__global__ void k_scalar_after_value(const __grid_constant__ StencilParams sp, Buffers b, int world, int phase) {
     ScgState* s = b.st;
     if (s->done) return;
-    double t[NSLOT] = {0, 0, 0, 0};
-    for (int r = 0; r < world; ++r)
-        for (int k = 0; k < NSLOT; ++k) t[k] += b.part[r * NSLOT + k];
+    double t[NSLOT];
+    rank_totals(sp, b, world, 0, t);
     scg_after_value(s, t, b.trace, phase);
 }
 
-__global__ void k_scalar_after_curv(Buffers b, int world) {
+__global__ void k_scalar_after_curv(const __grid_constant__ StencilParams sp, Buffers b, int world) {
     ScgState* s = b.st;
     if (s->done) return;
     if (!s->success) { scg_pre_value(s); return; }
-    double t[NSLOT] = {0, 0, 0, 0};
-    for (int r = 0; r < world; ++r)
-        for (int k = 0; k < NSLOT; ++k) t[k] += b.part[r * NSLOT + k];
+    double t[NSLOT];
+    rank_totals(sp, b, world, 1, t);
     scg_after_curv(s, t);
 }
 
@@ -474,12 +493,12 @@ cudaError_t launch_update_curv(int kr, int bw, int pn, const StencilParams& sp, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_scalar_after_value(const Buffers& b, int world, int phase, cudaStream_t s) {
-    k_scalar_after_value<<<1, 1, 0, s>>>(b, world, phase);
+cudaError_t launch_scalar_after_value(const StencilParams& sp, const Buffers& b, int world, int phase, cudaStream_t s) {
+    k_scalar_after_value<<<1, 1, 0, s>>>(sp, b, world, phase);
     return cudaGetLastError();
 }
-cudaError_t launch_scalar_after_curv(const Buffers& b, int world, cudaStream_t s) {
-    k_scalar_after_curv<<<1, 1, 0, s>>>(b, world);
+cudaError_t launch_scalar_after_curv(const StencilParams& sp, const Buffers& b, int world, cudaStream_t s) {
+    k_scalar_after_curv<<<1, 1, 0, s>>>(sp, b, world);
     return cudaGetLastError();
 }
 

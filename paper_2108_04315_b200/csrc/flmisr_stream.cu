@@ -484,7 +484,56 @@ __device__ FL_PHASE_INLINE void vg_phase(const StencilParams& sp, const Buffers&
     acc[3] = a_rro;
 }
 
-template <int BW, int PN>
+// det mode, per-phase kernels (world > 1 over NCCL or device copies; one item per warp): the CTA's exact
+// partial goes to its slot, the last CTA sums the slots exactly and publishes the band's FXW words as
+// the rank-sum record (rank_sums); the scalar kernel after the allgather sums the bands exactly
+__device__ bool reduce_partials_det(FxCta<SWPB>& fc, double* part, int ntiles, int tile, unsigned* counter,
+                                    __int128 (&tot)[FXW]) {
+    __shared__ int s_last;
+    __syncthreads();
+    fx_cta_reduce(fc);
+    __syncthreads();
+    __int128* slot = reinterpret_cast<__int128*>(part);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < FXW; ++k) slot[(size_t)tile * FXW + k] = fx_cta(fc, k);
+        unsigned prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
+        s_last = prev == (unsigned)(ntiles - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    fx_sum_raw(slot, ntiles, tot);
+    if (threadIdx.x == 0) *counter = 0u;
+    return true;
+}
+template <int WHICH>
+__device__ void finish_det(const StencilParams& sp, const Buffers& b, const __int128 (&tw)[FXW], int phase) {
+    if (threadIdx.x != 0) return;
+    if (sp.world > 1 && phase != PH_DEBUG) {   // the band's exact record for the allgather
+        __int128* rs = reinterpret_cast<__int128*>(b.rank_sums);
+#pragma unroll
+        for (int k = 0; k < FXW; ++k) rs[k] = tw[k];
+        return;
+    }
+    double tot[NSLOT];
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k)
+        tot[k] = tw[NSLOT] != 0 ? __longlong_as_double(0x7ff8000000000000ll) : fx_to_double(tw[k]);
+    affine_det<WHICH>(sp, tot);
+    ScgState* s = b.st;
+    if (phase == PH_DEBUG) {
+#pragma unroll
+        for (int k = 0; k < NSLOT; ++k) s->dbg[k] = tot[k];
+        return;
+    }
+    ScgState l = *s;
+    if (WHICH == 0) scg_after_value(&l, tot, b.trace, phase);
+    else scg_after_curv(&l, tot);
+    *s = l;
+}
+
+template <int BW, int PN, bool DET = false>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ ScgState S;
@@ -511,11 +560,21 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_vg_stream(StencilParams sp
     xcur = __shfl_sync(0xffffffffu, xcur, 0);
     rcur = __shfl_sync(0xffffffffu, rcur, 0);
     alpha = phase == PH_ITER ? __shfl_sync(0xffffffffu, alpha, 0) : 0.0f;
-    const Geo g = geometry(sp, blockIdx.x);
+    const int wslot = blockIdx.x * SWPB + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const Geo g = DET ? geometry_item<SHALO, true>(sp, wslot) : geometry(sp, blockIdx.x);
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
     uint32_t par = 0;
+    if constexpr (DET) {   // world > 1 (det mode at world 1 runs the persistent loop kernel)
+        FxCta<SWPB>& fc = fx_shared();
+        fx_zero(fc);
+        __syncthreads();
+        vg_phase<BW, PN, true>(sp, b, g, ring, xcur, rcur, alpha, par, acc);   // commits per tile
+        __int128 tw[FXW];
+        if (reduce_partials_det(fc, b.part, gridDim.x, blockIdx.x, &st->counter, tw)) finish_det<0>(sp, b, tw, phase);
+        return;
+    }
     vg_phase<BW, PN>(sp, b, g, ring, xcur, rcur, alpha, par, acc);
     if (deferred) {
         publish(acc, b.part, seq);
@@ -810,7 +869,7 @@ __device__ __forceinline__ void uc_items(const StencilParams& sp, const Buffers&
     }
 }
 
-template <int BW, int PN>
+template <int BW, int PN, bool DET = false>
 __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp, Buffers b, int phase) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ ScgState S;
@@ -843,11 +902,24 @@ __global__ void __launch_bounds__(SWPB * 32, SMINB) k_uc_stream(StencilParams sp
     rcur = __shfl_sync(0xffffffffu, rcur, 0);
     au = __shfl_sync(0xffffffffu, au, 0);
     be = __shfl_sync(0xffffffffu, be, 0);
-    const Geo g = geometry(sp, blockIdx.x);
+    const int wslot = blockIdx.x * SWPB + __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const Geo g = DET ? geometry_item<SHALO, true>(sp, wslot) : geometry(sp, blockIdx.x);
     Ring ring;
     ring.init(smem, __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), g.lane);
     double acc[NSLOT];
     uint32_t par = 0;
+    if constexpr (DET) {
+        FxCta<SWPB>& fc = fx_shared();
+        fx_zero(fc);
+        __syncthreads();
+        uc_phase<BW, PN, true>(sp, b, g, ring, xcur, rcur, au, be, par, acc);   // commits per tile
+        __int128 tw[FXW];
+        if (reduce_partials_det(fc, b.part, gridDim.x, blockIdx.x, &st->counter, tw)) {
+            if (threadIdx.x == 0 && phase != PH_DEBUG) st->xcur = xcur ^ 1;
+            finish_det<1>(sp, b, tw, phase);
+        }
+        return;
+    }
     uc_phase<BW, PN>(sp, b, g, ring, xcur, rcur, au, be, par, acc);
     if (deferred) {
         publish(acc, b.part, seq);
@@ -1196,14 +1268,15 @@ bool pdl_enabled() {
 }
 
 template <typename K>
-cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers& b, int phase, cudaStream_t s) {
+cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers& b, int phase, cudaStream_t s,
+                        size_t smem = RING_SMEM) {
     // opt in to > 48 KB of dynamic shared memory once per kernel instantiation (per device)
-    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), RING_SMEM);
+    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kernel), smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((nw + SWPB - 1) / SWPB);
     cfg.blockDim = dim3(SWPB * 32);
-    cfg.dynamicSmemBytes = RING_SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1215,8 +1288,10 @@ cudaError_t launch_ring(K kernel, int nw, const StencilParams& sp, const Buffers
 
 }  // namespace
 
-#define FL_SCASE(K, BW_, PN_) \
-    case BW_ * 10 + PN_: return launch_ring(K<BW_, PN_>, sp.nitems, sp, b, phase, s);
+#define FL_SCASE(K, BW_, PN_)                                                                                 \
+    case BW_ * 10 + PN_:                                                                                      \
+        return sp.det ? launch_ring(K<BW_, PN_, true>, sp.nitems, sp, b, phase, s, RING_SMEM + FX_SMEM) \
+                      : launch_ring(K<BW_, PN_, false>, sp.nitems, sp, b, phase, s);
 
 template <typename K>
 cudaError_t launch_loop(K kernel, int nw, const StencilParams& sp, const Buffers& b, cudaStream_t s, size_t smem) {

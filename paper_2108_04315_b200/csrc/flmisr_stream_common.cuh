@@ -330,11 +330,6 @@ __device__ __forceinline__ __int128 fx_of(float v) {
     const unsigned long long m = ex ? ((bits & 0x7fffffu) | 0x800000u) : 0ull;
     return fx_shift<24>(m, ex - 150 + 64, (bits >> 31) != 0);     // v = m 2^(ex - 150)
 }
-__device__ __forceinline__ double fx_to_double(__int128 s) {
-    const long long hi = (long long)(s >> 64);
-    const unsigned long long lo = (unsigned long long)s;
-    return (double)hi + (double)lo * 5.421010862427522e-20;   // 2^-64
-}
 __device__ __forceinline__ __int128 fx_shfl_xor(__int128 v, int o) {
     const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(v >> 64), o);
     const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)v, o);
@@ -391,9 +386,8 @@ __device__ __forceinline__ __int128 fx_cta(const FxCta<WPB>& fc, int k) {
     for (int w = 0; w < WPB; ++w) t += fc.red[w][k];
     return t;
 }
-// all threads: exact sum of n slots of FXW words at slot[i * FXW + k] -> tot (scaled and offset by the
-// caller); the count of non-finite tile values makes every total NaN
-__device__ __forceinline__ void fx_sum_slots(const __int128* slot, int n, double (&tot)[NSLOT]) {
+// all threads: exact sum of n slots of FXW words at slot[i * FXW + k] -> t (128-bit totals)
+__device__ __forceinline__ void fx_sum_raw(const __int128* slot, int n, __int128 (&t)[FXW]) {
     __shared__ __int128 sred[32][FXW];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     __int128 loc[FXW];
@@ -408,13 +402,18 @@ __device__ __forceinline__ void fx_sum_slots(const __int128* slot, int n, double
         if (lane == 0) sred[warp][k] = v;
     }
     __syncthreads();
-    __int128 t[FXW];
 #pragma unroll
     for (int k = 0; k < FXW; ++k) {
         t[k] = 0;
         for (int w = 0; w < nw; ++w) t[k] += sred[w][k];
     }
     __syncthreads();   // sred is reused by the next call
+}
+// ... converted (scaled and offset by the caller); the count of non-finite tile values makes every
+// total NaN
+__device__ __forceinline__ void fx_sum_slots(const __int128* slot, int n, double (&tot)[NSLOT]) {
+    __int128 t[FXW];
+    fx_sum_raw(slot, n, t);
     const bool bad = t[NSLOT] != 0;
 #pragma unroll
     for (int k = 0; k < NSLOT; ++k) tot[k] = bad ? __longlong_as_double(0x7ff8000000000000ll) : fx_to_double(t[k]);

@@ -1,8 +1,9 @@
 """det mode (flmisr_config.det_rows): results bit-identical for every band count g (SURVEY 8(e)
 "bit-stable"; P:404 -- the consensus run equals the centralised run).
 
-The g = 1 persistent loop kernel and the g-band peer protocol (all bands in one cooperative launch on
-one device, the multi-GPU kernel with local pointers) cut their bands into different warp segments (one
+The g = 1 persistent loop kernel, the g-band peer protocol (all bands in one cooperative launch on one
+device, the multi-GPU kernel with local pointers) and the per-phase band kernels of the NCCL transport
+(device copies in place of the allgather and the halo send/recv) cut their bands into different warp segments (one
 wave each: a band of 1/g of the image on 1/g of the SMs), but every segment is a union of the same
 fixed global tiles of T HR rows, each tile's sums are committed separately inside the row loop and
 all sums are exact (128-bit fixed point), so the final image, the f trace and the accept sequence
@@ -28,7 +29,7 @@ def _stack(lr_h, lr_w, mag, seed):
     return sh, synth.detector_stack(truth, mag, sh, 1 / 255, seed=seed).astype(np.float32)
 
 
-def _run(g, lr_h, lr_w, mag, sh, yd, n_iter, T, **kw):
+def _run(g, lr_h, lr_w, mag, sh, yd, n_iter, T, transport="peer", **kw):
     common = dict(k=len(sh), lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=synth.gaussian_psf(), mag=mag, n_iter=n_iter,
                   det_rows=T, **kw)
     if g == 1:
@@ -41,7 +42,10 @@ def _run(g, lr_h, lr_w, mag, sh, yd, n_iter, T, **kw):
     tile = T * mag // np.gcd(T, mag)
     for p in pls[:-1]:   # bands are unions of the fixed tiles
         assert p.row_lo % tile == 0 and p.row_hi % tile == 0
-    h, rep = flmisr.reconstruct_virtual_peer(pls, yd)
+    # "peer": the peer-memory band loop (persistent kernels, mailboxes); "copies": the per-phase band
+    # kernels with device copies in place of the NCCL allgather and halo send/recv
+    run = flmisr.reconstruct_virtual_peer if transport == "peer" else flmisr.reconstruct_virtual
+    h, rep = run(pls, yd)
     for p in pls:
         p.destroy()
     return h.cpu().numpy(), rep
@@ -67,10 +71,11 @@ def test_bit_identical_across_band_counts(name):
     ref, rref = _run(1, lr_h, lr_w, mag, sh, yd, n_iter, T, **c)
     assert np.isfinite(ref).all()
     for g in gs[1:]:
-        h, rep = _run(g, lr_h, lr_w, mag, sh, yd, n_iter, T, **c)
-        np.testing.assert_array_equal(rep["trace"], rref["trace"], err_msg=f"g={g}: trace differs")
-        np.testing.assert_array_equal(h, ref, err_msg=f"g={g}: image differs")
-        assert rep["accepted"] == rref["accepted"]
+        for transport in ("peer", "copies"):
+            h, rep = _run(g, lr_h, lr_w, mag, sh, yd, n_iter, T, transport=transport, **c)
+            np.testing.assert_array_equal(rep["trace"], rref["trace"], err_msg=f"g={g} {transport}: trace differs")
+            np.testing.assert_array_equal(h, ref, err_msg=f"g={g} {transport}: image differs")
+            assert rep["accepted"] == rref["accepted"]
 
 
 def test_det_meets_oracle_bar_and_matches_default_sums(orc):
@@ -106,10 +111,10 @@ def test_det_repeatable_and_config_errors():
     with pytest.raises(flmisr.FlmisrError, match="det_rows needs the streaming path"):
         flmisr.Plan(k=3, lr_h=21, lr_w=20, shifts=np.array([[0, 0], [0.5, 0.5], [0.3, 0.1]]),
                     psf=synth.gaussian_psf(), mag=2, det_rows=6)
-    # the per-phase band transport (device copies / NCCL) sums in fp64: refused in det mode
+    # bands of different det_rows are not one configuration
     pls = [flmisr.Plan(k=4, lr_h=lr_h, lr_w=lr_w, shifts=sh, psf=synth.gaussian_psf(), mag=2, rank=r, world=2,
-                       virtual=True, det_rows=6) for r in range(2)]
-    with pytest.raises(flmisr.FlmisrError, match="reconstruct_virtual_peer"):
+                       virtual=True, det_rows=6 if r == 0 else 9) for r in range(2)]
+    with pytest.raises(flmisr.FlmisrError, match="one configuration"):
         flmisr.reconstruct_virtual(pls, yd)
     for p in pls:
         p.destroy()
