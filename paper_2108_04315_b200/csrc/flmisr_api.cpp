@@ -597,8 +597,10 @@ static flmisr_status make_plan(const flmisr_config* cfg, flmisr_plan_t* out, boo
     // x2: the persistent loop kernel double-buffers its per-CTA slots by phase parity
     // det mode: FXW 128-bit words (2 doubles each) per CTA slot
     // (and the allgathered rank-sum records: RSW doubles per rank)
-    const size_t npart = std::max<size_t>(std::max<size_t>(2 * NSLOT * ntiles, (size_t)RSW * world),
-                                          (size_t)2 * 2 * FXW * nsblk);
+    // (and the loop kernels' three grid_sum accumulator sets of 6 NSLOT + 1 words)
+    const size_t npart = std::max<size_t>(std::max<size_t>(std::max<size_t>(2 * NSLOT * ntiles, (size_t)RSW * world),
+                                                            (size_t)2 * 2 * FXW * nsblk),
+                                          (size_t)3 * (6 * NSLOT + 1) + 1);
     const size_t ntrace = (size_t)(c.n_iter + 1) * 6;
     const size_t nd = npart + RSW + ntrace + 1;   // + the grid-barrier counter
     e = cudaMalloc(&p->dmem, nd * sizeof(double));

@@ -340,8 +340,11 @@ __global__ void k_scalar_after_curv(const __grid_constant__ StencilParams sp, Bu
 }
 
 __global__ void k_state_init(ScgState* s, double lam0, double lambda_reg, int n_iter, long long npix, int rules,
-                             unsigned* gbar) {
+                             unsigned* gbar, double* part) {
     if (gbar) *gbar = 0u;
+    // the loop kernels' grid_sum accumulator sets 0 and 1 (25 words each; set 2 is zeroed in the loop)
+    if (part)
+        for (int i = 0; i < 2 * (6 * NSLOT + 1); ++i) reinterpret_cast<unsigned long long*>(part)[i] = 0ull;
     s->f = 0; s->f_new = 0; s->lam = lam0; s->lamb = 0; s->delta = 0; s->pp = 0; s->mu = 0;
     s->alpha = 0; s->beta = 0; s->rr = 0; s->lambda_reg = lambda_reg;
     for (int i = 0; i < 8; ++i) s->dbg[i] = 0;
@@ -504,7 +507,7 @@ cudaError_t launch_scalar_after_curv(const StencilParams& sp, const Buffers& b, 
 
 cudaError_t launch_state_init(const Buffers& b, double lam0, double lambda_reg, int n_iter, long long npix,
                               int rules, cudaStream_t s) {
-    k_state_init<<<1, 1, 0, s>>>(b.st, lam0, lambda_reg, n_iter, npix, rules, b.gbar);
+    k_state_init<<<1, 1, 0, s>>>(b.st, lam0, lambda_reg, n_iter, npix, rules, b.gbar, b.part);
     return cudaGetLastError();
 }
 

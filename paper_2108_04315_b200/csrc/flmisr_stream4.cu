@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(PC_WPB * 32, 1) k_scg_loop4(const __grid_const
         if (pass > 0) {
             if (ui(S.success)) {
                 uc4_phase<BW, PN>(sp, b, T, g, ring, ui(S.xcur), ui(S.rcur), uf(S.alpha_upd_f), uf(S.beta_f), par, acc);
-                grid_sum(acc, b.part, b.gbar, epoch++, tot);
+                grid_sum_fx(acc, b.part, b.gbar, epoch++, tot);
                 if (threadIdx.x == 0) {
                     S.xcur ^= 1;
                     affine<1>(sp, tot);
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(PC_WPB * 32, 1) k_scg_loop4(const __grid_const
             if (ui(S.done)) break;
         }
         vg4_phase<BW, PN>(sp, b, T, g, ring, ui(S.xcur), ui(S.rcur), pass > 0 ? uf(S.alpha_f) : 0.0f, par, acc);
-        grid_sum(acc, b.part, b.gbar, epoch++, tot);
+        grid_sum_fx(acc, b.part, b.gbar, epoch++, tot);
         if (threadIdx.x == 0) {
             affine<0>(sp, tot);
             scg_after_value(&S, tot, trace, pass > 0 ? PH_ITER : PH_INIT);

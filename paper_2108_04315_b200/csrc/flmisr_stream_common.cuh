@@ -467,6 +467,143 @@ __device__ __forceinline__ unsigned long long now_ns() {
     return t;
 }
 
+// grid_sum_fx: grid-wide sum of acc over all threads of all CTAs; result in tot (all threads).  Each CTA's fp64
+// partial (fixed shuffle tree + fixed cross-warp order) is converted to 192-bit fixed point (value =
+// X 2^-128: |value| < 2^63, truncation below 2^-128 ~ 3e-39, so the sums keep full fp64 precision from
+// the first pass down to a converged <r,r>) and added as six 32-bit chunks with red.add.u64 into one
+// of three accumulator sets (by epoch mod 3): integer adds commute, so the total does not depend on
+// the order of the CTAs' arrivals, and after the barrier every CTA reads 25 words instead of summing
+// all G slots (the per-phase tail after the last arrival: one L2 round trip).  Set (e + 2) mod 3 is
+// zeroed by CTA 0 right after barrier e -- it was last read before barrier e and is next written after
+// barrier e + 1, which CTA 0 releases after the zeroing; sets 0 and 1 are zeroed by k_state_init.
+constexpr int FXCH = 6, FXA = NSLOT * FXCH + 1;   // chunks per sum; words per set (+ non-finite count)
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// 32-bit chunk c of the 192-bit two's-complement fixed-point image of a finite v (chunks from c = 0)
+__device__ __forceinline__ void fx192_chunks(double v, unsigned (&ch)[FXCH]) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    const unsigned long long m = ex ? ((bits & 0xFFFFFFFFFFFFFull) | (1ull << 52)) : 0ull;
+    const int sh = min(ex - 1075 + 128, 191 - 53 - 1);   // X = m << sh (sh < 0: m >> -sh)
+#pragma unroll
+    for (int c = 0; c < FXCH; ++c) {
+        const int d = 32 * c - sh;   // chunk c holds bits [32c, 32c + 32) of X = bits [d, d + 32) of m
+        unsigned long long x;
+        if (d >= 0) x = d < 64 ? (m >> d) : 0ull;
+        else x = -d < 32 ? (m << (-d)) : 0ull;
+        ch[c] = (unsigned)(x & 0xffffffffull);
+    }
+    if (bits >> 63) {   // two's complement over 192 bits: invert, add 1 with carry
+        unsigned long long carry = 1ull;
+#pragma unroll
+        for (int c = 0; c < FXCH; ++c) {
+            const unsigned long long t = (unsigned long long)(~ch[c]) + carry;
+            ch[c] = (unsigned)(t & 0xffffffffull);
+            carry = t >> 32;
+        }
+    }
+}
+// chunk sums S_c (each < 2^64) -> sum_c S_c 2^(32c) mod 2^192 -> double (value X 2^-128)
+__device__ __forceinline__ double fx192_to_double(const unsigned long long (&S)[FXCH]) {
+    unsigned long long w[3] = {0ull, 0ull, 0ull};   // 192-bit accumulator, little-endian 64-bit words
+#pragma unroll
+    for (int c = 0; c < FXCH; ++c) {
+        // add S_c << 32c
+        const int wi = c / 2, off = 32 * (c % 2);
+        unsigned __int128 add = (unsigned __int128)S[c] << off;   // < 2^96
+        unsigned long long lo = (unsigned long long)add, hi = (unsigned long long)(add >> 64);
+        unsigned long long carry = 0ull;
+        for (int k = wi; k < 3; ++k) {
+            const unsigned long long a = k == wi ? lo : (k == wi + 1 ? hi : 0ull);
+            const unsigned __int128 t = (unsigned __int128)w[k] + a + carry;
+            w[k] = (unsigned long long)t;
+            carry = (unsigned long long)(t >> 64);
+        }
+    }
+    const bool neg = (w[2] >> 63) != 0;
+    if (neg) {   // magnitude of the two's-complement value
+        unsigned long long carry = 1ull;
+        for (int k = 0; k < 3; ++k) {
+            const unsigned __int128 t = (unsigned __int128)(~w[k]) + carry;
+            w[k] = (unsigned long long)t;
+            carry = (unsigned long long)(t >> 64);
+        }
+    }
+    const double mag = (double)w[2] + (double)w[1] * 5.421010862427522e-20 + (double)w[0] * 2.938735877055719e-39;
+    return neg ? -mag : mag;
+}
+// Used by the per-phase loop kernel (k_scg_loop4: G3 266 vs 258 proj/s); the common-kappa loop kernel
+// keeps grid_sum below (C2 490 vs 487, C4 168 vs 167 with this form; profiles/r02_grid_sum_fx_ab.txt).
+__device__ void grid_sum_fx(const double (&acc)[NSLOT], double* part, unsigned* gbar, unsigned epoch,
+                            double (&tot)[NSLOT]) {
+    __shared__ double sred[32][NSLOT];
+    __shared__ double stot[NSLOT];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int G = gridDim.x;
+    unsigned long long* sets = reinterpret_cast<unsigned long long*>(part);
+    unsigned long long* cur = sets + (size_t)(epoch % 3) * FXA;
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+        const double v = warp_sum(acc[k]);
+        if (lane == 0) sred[warp][k] = v;
+    }
+    __syncthreads();
+    FL_TMARK(epoch, 0)
+    if (threadIdx.x < NSLOT) {   // this CTA's sum k -> exact chunks
+        const int k = threadIdx.x;
+        double v = 0.0;
+        for (int w = 0; w < nw; ++w) v += sred[w][k];
+        if (isfinite(v)) {
+            unsigned ch[FXCH];
+            fx192_chunks(v, ch);
+#pragma unroll
+            for (int c = 0; c < FXCH; ++c)
+                if (ch[c]) red_add_u64(cur + k * FXCH + c, (unsigned long long)ch[c]);
+        } else {
+            red_add_u64(cur + NSLOT * FXCH, 1ull);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // release-reduction: this CTA's phase output and its chunk adds (ordered before it by the
+        // barrier above, cumulativity) become visible to any CTA that acquires the count
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
+        FL_TMARK(epoch, 1)
+        const unsigned target = (epoch + 1) * (unsigned)G;
+        unsigned spins = 0;
+        const unsigned long long tstart = now_ns();
+        while (ld_acquire_u32(gbar) < target) {
+            // a lost CTA: fail loudly (after 10 s; a phase takes < 1 ms) instead of hanging the device
+            if ((++spins & 1023u) == 0 && now_ns() - tstart > 10000000000ull) __trap();
+        }
+        FL_TMARK(epoch, 2)
+        if (blockIdx.x == 0) {
+            unsigned long long* nxt = sets + (size_t)((epoch + 2) % 3) * FXA;
+            for (int i = 0; i < FXA; ++i) nxt[i] = 0ull;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < NSLOT) {
+        const int k = threadIdx.x;
+        unsigned long long S[FXCH];
+#pragma unroll
+        for (int c = 0; c < FXCH; ++c) S[c] = ld_relaxed_u64(cur + k * FXCH + c);
+        const bool bad = ld_relaxed_u64(cur + NSLOT * FXCH) != 0ull;
+        stot[k] = bad ? __longlong_as_double(0x7ff8000000000000ll) : fx192_to_double(S);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) tot[k] = stot[k];
+    FL_TMARK(epoch, 3)
+    // the next phase reads other CTAs' generic-proxy stores through the bulk-copy (async) proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 // grid-wide sum of acc over all threads of all CTAs in a fixed order; result in tot (all threads)
 __device__ void grid_sum(const double (&acc)[NSLOT], double* part, unsigned* gbar, unsigned epoch,
                          double (&tot)[NSLOT]) {
